@@ -1,0 +1,417 @@
+/*
+ * oracle.c -- plain, slow, obviously-correct CPU reference for the dGN
+ * evaluation hot path of Tensor Fox (arxiv 2110.05997, PAPER.md).
+ *
+ * TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference leg may load this library.
+ * It shares no code, header, table or helper with the CUDA path
+ * (paper_2110_05997_b200/csrc) and never calls it.
+ *
+ * Conventions (PAPER.md:857-872 Alg. Unfolding; 1466-1473 vec/w layout):
+ *   T[i + I*(j + J*k)]   first index fastest; frontal slice k contiguous.
+ *   A[i + I*r], B[j + J*r], C[k + K*r]   column-major factor matrices.
+ *   w = [vec A; vec B; vec C], length n = R*(I+J+K).
+ *
+ * Arithmetic: every accumulation and every intermediate is carried in x86
+ * 80-bit `long double` (64-bit significand), so the oracle's own rounding
+ * (~1e-19 relative per operation) is far below the 1e-10 parity bar and any
+ * parity gap is attributable to the fp64 GPU path (R15).
+ *
+ * Pinning status of every function is listed in DESIGN.md §3 and tested in
+ * tests/test_oracle_pins.py.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <math.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+typedef long double ld;
+
+static int clamp_threads(int nthreads) {
+#ifdef _OPENMP
+  if (nthreads <= 0) nthreads = omp_get_max_threads();
+  return nthreads;
+#else
+  (void)nthreads;
+  return 1;
+#endif
+}
+
+/*
+ * oracle_eval: F(w) and grad F(w) by their definitions.
+ *   residual  f_ijk = t_ijk - sum_r a_ir b_jr c_kr        (eq. residual_function)
+ *   objective F = 1/2 sum_ijk f_ijk^2                      (eq. error_function)
+ *   gradient  grad F = J_f^T f                             (Lemma gradF)
+ *             with d f_ijk / d a_ir = -b_jr c_kr, etc.     (Lemma partialf)
+ * One pass over the entries in storage order; slices k are split over
+ * OpenMP threads (static schedule), per-thread partial sums of gA, gB and F
+ * are combined in thread order, so the result is deterministic for a fixed
+ * thread count. gC row k is owned by the thread that owns slice k.
+ */
+int oracle_eval(int64_t I, int64_t J, int64_t K, int64_t R, const double *T,
+                const double *A, const double *B, const double *C,
+                double *f_out, double *gA, double *gB, double *gC, int nthreads) {
+  if (I < 1 || J < 1 || K < 1 || R < 1 || !T || !A || !B || !C) return 1;
+  int nt = clamp_threads(nthreads);
+  ld *pA = (ld *)calloc((size_t)nt * I * R, sizeof(ld));
+  ld *pB = (ld *)calloc((size_t)nt * J * R, sizeof(ld));
+  ld *pF = (ld *)calloc((size_t)nt, sizeof(ld));
+  ld *gCl = (ld *)calloc((size_t)K * R, sizeof(ld));
+  if (!pA || !pB || !pF || !gCl) { free(pA); free(pB); free(pF); free(gCl); return 6; }
+
+#pragma omp parallel num_threads(nt)
+  {
+#ifdef _OPENMP
+    int tid = omp_get_thread_num();
+#else
+    int tid = 0;
+#endif
+    ld *myA = pA + (size_t)tid * I * R;
+    ld *myB = pB + (size_t)tid * J * R;
+    ld myF = 0.0L;
+    ld *bc = (ld *)malloc(sizeof(ld) * R);
+#pragma omp for schedule(static)
+    for (int64_t k = 0; k < K; ++k) {
+      for (int64_t j = 0; j < J; ++j) {
+        for (int64_t r = 0; r < R; ++r) bc[r] = (ld)B[j + J * r] * (ld)C[k + K * r];
+        for (int64_t i = 0; i < I; ++i) {
+          /* residual f_ijk (eq. residual_function) */
+          ld x = 0.0L;
+          for (int64_t r = 0; r < R; ++r) x += (ld)A[i + I * r] * bc[r];
+          ld e = (ld)T[i + I * (j + J * k)] - x;
+          myF += e * e;
+          /* J_f^T f, column by column (Lemma partialf) */
+          for (int64_t r = 0; r < R; ++r) {
+            myA[i + I * r] -= e * bc[r];
+            myB[j + J * r] -= e * (ld)A[i + I * r] * (ld)C[k + K * r];
+            gCl[k + K * r] -= e * (ld)A[i + I * r] * (ld)B[j + J * r];
+          }
+        }
+      }
+    }
+    pF[tid] = myF;
+    free(bc);
+  }
+  ld F = 0.0L;
+  for (int t = 0; t < nt; ++t) F += pF[t];
+  *f_out = (double)(0.5L * F);
+  for (int64_t q = 0; q < I * R; ++q) {
+    ld s = 0.0L;
+    for (int t = 0; t < nt; ++t) s += pA[(size_t)t * I * R + q];
+    gA[q] = (double)s;
+  }
+  for (int64_t q = 0; q < J * R; ++q) {
+    ld s = 0.0L;
+    for (int t = 0; t < nt; ++t) s += pB[(size_t)t * J * R + q];
+    gB[q] = (double)s;
+  }
+  for (int64_t q = 0; q < K * R; ++q) gC[q] = (double)gCl[q];
+  free(pA); free(pB); free(pF); free(gCl);
+  return 0;
+}
+
+/*
+ * oracle_slice_eval: the same definitions restricted to the entries that
+ * share one fixed index, i.e. one slice of T (PAPER.md:401-416 slice defs;
+ * 579-586 slice formulas). For the fixed index with factor row x (length R)
+ * and the slice S (n1 x n2, column-major, S[a + n1*b]) with the other two
+ * factor matrices X (n1 x R) and Y (n2 x R):
+ *   e_ab = s_ab - sum_r x_r X_ar Y_br,  f = 1/2 sum e_ab^2,  g_r = -sum_ab e_ab X_ar Y_br.
+ * g is the gradient row of the fixed index (row i of dF/dA for a horizontal
+ * slice, row j of dF/dB for a lateral one, row k of dF/dC for a frontal one)
+ * and f is that slice's share of F. Used for sampled checks at full size.
+ */
+int oracle_slice_eval(int64_t n1, int64_t n2, int64_t R, const double *S, int64_t lds1, int64_t lds2,
+                      const double *x, const double *X, int64_t ldX, const double *Y, int64_t ldY,
+                      double *f_out, double *g) {
+  /* S element (a,b) lives at S[a*lds1 + b*lds2]; X(a,r) at X[a + ldX*r]; Y(b,r) at Y[b + ldY*r] */
+  if (n1 < 1 || n2 < 1 || R < 1) return 1;
+  ld *gl = (ld *)calloc((size_t)R, sizeof(ld));
+  ld *xy = (ld *)malloc(sizeof(ld) * R);
+  ld F = 0.0L;
+  for (int64_t b = 0; b < n2; ++b) {
+    for (int64_t r = 0; r < R; ++r) xy[r] = (ld)x[r] * (ld)Y[b + ldY * r];
+    for (int64_t a = 0; a < n1; ++a) {
+      ld v = 0.0L;
+      for (int64_t r = 0; r < R; ++r) v += (ld)X[a + ldX * r] * xy[r];
+      ld e = (ld)S[a * lds1 + b * lds2] - v;
+      F += e * e;
+      for (int64_t r = 0; r < R; ++r) gl[r] -= e * (ld)X[a + ldX * r] * (ld)Y[b + ldY * r];
+    }
+  }
+  *f_out = (double)(0.5L * F);
+  for (int64_t r = 0; r < R; ++r) g[r] = (double)gl[r];
+  free(gl); free(xy);
+  return 0;
+}
+
+/*
+ * oracle_gn_matvec_plain: y = (J_f^T J_f + lambda I) v without Grams.
+ *   u = J_f v with (J_f v)_ijk = -sum_r (vA_ir b_jr c_kr + a_ir vB_jr c_kr + a_ir b_jr vC_kr)
+ *   (Lemma partialf), then y = J_f^T u + lambda v by the
+ *   same column formulas as in oracle_eval. O(IJKR) per call.
+ */
+int oracle_gn_matvec_plain(int64_t I, int64_t J, int64_t K, int64_t R,
+                           const double *A, const double *B, const double *C,
+                           const double *v, double lambda, double *y, int nthreads) {
+  if (I < 1 || J < 1 || K < 1 || R < 1) return 1;
+  const double *vA = v, *vB = v + I * R, *vC = v + (I + J) * R;
+  int nt = clamp_threads(nthreads);
+  ld *pA = (ld *)calloc((size_t)nt * I * R, sizeof(ld));
+  ld *pB = (ld *)calloc((size_t)nt * J * R, sizeof(ld));
+  ld *yC = (ld *)calloc((size_t)K * R, sizeof(ld));
+#pragma omp parallel num_threads(nt)
+  {
+#ifdef _OPENMP
+    int tid = omp_get_thread_num();
+#else
+    int tid = 0;
+#endif
+    ld *myA = pA + (size_t)tid * I * R;
+    ld *myB = pB + (size_t)tid * J * R;
+#pragma omp for schedule(static)
+    for (int64_t k = 0; k < K; ++k)
+      for (int64_t j = 0; j < J; ++j)
+        for (int64_t i = 0; i < I; ++i) {
+          ld u = 0.0L;
+          for (int64_t r = 0; r < R; ++r) {
+            ld a = A[i + I * r], b = B[j + J * r], c = C[k + K * r];
+            u -= (ld)vA[i + I * r] * b * c + a * (ld)vB[j + J * r] * c + a * b * (ld)vC[k + K * r];
+          }
+          for (int64_t r = 0; r < R; ++r) {
+            ld a = A[i + I * r], b = B[j + J * r], c = C[k + K * r];
+            myA[i + I * r] -= u * b * c;
+            myB[j + J * r] -= u * a * c;
+            yC[k + K * r] -= u * a * b;
+          }
+        }
+  }
+  for (int64_t q = 0; q < I * R; ++q) {
+    ld s = 0.0L;
+    for (int t = 0; t < nt; ++t) s += pA[(size_t)t * I * R + q];
+    y[q] = (double)(s + (ld)lambda * (ld)vA[q]);
+  }
+  for (int64_t q = 0; q < J * R; ++q) {
+    ld s = 0.0L;
+    for (int t = 0; t < nt; ++t) s += pB[(size_t)t * J * R + q];
+    y[I * R + q] = (double)(s + (ld)lambda * (ld)vB[q]);
+  }
+  for (int64_t q = 0; q < K * R; ++q) y[(I + J) * R + q] = (double)(yC[q] + (ld)lambda * (ld)vC[q]);
+  free(pA); free(pB); free(yC);
+  return 0;
+}
+
+/* pi^(l) = W^(l)T W^(l). grams = [pi_A | pi_B | pi_C], each R x R column-major. */
+static void gram_ld(int64_t n, int64_t R, const double *W, ld *out) {
+  for (int64_t r = 0; r < R; ++r)
+    for (int64_t s = 0; s < R; ++s) {
+      ld acc = 0.0L;
+      for (int64_t a = 0; a < n; ++a) acc += (ld)W[a + n * r] * (ld)W[a + n * s];
+      out[r + R * s] = acc;
+    }
+}
+
+int oracle_grams(int64_t I, int64_t J, int64_t K, int64_t R, const double *A, const double *B,
+                 const double *C, double *grams) {
+  ld *g = (ld *)malloc(sizeof(ld) * 3 * R * R);
+  gram_ld(I, R, A, g);
+  gram_ld(J, R, B, g + R * R);
+  gram_ld(K, R, C, g + 2 * R * R);
+  for (int64_t q = 0; q < 3 * R * R; ++q) grams[q] = (double)g[q];
+  free(g);
+  return 0;
+}
+
+/*
+ * Hadamard chains for L = 3:
+ *   Pi^(1) = pi^(2) * pi^(3),  Pi^(2) = pi^(1) * pi^(3),  Pi^(3) = pi^(1) * pi^(2);
+ *   Pi^(1,2) = pi^(3),  Pi^(1,3) = pi^(2),  Pi^(2,3) = pi^(1)  (product over l not in {l', l''}).
+ * out = [Pi1 | Pi2 | Pi3 | Pi12 | Pi13 | Pi23].
+ */
+static void pi_ld(int64_t R, const ld *g, ld *out) {
+  const ld *pA = g, *pB = g + R * R, *pC = g + 2 * R * R;
+  for (int64_t q = 0; q < R * R; ++q) {
+    out[q] = pB[q] * pC[q];
+    out[R * R + q] = pA[q] * pC[q];
+    out[2 * R * R + q] = pA[q] * pB[q];
+    out[3 * R * R + q] = pC[q];
+    out[4 * R * R + q] = pB[q];
+    out[5 * R * R + q] = pA[q];
+  }
+}
+
+int oracle_pi(int64_t R, const double *grams, double *pi) {
+  ld *g = (ld *)malloc(sizeof(ld) * 3 * R * R), *p = (ld *)malloc(sizeof(ld) * 6 * R * R);
+  for (int64_t q = 0; q < 3 * R * R; ++q) g[q] = grams[q];
+  pi_ld(R, g, p);
+  for (int64_t q = 0; q < 6 * R * R; ++q) pi[q] = (double)p[q];
+  free(g); free(p);
+  return 0;
+}
+
+/*
+ * Thm Hv: for each mode l',
+ *   Y^(l') = V^(l') Pi^(l') + sum_{l'' != l'} W^(l') (Pi^(l',l'') * (V^(l'')T W^(l'')))
+ * then y = vec(Y) + lambda v. Written with explicit loops in the theorem's order.
+ */
+static void hv_ld(int64_t I, int64_t J, int64_t K, int64_t R, const double *A, const double *B,
+                  const double *C, const ld *v, ld lambda, ld *y) {
+  const int64_t dims[3] = {I, J, K};
+  const double *W[3] = {A, B, C};
+  int64_t off[3] = {0, I * R, (I + J) * R};
+  ld *g = (ld *)malloc(sizeof(ld) * 3 * R * R), *pi = (ld *)malloc(sizeof(ld) * 6 * R * R);
+  gram_ld(I, R, A, g);
+  gram_ld(J, R, B, g + R * R);
+  gram_ld(K, R, C, g + 2 * R * R);
+  pi_ld(R, g, pi);
+  /* index of Pi^(l',l'') in pi[] for l' != l'' */
+  int pair_idx[3][3] = {{-1, 3, 4}, {3, -1, 5}, {4, 5, -1}};
+  ld *M = (ld *)malloc(sizeof(ld) * R * R);
+  for (int l1 = 0; l1 < 3; ++l1) {
+    int64_t n1 = dims[l1];
+    const ld *P1 = pi + (int64_t)l1 * R * R;
+    const ld *V1 = v + off[l1];
+    ld *Y = y + off[l1];
+    /* Case 2: V^(l') Pi^(l') */
+    for (int64_t a = 0; a < n1; ++a)
+      for (int64_t s = 0; s < R; ++s) {
+        ld acc = 0.0L;
+        for (int64_t r = 0; r < R; ++r) acc += V1[a + n1 * r] * P1[r + R * s];
+        Y[a + n1 * s] = acc + lambda * V1[a + n1 * s];
+      }
+    /* Case 1: W^(l') (Pi^(l',l'') * (V^(l'')T W^(l''))) */
+    for (int l2 = 0; l2 < 3; ++l2) {
+      if (l2 == l1) continue;
+      int64_t n2 = dims[l2];
+      const ld *V2 = v + off[l2];
+      const double *W2 = W[l2];
+      const ld *P12 = pi + (int64_t)pair_idx[l1][l2] * R * R;
+      for (int64_t r = 0; r < R; ++r)
+        for (int64_t s = 0; s < R; ++s) {
+          ld acc = 0.0L; /* (V2^T W2)_{rs} */
+          for (int64_t b = 0; b < n2; ++b) acc += V2[b + n2 * r] * (ld)W2[b + n2 * s];
+          M[r + R * s] = P12[r + R * s] * acc;
+        }
+      const double *W1 = W[l1];
+      for (int64_t a = 0; a < n1; ++a)
+        for (int64_t s = 0; s < R; ++s) {
+          ld acc = 0.0L;
+          for (int64_t r = 0; r < R; ++r) acc += (ld)W1[a + n1 * r] * M[r + R * s];
+          Y[a + n1 * s] += acc;
+        }
+    }
+  }
+  free(g); free(pi); free(M);
+}
+
+int oracle_gn_matvec_hv(int64_t I, int64_t J, int64_t K, int64_t R, const double *A, const double *B,
+                        const double *C, const double *v, double lambda, double *y) {
+  int64_t n = R * (I + J + K);
+  ld *vl = (ld *)malloc(sizeof(ld) * n), *yl = (ld *)malloc(sizeof(ld) * n);
+  for (int64_t q = 0; q < n; ++q) vl[q] = v[q];
+  hv_ld(I, J, K, R, A, B, C, vl, (ld)lambda, yl);
+  for (int64_t q = 0; q < n; ++q) y[q] = (double)yl[q];
+  free(vl); free(yl);
+  return 0;
+}
+
+/*
+ * Diagonal of J_f^T J_f: entry (l, a, r) is the squared norm of the Jacobian
+ * column d f / d w^(l)_{a r}, whose nonzeros are -prod_{l != l'} w (Lemma
+ * partialf), i.e. prod_{l != l'} ||w_r^(l)||^2 (= Pi^(l)_rr).
+ */
+static void jtj_diag_ld(int64_t I, int64_t J, int64_t K, int64_t R, const double *A, const double *B,
+                        const double *C, ld *d) {
+  const int64_t dims[3] = {I, J, K};
+  const double *W[3] = {A, B, C};
+  ld *nrm = (ld *)malloc(sizeof(ld) * 3 * R);
+  for (int l = 0; l < 3; ++l)
+    for (int64_t r = 0; r < R; ++r) {
+      ld s = 0.0L;
+      for (int64_t a = 0; a < dims[l]; ++a) s += (ld)W[l][a + dims[l] * r] * (ld)W[l][a + dims[l] * r];
+      nrm[l * R + r] = s;
+    }
+  const int64_t off[3] = {0, I * R, (I + J) * R};
+  for (int l = 0; l < 3; ++l)
+    for (int64_t r = 0; r < R; ++r) {
+      ld p = 1.0L;
+      for (int m = 0; m < 3; ++m) if (m != l) p *= nrm[m * R + r];
+      for (int64_t a = 0; a < dims[l]; ++a) d[off[l] + a + dims[l] * r] = p;
+    }
+  free(nrm);
+}
+
+int oracle_jtj_diag(int64_t I, int64_t J, int64_t K, int64_t R, const double *A, const double *B,
+                    const double *C, double *d) {
+  int64_t n = R * (I + J + K);
+  ld *dl = (ld *)malloc(sizeof(ld) * n);
+  jtj_diag_ld(I, J, K, R, A, B, C, dl);
+  for (int64_t q = 0; q < n; ++q) d[q] = (double)dl[q];
+  free(dl);
+  return 0;
+}
+
+/*
+ * Alg. CG-dGN with D = I (damping lambda*I, DESIGN.md
+ * reading R2) and M = I (jacobi = 0) or M = diag(J^T J) + lambda I (jacobi = 1,
+ * PAPER.md:2655-2660, 4549-4567):
+ *   B = M^{-1/2} (J^T J + lambda I) M^{-1/2};  x0 = 0;  r0 = M^{-1/2} rhs;  p0 = r0
+ *   for i = 1..maxiter:
+ *     z = B p;  alpha = ||r||^2 / <p, z>;  x += alpha p;  r -= alpha z;
+ *     eps = ||r||^2;  beta = eps / ||r_old||^2;  p = r + beta p;  if eps < tol: break
+ * Returns x in w-coordinates, x = M^{-1/2} x_hat (reading R3).
+ * x_hist (nullable): maxiter*n, the iterate after each iteration (w-coordinates);
+ * r2/alpha/beta (nullable): per-iteration ||r||^2, alpha, beta. *iters = iterations done.
+ * Returns 5 if alpha or beta is not finite.
+ */
+int oracle_cg(int64_t I, int64_t J, int64_t K, int64_t R, const double *A, const double *B,
+              const double *C, const double *rhs, double lambda, int maxiter, double tol, int jacobi,
+              double *x_out, double *x_hist, double *r2_hist, double *alpha_hist, double *beta_hist,
+              int *iters) {
+  int64_t n = R * (I + J + K);
+  ld *x = (ld *)calloc(n, sizeof(ld)), *r = (ld *)malloc(sizeof(ld) * n), *p = (ld *)malloc(sizeof(ld) * n);
+  ld *z = (ld *)malloc(sizeof(ld) * n), *tmp = (ld *)malloc(sizeof(ld) * n), *minv = (ld *)malloc(sizeof(ld) * n);
+  int status = 0;
+  if (jacobi) {
+    jtj_diag_ld(I, J, K, R, A, B, C, minv);
+    for (int64_t q = 0; q < n; ++q) minv[q] = 1.0L / sqrtl(minv[q] + (ld)lambda);
+  } else {
+    for (int64_t q = 0; q < n; ++q) minv[q] = 1.0L;
+  }
+  ld rr = 0.0L;
+  for (int64_t q = 0; q < n; ++q) { r[q] = minv[q] * (ld)rhs[q]; p[q] = r[q]; rr += r[q] * r[q]; }
+  int it = 0;
+  for (int i = 1; i <= maxiter; ++i) {
+    /* z = B p in three steps */
+    for (int64_t q = 0; q < n; ++q) tmp[q] = minv[q] * p[q];
+    hv_ld(I, J, K, R, A, B, C, tmp, (ld)lambda, z);
+    for (int64_t q = 0; q < n; ++q) z[q] *= minv[q];
+    ld pz = 0.0L;
+    for (int64_t q = 0; q < n; ++q) pz += p[q] * z[q];
+    ld alpha = rr / pz;
+    if (!isfinite((double)alpha)) { status = 5; break; }
+    ld rr_new = 0.0L;
+    for (int64_t q = 0; q < n; ++q) {
+      x[q] += alpha * p[q];
+      r[q] -= alpha * z[q];
+      rr_new += r[q] * r[q];
+    }
+    ld beta = rr_new / rr;
+    if (!isfinite((double)beta)) { status = 5; break; }
+    for (int64_t q = 0; q < n; ++q) p[q] = r[q] + beta * p[q];
+    rr = rr_new;
+    it = i;
+    if (x_hist) for (int64_t q = 0; q < n; ++q) x_hist[(int64_t)(i - 1) * n + q] = (double)(minv[q] * x[q]);
+    if (r2_hist) r2_hist[i - 1] = (double)rr_new;
+    if (alpha_hist) alpha_hist[i - 1] = (double)alpha;
+    if (beta_hist) beta_hist[i - 1] = (double)beta;
+    if (rr_new < (ld)tol) break;
+  }
+  for (int64_t q = 0; q < n; ++q) x_out[q] = (double)(minv[q] * x[q]);
+  if (iters) *iters = it;
+  free(x); free(r); free(p); free(z); free(tmp); free(minv);
+  return status;
+}

@@ -1,0 +1,126 @@
+// Microbenchmarks for the roofline denominators MEASURED_PEAKS.json lacks:
+// FP64 tensor-core (DMMA via mma.sync.m8n8k4.f64), FP64 FMA (DFMA) and read-only HBM bandwidth.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/peaks tools/peaks.cu
+#include <cstdio>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { fprintf(stderr, "%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e)); exit(1); } } while (0)
+
+template <int NACC>
+__global__ void k_dmma(double* out, int iters) {
+  double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+  double c[NACC][2];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) { c[i][0] = 0.0; c[i][1] = 0.0; }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < NACC; ++i)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.678) out[0] = s;
+}
+
+template <int NACC>
+__global__ void k_dfma(double* out, int iters) {
+  double a = 1.0 + threadIdx.x * 1e-12, b = 1e-9;
+  double x[NACC];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) x[i] = i * 1e-3;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) x[i] = fma(x[i], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) s += x[i];
+  if (s == 12345.678) out[0] = s;
+}
+
+__global__ void k_read(const double2* __restrict__ p, size_t n, double* out) {
+  double s = 0.0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    double2 v = __ldcs(p + i);
+    s += v.x + v.y;
+  }
+  if (s == 12345.678) out[0] = s;
+}
+
+int main(int argc, char** argv) {
+  int dev = 0; CK(cudaSetDevice(dev));
+  cudaDeviceProp pr; CK(cudaGetDeviceProperties(&pr, dev));
+  int nsm = pr.multiProcessorCount;
+  double* out; CK(cudaMalloc(&out, 8));
+  cudaEvent_t e0, e1; CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+  float ms;
+  printf("{\"gpu\": \"%s\", \"sms\": %d", pr.name, nsm);
+  // DMMA sweep over warps per SM and accumulator chains
+  double best_dmma = 0;
+  for (int tpb : {128, 256, 512, 1024}) {
+    for (int blocks_per_sm : {1, 2}) {
+      int iters = 4000;
+      dim3 g(nsm * blocks_per_sm), b(tpb);
+      k_dmma<8><<<g, b>>>(out, 10); CK(cudaDeviceSynchronize());
+      CK(cudaEventRecord(e0));
+      k_dmma<8><<<g, b>>>(out, iters);
+      CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1)); CK(cudaEventElapsedTime(&ms, e0, e1));
+      double flops = 2.0 * 256 * 8 * (double)iters * (g.x * (tpb / 32));
+      double tf = flops / (ms * 1e-3) / 1e12;
+      printf(", \"dmma_tpb%d_bps%d_tflops\": %.2f", tpb, blocks_per_sm, tf);
+      if (tf > best_dmma) best_dmma = tf;
+    }
+  }
+  // DMMA single-warp-per-SMSP chain latency probe: 1 acc chain, 4 warps per SM
+  {
+    int iters = 20000; dim3 g(nsm), b(128);
+    k_dmma<1><<<g, b>>>(out, 10); CK(cudaDeviceSynchronize());
+    CK(cudaEventRecord(e0)); k_dmma<1><<<g, b>>>(out, iters); CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    double ns_per = ms * 1e6 / iters;
+    printf(", \"dmma_dep_chain_ns\": %.3f", ns_per);
+    k_dmma<2><<<g, b>>>(out, 10); CK(cudaDeviceSynchronize());
+    CK(cudaEventRecord(e0)); k_dmma<2><<<g, b>>>(out, iters); CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    printf(", \"dmma_2chain_ns_per_iter\": %.3f", ms * 1e6 / iters);
+    k_dmma<4><<<g, b>>>(out, 10); CK(cudaDeviceSynchronize());
+    CK(cudaEventRecord(e0)); k_dmma<4><<<g, b>>>(out, iters); CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    printf(", \"dmma_4chain_ns_per_iter\": %.3f", ms * 1e6 / iters);
+  }
+  double best_dfma = 0;
+  for (int tpb : {256, 512, 1024}) {
+    for (int blocks_per_sm : {1, 2}) {
+      int iters = 20000;
+      dim3 g(nsm * blocks_per_sm), b(tpb);
+      k_dfma<8><<<g, b>>>(out, 10); CK(cudaDeviceSynchronize());
+      CK(cudaEventRecord(e0));
+      k_dfma<8><<<g, b>>>(out, iters);
+      CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1)); CK(cudaEventElapsedTime(&ms, e0, e1));
+      double flops = 2.0 * 8 * (double)iters * g.x * tpb;
+      double tf = flops / (ms * 1e-3) / 1e12;
+      printf(", \"dfma_tpb%d_bps%d_tflops\": %.2f", tpb, blocks_per_sm, tf);
+      if (tf > best_dfma) best_dfma = tf;
+    }
+  }
+  // read-only HBM bandwidth over 8 GiB
+  size_t bytes = (size_t)8 << 30; size_t n4 = bytes / sizeof(double2);
+  double2* buf; CK(cudaMalloc(&buf, bytes)); CK(cudaMemset(buf, 0, bytes));
+  double best_bw = 0;
+  for (int bps : {2, 4, 8}) {
+    dim3 g(nsm * bps), b(512);
+    k_read<<<g, b>>>(buf, n4, out); CK(cudaDeviceSynchronize());
+    for (int rep = 0; rep < 3; ++rep) {
+      CK(cudaEventRecord(e0)); k_read<<<g, b>>>(buf, n4, out); CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      double gbs = bytes / (ms * 1e-3) / 1e9;
+      if (gbs > best_bw) best_bw = gbs;
+    }
+  }
+  printf(", \"best_dmma_tflops\": %.2f, \"best_dfma_tflops\": %.2f, \"read_hbm_gbs\": %.1f}\n", best_dmma, best_dfma, best_bw);
+  CK(cudaFree(buf));
+  return 0;
+}
