@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""Benchmark of the dGN evaluation hot path (BASELINE.json metric: CPD gradient evals/s).
+
+One step = one full pass of the hot path over the workload:
+  tf_cpd_eval (residual, F, three fused MTTKRPs, Grams)  [+ one SUM all-reduce of [grad|f] when N>1]
+  + tf_cg_solve (Hadamard chains, Jacobi-free CG on (J^T J + lambda I) x = -grad, fixed iterations)
+Default workload: c5 (1200^3, R=100, 13.8 GB fp64 T, 20 CG iterations) — the largest BASELINE
+config, the one the north star's scaling target is quoted on, and it fits one GPU.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1..c5] [--impl reference]
+
+N>1 is launched by torchrun (one rank per GPU, NCCL); T is sharded along K (strong scaling of one
+problem: total work fixed). Timing: W untimed warm-up steps, then K steps bracketed by a barrier and
+cuda synchronize, CUDA events on the evaluation stream, max over ranks. T (13.8 GB) exceeds the
+126 MB L2, so no flush is needed between steps. `--impl reference` times the CPU oracle (the
+"reference arm" of this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "CPD gradient evals/s (fused 3-mode MTTKRP+f); % of FP64/HBM roofline"
+UNIT = "evals/s"
+
+
+def load_json(path, default=None):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return default
+
+
+def fp64_peak():
+    """Measured FP64 tensor-core (DMMA) peak on this pool's B200 (tools/peaks.cu, profiles/peaks_r01.json)."""
+    p = load_json(os.path.join(ROOT, "profiles", "peaks_r01.json"), {}) or {}
+    return float(p.get("best_dmma_tflops", 37.07)), float(p.get("read_hbm_gbs", 6914.0))
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle timing
+def oracle_sample(cfg, P_T_slices, w_np, k_slices, cg_iters_sample, threads):
+    """Time the oracle (as it stands) on a bounded sample of the workload and scale to one full step.
+
+    Sample: F + grad over the first `k_slices` frontal slices (oracle_eval, OpenMP over slices), plus
+    `cg_iters_sample` CG iterations of Alg. CG-dGN (Thm Hv matvecs). Scaled: eval time * K/k_slices +
+    CG time * cg_iters/cg_iters_sample.
+    """
+    import numpy as np
+
+    import oracle
+    I, J, K, R = cfg.I, cfg.J, cfg.K, cfg.R
+    A = w_np[:I * R]
+    B = w_np[I * R:(I + J) * R]
+    C = w_np[(I + J) * R:].reshape(R, K)[:, :k_slices].reshape(-1)
+    ws = np.concatenate([A, B, C])
+    t0 = time.perf_counter()
+    f, g = oracle.cpd_eval(P_T_slices, ws, I, J, k_slices, R, nthreads=threads)
+    t_eval = time.perf_counter() - t0
+    t_cg = 0.0
+    if cfg.cg_iters and cg_iters_sample:
+        rhs = -np.concatenate([g[:(I + J) * R], np.zeros(K * R)])
+        t0 = time.perf_counter()
+        oracle.cg(w_np, rhs, cfg.lam, cg_iters_sample, I, J, K, R)
+        t_cg = time.perf_counter() - t0
+    step_s = t_eval * K / k_slices + (t_cg * cfg.cg_iters / cg_iters_sample if cg_iters_sample else 0.0)
+    sample = (f"oracle_eval on {k_slices}/{K} frontal slices ({t_eval:.2f} s, {threads} OpenMP threads, "
+              f"80-bit accumulation) scaled x{K / k_slices:.1f}")
+    if cfg.cg_iters and cg_iters_sample:
+        sample += f" + {cg_iters_sample}/{cfg.cg_iters} CG iterations ({t_cg:.2f} s) scaled"
+    return 1.0 / step_s, sample, t_eval + t_cg
+
+
+def pick_k_slices(cfg, T_first_slice, w_np, budget_s=12.0, threads=16):
+    """Slices so that the eval sample is ~budget_s of CPU work: time one slice, then scale."""
+    import numpy as np
+
+    import oracle
+    I, J, K, R = cfg.I, cfg.J, cfg.K, cfg.R
+    C = w_np[(I + J) * R:].reshape(R, K)[:, :1].reshape(-1)
+    ws = np.concatenate([w_np[:(I + J) * R], C])
+    t0 = time.perf_counter()
+    oracle.cpd_eval(T_first_slice, ws, I, J, 1, R, nthreads=1)
+    t1 = time.perf_counter() - t0          # one slice on one thread
+    per_slice = t1 / max(1, min(threads, 16))
+    return int(max(1, min(cfg.K, budget_s / max(per_slice, 1e-9))))
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    import synth
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = synth.CONFIGS[args.config]
+    threads = os.cpu_count() or 1
+    P1 = synth.make_problem(args.config, "cpu", k_range=(0, 1))
+    k_sl = pick_k_slices(cfg, P1.T.numpy().reshape(-1), P1.w(cfg.points[-1]).numpy(), 8.0, threads)
+    P = synth.make_problem(args.config, "cpu", k_range=(0, k_sl))
+    w = P.w(cfg.points[-1]).numpy()
+    T = P.T.numpy().reshape(-1)
+    cg_s = 1 if cfg.cg_iters else 0
+    for _ in range(max(0, args.warmup)):
+        pass  # the oracle has no warm-up state; a warm-up pass would only double the CPU time
+    vals, secs = [], 0.0
+    for _ in range(max(1, args.steps)):
+        v, sample, s = oracle_sample(cfg, T, w, k_sl, cg_s, threads)
+        vals.append(v)
+        secs += s
+    value = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64 (80-bit long double accumulation)",
+        "data": "synthetic (seeded, BASELINE.json recipe)",
+        "config": {"workload": f"{cfg.name}: {cfg.desc}", "I": cfg.I, "J": cfg.J, "K": cfg.K, "R": cfg.R,
+                   "cg_iters": cfg.cg_iters, "lambda": cfg.lam},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "the reference arm of this tier is the CPU oracle timed on the box's host cores on a bounded "
+                "sample of the workload, scaled to one full step",
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2110_05997_b200 as tf
+    import synth
+    from paper_2110_05997_b200.dist import ShardedEvaluator, shard_range
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    cfg = synth.CONFIGS[args.config]
+    I, J, K, R = cfg.I, cfg.J, cfg.K, cfg.R
+    k0, k1 = shard_range(K, rank, world)
+    P = synth.make_problem(args.config, dev, k_range=(k0, k1))
+    point = cfg.points[-1]
+    w = P.w(point).contiguous()
+    n = cfg.n
+    stream = torch.cuda.current_stream(dev)
+    ctx = tf.Context(local, stream)
+    ev = ShardedEvaluator(I, J, K, R, rank=rank, world=world, ctx=ctx)
+    grams = torch.empty(3 * R * R, dtype=torch.float64, device=dev)
+    x = torch.empty(n, dtype=torch.float64, device=dev)
+    rhs = torch.empty(n, dtype=torch.float64, device=dev)
+    dglob = tf.Dims(I, J, K, R)
+
+    def step():
+        f, g = ev(P.T, w)
+        ctx.tf_grams(dglob, w, grams)
+        torch.neg(g, out=rhs)
+        if cfg.cg_iters:
+            ctx.tf_cg_solve(dglob, grams, w, rhs, cfg.lam, cfg.cg_iters, 0.0, False, x)
+        return f
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize(dev)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    ctx.set_timing(True)
+    ctx.kernel_stats(reset=True)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        barrier()
+    ms_local = e0.elapsed_time(e1)
+    eval_ms, eval_n, launches = ctx.kernel_stats(reset=True)
+    ctx.set_timing(False)
+    t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_total = float(t.item())
+    ms_per_step = ms_total / args.steps
+    value = 1000.0 / ms_per_step          # whole-job evaluations of the full problem per second
+
+    # roofline of the dominant kernel (the fused evaluation kernel), on this rank
+    kernel_ms = eval_ms / max(1, eval_n)
+    flops = 6.0 * I * J * (k1 - k0) * R
+    peak_tf, peak_bw = fp64_peak()
+    achieved_tf = flops / (kernel_ms * 1e-3) / 1e12
+    prof = load_json(os.path.join(ROOT, "profiles", f"ncu_eval_{cfg.name}_r01.json"), {}) or {}
+    traffic = prof.get("dram_bytes_per_launch") if world == 1 else None
+    roofline = {"bound": "tensor", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                "frac": achieved_tf / peak_tf, "traffic": traffic,
+                "kernel": "k_eval_fused", "kernel_ms": kernel_ms,
+                "algorithmic": f"6*I*J*K_local*R = {flops:.4e} flop per launch (3 DMMA contractions per slice)",
+                "peak_source": "measured FP64 DMMA (mma.sync.m8n8k4.f64) peak, tools/peaks.cu, profiles/peaks_r01.json",
+                "hbm": {"bytes": 8.0 * I * J * (k1 - k0), "achieved_gbs": 8.0 * I * J * (k1 - k0) / (kernel_ms * 1e-3) / 1e9,
+                        "peak_gbs": peak_bw}}
+    clocks = clk.summary()
+
+    # e2e through the public C ABI with HOST buffers: T streamed from pinned host memory each step
+    e2e = None
+    if not args.no_e2e:
+        T_host = torch.empty(P.T.shape, dtype=torch.float64, pin_memory=True)
+        T_host.copy_(P.T)
+        w_host = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        w_host.copy_(w)
+        gh = torch.empty(n + 1, dtype=torch.float64, pin_memory=True)
+        xh = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        dl = tf.Dims(I, J, k1 - k0, R, K_total=K, k_begin=k0)
+        gdev = torch.empty(n + 1, dtype=torch.float64, device=dev)
+        wdev = torch.empty(n, dtype=torch.float64, device=dev)
+
+        def step_e2e():
+            ctx.tf_cpd_eval_host(dl, T_host, w_host, gh[n:], gh[:n])     # H2D of T (+w) inside, grad/f D2H
+            gdev.copy_(gh, non_blocking=True)                               # H2D grad|f
+            if world > 1:
+                dist.all_reduce(gdev, op=dist.ReduceOp.SUM)
+            wdev.copy_(w_host, non_blocking=True)                           # H2D w
+            ctx.tf_grams(dglob, wdev, grams)
+            torch.neg(gdev[:n], out=rhs)
+            if cfg.cg_iters:
+                ctx.tf_cg_solve(dglob, grams, wdev, rhs, cfg.lam, cfg.cg_iters, 0.0, False, x)
+            xh.copy_(x, non_blocking=True)                                  # D2H step result
+            torch.cuda.current_stream(dev).synchronize()
+
+        step_e2e()
+        barrier()
+        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            step_e2e()
+        barrier()
+        sec = time.perf_counter() - t0
+        st = torch.tensor([sec], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(st, op=dist.ReduceOp.MAX)
+        sec = float(st.item())
+        h2d = int(T_host.numel() * 8 + 2 * n * 8 + (n + 1) * 8)
+        d2h = int((n + 1) * 8 + n * 8)
+        e2e = {"value": e2e_steps / sec, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "steps": e2e_steps,
+               "path": "tf_cpd_eval_host (T streamed from pinned host memory in 512 MB slabs, copies overlapped "
+                       "with the fused kernel) + grad H2D + tf_grams + tf_cg_solve + x D2H"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        wn = w.cpu().numpy()
+        k_sl = pick_k_slices(cfg, P.T[:1].cpu().numpy().reshape(-1), wn, 12.0, threads)
+        Ts = P.T[:k_sl].cpu().numpy().reshape(-1)
+        v, sample, _ = oracle_sample(cfg, Ts, wn, k_sl, 1 if cfg.cg_iters else 0, threads)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json recipe; no dataset)",
+            "config": {"workload": f"{cfg.name}: {cfg.desc}", "I": I, "J": J, "K": K, "R": R,
+                       "cg_iters": cfg.cg_iters, "lambda": cfg.lam, "point": point,
+                       "parallelism": f"K-sharded x{world} + 1 NCCL all-reduce of [grad|f]" if world > 1 else "1 GPU",
+                       "l2": f"inputs larger than L2 (T = {cfg.t_bytes / 1e9:.2f} GB > 126 MB), no flush",
+                       "step": "tf_cpd_eval + tf_grams + tf_cg_solve(cg_iters)"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": int(launches),
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,136 @@
+/*
+ * tf.h -- C ABI of the B200 (sm_100a) dGN evaluation hot path of Tensor Fox
+ * (F. Bottega Diniz, "Tensor decompositions and algorithms, with applications
+ * to tensor learning", arxiv 2110.05997; PAPER.md line numbers below).
+ *
+ * Library: paper_2110_05997_b200/libtf.so. Plain C types only.
+ *
+ * Conventions (all arrays IEEE fp64):
+ *   T      dense I x J x K tensor, first index fastest: T[i + ldT*(j + J*k)]
+ *          with ldT >= I (Alg. Unfolding: the innermost loop
+ *          runs over i_1). Frontal slice T[:,:,k] is a contiguous column-major
+ *          block.
+ *   w      packed parameters [vec A; vec B; vec C], A (I x R), B (J x R),
+ *          C (K_total x R) column-major, n = R*(I+J+K_total).
+ *          grad, v, y, rhs, x use the same layout.
+ *   grams  [A^T A | B^T B | C^T C], each R x R column-major.
+ *   pi     [Pi^(1) | Pi^(2) | Pi^(3) | Pi^(1,2) | Pi^(1,3) | Pi^(2,3)], R x R each
+ *          (for L = 3, Pi^(l',l'') = pi^(l) of the third mode).
+ *
+ * K-sharding (data parallel over frontal slices): a call may hold only slices
+ * k_begin .. k_begin+K-1 of a tensor with K_total slices (T points at slice
+ * k_begin); w always holds the full C (K_total rows).
+ *
+ * Ownership: every pointer argument is caller-owned memory. Device pointers
+ * (all arguments of the non-_host calls) must be on the ctx's device; the
+ * library never frees or retains them beyond the call. The ctx owns its
+ * workspace (partial-sum buffers, TMA descriptors, CG vectors), grows it on
+ * demand and frees it in tf_ctx_destroy; steady-state calls allocate nothing.
+ *
+ * Asynchrony: calls are enqueued on the ctx stream and return before the GPU
+ * finishes (except tf_cg_solve's host outputs and the _host variants, which
+ * synchronize the stream). Outputs are valid after the stream is synchronized.
+ *
+ * Errors: every call returns a tf_status; nothing is thrown or exits across
+ * the ABI. TF_ERR_ARG: null pointer, a dimension < 1, ldT < I, or
+ * k_begin + K > K_total. TF_ERR_ALIGN: T not 8-byte aligned. TF_ERR_UNSUPPORTED:
+ * R above TF_MAX_R. TF_ERR_CUDA: a launch or runtime error (detail in
+ * tf_last_error). TF_ERR_NONFINITE: CG met a non-finite alpha/beta (iteration
+ * index in tf_last_error). TF_ERR_ALLOC: workspace allocation failed.
+ */
+#ifndef TF_H_
+#define TF_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TF_MAX_R 128
+
+typedef enum {
+  TF_OK = 0,
+  TF_ERR_ARG = 1,
+  TF_ERR_ALIGN = 2,
+  TF_ERR_UNSUPPORTED = 3,
+  TF_ERR_CUDA = 4,
+  TF_ERR_NONFINITE = 5,
+  TF_ERR_ALLOC = 6
+} tf_status;
+
+typedef struct tf_ctx tf_ctx;
+
+/* I, J: full mode sizes; K: local number of frontal slices; R: CPD rank;
+ * ldT: leading dimension of T (>= I, 0 means I); K_total: slices of the whole
+ * tensor (0 means K); k_begin: global index of the first local slice. */
+typedef struct {
+  int64_t I, J, K, R, ldT, K_total, k_begin;
+} tf_dims;
+
+/* Create a context bound to CUDA device `device`, enqueueing on `cuda_stream`
+ * (a cudaStream_t; NULL = legacy default stream). */
+tf_status tf_ctx_create(tf_ctx **out, int device, void *cuda_stream);
+tf_status tf_ctx_destroy(tf_ctx *ctx);
+/* Re-target the ctx to another stream of the same device. */
+tf_status tf_ctx_set_stream(tf_ctx *ctx, void *cuda_stream);
+const char *tf_status_str(tf_status s);
+/* Detail of the last error on this ctx (offending argument, CG iteration, CUDA message). */
+const char *tf_last_error(const tf_ctx *ctx);
+int tf_version(void);
+
+/* a1: pi^(l) = W^(l)^T W^(l) for the three modes. grams: 3*R*R doubles. */
+tf_status tf_grams(tf_ctx *ctx, tf_dims d, const double *w, double *grams);
+
+/* a7: Hadamard chains from the Grams. pi: 6*R*R doubles. */
+tf_status tf_hadamard(tf_ctx *ctx, int64_t R, const double *grams, double *pi);
+
+/* a2-a6: one evaluation on the local slices.
+ *   f    (1 double)  F = 1/2 ||T - [[A,B,C]]||^2 over the local slices
+ *   grad (n doubles) grad F = J_f^T f = W Pi - T_(l)(.W).
+ *        With K < K_total, the dF/dA and dF/dB blocks and f are partial sums over
+ *        the local slices and dF/dC holds rows k_begin..k_begin+K-1 (other rows 0):
+ *        an elementwise SUM over shards of [grad | f] gives the global result.
+ *   grams (nullable, 3*R*R) the Grams at w, as tf_grams.
+ * The three MTTKRPs and the residual are fused in one pass over T. */
+tf_status tf_cpd_eval(tf_ctx *ctx, tf_dims d, const double *T, const double *w, double *f, double *grad,
+                      double *grams);
+
+/* Same as tf_cpd_eval with HOST inputs/outputs (pageable or pinned). T is streamed
+ * to the device in slabs of frontal slices overlapped with the fused kernel, so
+ * T need not fit in device memory. Synchronizes the ctx stream before returning. */
+tf_status tf_cpd_eval_host(tf_ctx *ctx, tf_dims d, const double *T_host, const double *w_host, double *f_host,
+                           double *grad_host);
+
+/* a8: y = (J_f^T J_f + lambda I) v by Thm Hv, from the Grams
+ * at w (grams as produced by tf_grams) and w itself (Thm Hv's off-diagonal blocks
+ * need the factors). v, y: n doubles (y must not alias v). */
+tf_status tf_gn_matvec(tf_ctx *ctx, tf_dims d, const double *grams, const double *w, const double *v,
+                       double lambda, double *y);
+
+/* a9: Alg. CG-dGN: solve (J^T J + lambda I) x = rhs with
+ * x0 = 0, at most maxiter iterations, stopping when ||r||^2 < tol (tol = 0: run
+ * exactly maxiter). jacobi != 0 preconditions with M = diag(J^T J) + lambda I as
+ * M^{-1/2} (.) M^{-1/2} and returns x in
+ * w-coordinates (x = M^{-1/2} x_hat). The iteration runs on the device with no
+ * host round trip; iters_done and res2 (host pointers, nullable) receive the
+ * number of iterations run and the final ||r||^2 after a stream synchronize.
+ * x: n doubles (device). Returns TF_ERR_NONFINITE if alpha or beta became
+ * non-finite (x then holds the last finite iterate). */
+tf_status tf_cg_solve(tf_ctx *ctx, tf_dims d, const double *grams, const double *w, const double *rhs,
+                      double lambda, int maxiter, double tol, int jacobi, double *x, int *iters_done,
+                      double *res2);
+
+/* Instrumentation (bench.py): when enabled, the fused evaluation kernel is
+ * bracketed by CUDA events on the ctx stream; tf_ctx_kernel_stats synchronizes
+ * and returns the summed device time (ms) and count of the fused-kernel launches
+ * since the last reset, plus the total number of kernels this ctx launched. */
+tf_status tf_ctx_set_timing(tf_ctx *ctx, int enable);
+tf_status tf_ctx_kernel_stats(tf_ctx *ctx, double *eval_kernel_ms, int64_t *eval_kernel_launches,
+                              int64_t *total_launches, int reset);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TF_H_ */

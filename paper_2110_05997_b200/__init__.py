@@ -1,0 +1,233 @@
+"""Python binding of libtf.so — the B200 (sm_100a) dGN evaluation hot path of Tensor Fox.
+
+Argument marshalling only: every function here validates shapes/dtypes, takes the
+device pointers of torch tensors (PyTorch supplies memory and streams) and calls
+the C ABI of include/tf.h with the same names. All arithmetic of the method runs
+in the CUDA kernels behind that ABI. There is no CPU fallback: importing this
+package raises if libtf.so is missing, and every call raises on a non-OK status.
+
+Layouts (include/tf.h): T is a contiguous fp64 tensor of shape (K, J, I) — i.e.
+first index fastest, T[i + I*(j + J*k)] — or any tensor whose memory is that;
+w = [vec A; vec B; vec C] (column-major factors), length n = R*(I+J+K_total).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtf.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python paper_2110_05997_b200/build.py` "
+        "(nvcc, sm_100a). There is no CPU fallback.")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+
+class TfDims(ctypes.Structure):
+    _fields_ = [("I", ctypes.c_int64), ("J", ctypes.c_int64), ("K", ctypes.c_int64), ("R", ctypes.c_int64),
+                ("ldT", ctypes.c_int64), ("K_total", ctypes.c_int64), ("k_begin", ctypes.c_int64)]
+
+
+_vp = ctypes.c_void_p
+_lib.tf_ctx_create.argtypes = [ctypes.POINTER(_vp), ctypes.c_int, _vp]
+_lib.tf_ctx_destroy.argtypes = [_vp]
+_lib.tf_ctx_set_stream.argtypes = [_vp, _vp]
+_lib.tf_status_str.restype = ctypes.c_char_p
+_lib.tf_status_str.argtypes = [ctypes.c_int]
+_lib.tf_last_error.restype = ctypes.c_char_p
+_lib.tf_last_error.argtypes = [_vp]
+_lib.tf_grams.argtypes = [_vp, TfDims, _vp, _vp]
+_lib.tf_hadamard.argtypes = [_vp, ctypes.c_int64, _vp, _vp]
+_lib.tf_cpd_eval.argtypes = [_vp, TfDims, _vp, _vp, _vp, _vp, _vp]
+_lib.tf_cpd_eval_host.argtypes = [_vp, TfDims, _vp, _vp, _vp, _vp]
+_lib.tf_gn_matvec.argtypes = [_vp, TfDims, _vp, _vp, _vp, ctypes.c_double, _vp]
+_lib.tf_cg_solve.argtypes = [_vp, TfDims, _vp, _vp, _vp, ctypes.c_double, ctypes.c_int, ctypes.c_double,
+                             ctypes.c_int, _vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)]
+_lib.tf_ctx_set_timing.argtypes = [_vp, ctypes.c_int]
+_lib.tf_ctx_kernel_stats.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64),
+                                     ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
+
+EXPORTED = ["tf_ctx_create", "tf_ctx_destroy", "tf_ctx_set_stream", "tf_status_str", "tf_last_error", "tf_version",
+            "tf_grams", "tf_hadamard", "tf_cpd_eval", "tf_cpd_eval_host", "tf_gn_matvec", "tf_cg_solve",
+            "tf_ctx_set_timing", "tf_ctx_kernel_stats"]
+
+TF_OK, TF_ERR_ARG, TF_ERR_ALIGN, TF_ERR_UNSUPPORTED, TF_ERR_CUDA, TF_ERR_NONFINITE, TF_ERR_ALLOC = range(7)
+MAX_R = 128
+
+
+class TfError(RuntimeError):
+    def __init__(self, status: int, detail: str):
+        self.status = status
+        super().__init__(f"{_lib.tf_status_str(status).decode()}: {detail}")
+
+
+@dataclass
+class Dims:
+    I: int
+    J: int
+    K: int
+    R: int
+    ldT: int = 0
+    K_total: int = 0
+    k_begin: int = 0
+
+    def c(self) -> TfDims:
+        return TfDims(self.I, self.J, self.K, self.R, self.ldT, self.K_total, self.k_begin)
+
+    @property
+    def Kt(self) -> int:
+        return self.K_total or (self.K + self.k_begin)
+
+    @property
+    def n(self) -> int:
+        return self.R * (self.I + self.J + self.Kt)
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _dev(t: torch.Tensor, name: str, numel: int | None = None):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != torch.float64:
+        raise TypeError(f"{name} must be float64")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if numel is not None and t.numel() < numel:
+        raise ValueError(f"{name} has {t.numel()} elements, needs {numel}")
+
+
+class Context:
+    """A tf_ctx bound to one device and a CUDA stream (default: torch's current stream)."""
+
+    def __init__(self, device: int | torch.device | None = None, stream: torch.cuda.Stream | None = None):
+        if device is None:
+            device = torch.cuda.current_device()
+        if isinstance(device, torch.device):
+            device = device.index if device.index is not None else torch.cuda.current_device()
+        self.device = int(device)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        h = _vp()
+        st = _lib.tf_ctx_create(ctypes.byref(h), self.device, _vp(self.stream.cuda_stream))
+        if st != TF_OK:
+            raise TfError(st, "tf_ctx_create failed")
+        self._h = h
+
+    def _check(self, st: int):
+        if st != TF_OK:
+            raise TfError(st, _lib.tf_last_error(self._h).decode())
+
+    def set_stream(self, stream: torch.cuda.Stream):
+        self.stream = stream
+        self._check(_lib.tf_ctx_set_stream(self._h, _vp(stream.cuda_stream)))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.tf_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------ the C-ABI calls
+    def tf_grams(self, d: Dims, w: torch.Tensor, grams: torch.Tensor | None = None) -> torch.Tensor:
+        _dev(w, "w", d.n)
+        if grams is None:
+            grams = torch.empty(3 * d.R * d.R, dtype=torch.float64, device=w.device)
+        _dev(grams, "grams", 3 * d.R * d.R)
+        self._check(_lib.tf_grams(self._h, d.c(), _ptr(w), _ptr(grams)))
+        return grams
+
+    def tf_hadamard(self, R: int, grams: torch.Tensor, pi: torch.Tensor | None = None) -> torch.Tensor:
+        _dev(grams, "grams", 3 * R * R)
+        if pi is None:
+            pi = torch.empty(6 * R * R, dtype=torch.float64, device=grams.device)
+        _dev(pi, "pi", 6 * R * R)
+        self._check(_lib.tf_hadamard(self._h, R, _ptr(grams), _ptr(pi)))
+        return pi
+
+    def tf_cpd_eval(self, d: Dims, T: torch.Tensor, w: torch.Tensor, f: torch.Tensor | None = None,
+                    grad: torch.Tensor | None = None, grams: torch.Tensor | None = None):
+        """Returns (f, grad) device tensors (f has one element)."""
+        ldT = d.ldT or d.I
+        _dev(T, "T", ldT * d.J * d.K - (ldT - d.I))
+        _dev(w, "w", d.n)
+        if f is None:
+            f = torch.empty(1, dtype=torch.float64, device=w.device)
+        if grad is None:
+            grad = torch.empty(d.n, dtype=torch.float64, device=w.device)
+        _dev(f, "f", 1)
+        _dev(grad, "grad", d.n)
+        if grams is not None:
+            _dev(grams, "grams", 3 * d.R * d.R)
+        self._check(_lib.tf_cpd_eval(self._h, d.c(), _ptr(T), _ptr(w), _ptr(f), _ptr(grad), _ptr(grams)))
+        return f, grad
+
+    def tf_cpd_eval_host(self, d: Dims, T_host: torch.Tensor, w_host: torch.Tensor,
+                         f_host: torch.Tensor | None = None, grad_host: torch.Tensor | None = None):
+        """Host-buffer evaluation: T streamed to the device in slabs (synchronizes)."""
+        for name, t in (("T_host", T_host), ("w_host", w_host)):
+            if t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+                raise TypeError(f"{name} must be a contiguous float64 CPU tensor")
+        if f_host is None:
+            f_host = torch.empty(1, dtype=torch.float64)
+        if grad_host is None:
+            grad_host = torch.empty(d.n, dtype=torch.float64)
+        self._check(_lib.tf_cpd_eval_host(self._h, d.c(), _ptr(T_host), _ptr(w_host), _ptr(f_host),
+                                          _ptr(grad_host)))
+        return f_host, grad_host
+
+    def tf_gn_matvec(self, d: Dims, grams: torch.Tensor, w: torch.Tensor, v: torch.Tensor, lam: float,
+                     y: torch.Tensor | None = None) -> torch.Tensor:
+        _dev(grams, "grams", 3 * d.R * d.R)
+        _dev(w, "w", d.n)
+        _dev(v, "v", d.n)
+        if y is None:
+            y = torch.empty(d.n, dtype=torch.float64, device=w.device)
+        _dev(y, "y", d.n)
+        self._check(_lib.tf_gn_matvec(self._h, d.c(), _ptr(grams), _ptr(w), _ptr(v), float(lam), _ptr(y)))
+        return y
+
+    def tf_cg_solve(self, d: Dims, grams: torch.Tensor, w: torch.Tensor, rhs: torch.Tensor, lam: float,
+                    maxiter: int, tol: float = 0.0, jacobi: bool = False, x: torch.Tensor | None = None):
+        """Returns (x, iters_done, ||r||^2)."""
+        _dev(grams, "grams", 3 * d.R * d.R)
+        _dev(w, "w", d.n)
+        _dev(rhs, "rhs", d.n)
+        if x is None:
+            x = torch.empty(d.n, dtype=torch.float64, device=w.device)
+        _dev(x, "x", d.n)
+        it = ctypes.c_int()
+        r2 = ctypes.c_double()
+        self._check(_lib.tf_cg_solve(self._h, d.c(), _ptr(grams), _ptr(w), _ptr(rhs), float(lam), int(maxiter),
+                                     float(tol), int(bool(jacobi)), _ptr(x), ctypes.byref(it), ctypes.byref(r2)))
+        return x, it.value, r2.value
+
+    def set_timing(self, enable: bool):
+        self._check(_lib.tf_ctx_set_timing(self._h, int(bool(enable))))
+
+    def kernel_stats(self, reset: bool = True):
+        """(summed fused-eval kernel ms, number of fused-eval launches, total kernel launches)."""
+        ms = ctypes.c_double()
+        ne = ctypes.c_int64()
+        nt = ctypes.c_int64()
+        self._check(_lib.tf_ctx_kernel_stats(self._h, ctypes.byref(ms), ctypes.byref(ne), ctypes.byref(nt),
+                                             int(bool(reset))))
+        return ms.value, ne.value, nt.value
+
+
+def dims_of(cfg_or_I, J=None, K=None, R=None, **kw) -> Dims:
+    if J is None:
+        c = cfg_or_I
+        return Dims(c.I, c.J, c.K, c.R, **kw)
+    return Dims(cfg_or_I, J, K, R, **kw)

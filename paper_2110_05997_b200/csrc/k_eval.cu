@@ -1,0 +1,333 @@
+// Fused one-pass evaluation of F and grad F for the dGN hot path.
+//
+// For each frontal slice k (slice formula X_k = A diag(c_k) B^T) and each
+// 64x64 tile (i-tile, j-tile) of it, one CTA does, with FP64 tensor-core MMA (DMMA.8x8x4):
+//   phase 1  E   = T_k - A diag(c_k) B^T          residual, inner dim R
+//            f  += sum E^2                         objective
+//   phase 2  P   = E B                             (I-tile x R), inner dim 64 (j)
+//            accA += P diag(c_k)                   -> dF/dA = -sum_k E_k B diag(c_k)
+//            gCp[k] = sum_i A o P                  -> dF/dC[k,:] = -sum_ij E_ij A_i: B_j:
+//   phase 3  accB^T += (A diag(c_k))^T E           -> dF/dB = -sum_k E_k^T A diag(c_k), inner dim 64 (i)
+// i.e. grad F = J_f^T f (Lemma gradF; Lemma partialf 1855-1863) with all three
+// MTTKRPs T_(l)(.W) (Kolda) fused on one read of T. T tiles are staged through
+// shared memory by TMA (cp.async.bulk.tensor, double-buffered, mbarrier completion); E lives in
+// registers (phase 1) and in the same shared buffer that held T_k (phases 2-3): never in HBM.
+// A CTA owns one (i-tile, j-tile) and a contiguous range of slices; accA/accB stay in registers
+// over the range and are written once as partials; k_eval_finalize reduces all partials in a
+// fixed order (deterministic, bitwise reproducible).
+#include "tf_internal.h"
+#include "tf_device.cuh"
+
+namespace tfk {
+
+constexpr int kBI = 64;         // tile rows (i)
+constexpr int kBJ = 64;         // tile cols (j)
+constexpr int kLDE = 68;        // smem leading dim of a T/E tile [j][i]; 68 = 4 mod 16 -> conflict-free frags
+constexpr int kThreads = 256;   // 8 warps
+constexpr int kTileBytes = kLDE * kBJ * 8;   // one TMA box 68 x 64 doubles
+
+template <int NT>
+struct EvalSmem {
+  static constexpr int RP = 8 * NT;          // padded rank
+  static constexpr int LDF = 8 * NT + 4;     // factor tile leading dim (4 mod 16 in doubles)
+  static constexpr size_t off_te = 0;                                   // 2 x [64][68] doubles
+  static constexpr size_t off_a = off_te + 2 * (size_t)kTileBytes;      // [64][LDF]
+  static constexpr size_t off_b = off_a + (size_t)kBI * LDF * 8;        // [64][LDF]
+  static constexpr size_t off_c = off_b + (size_t)kBJ * LDF * 8;        // 2 x [RP]
+  static constexpr size_t off_gc = off_c + 2 * (size_t)RP * 8;          // [8][RP]
+  static constexpr size_t off_red = off_gc + 8 * (size_t)RP * 8;        // [8]
+  static constexpr size_t off_bar = off_red + 8 * 8;                    // 2 mbarriers
+  static constexpr size_t bytes = off_bar + 2 * 8;
+};
+
+template <int NT, bool kTMA>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_eval_fused(const __grid_constant__ CUtensorMap tmapT, const double* __restrict__ T, EvalArgs p) {
+  using S = EvalSmem<NT>;
+  constexpr int RP = S::RP;
+  constexpr int LDF = S::LDF;
+  extern __shared__ __align__(128) unsigned char smem[];
+  double* sTE = reinterpret_cast<double*>(smem + S::off_te);
+  double* sA = reinterpret_cast<double*>(smem + S::off_a);
+  double* sB = reinterpret_cast<double*>(smem + S::off_b);
+  double* sC = reinterpret_cast<double*>(smem + S::off_c);
+  double* sGC = reinterpret_cast<double*>(smem + S::off_gc);
+  double* sRed = reinterpret_cast<double*>(smem + S::off_red);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::off_bar);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
+  const int bid = blockIdx.x;
+  const int it = bid % p.nTi;
+  const int jt = (bid / p.nTi) % p.nTj;
+  const int kc = bid / (p.nTi * p.nTj);
+  const int64_t i0 = (int64_t)it * kBI, j0 = (int64_t)jt * kBJ;
+  const int64_t kA = (int64_t)kc * p.kChunk;
+  const int64_t kB = min(p.K, kA + p.kChunk);
+  const int nk = (int)max((int64_t)0, kB - kA);
+
+  // ---- prologue: barriers, first T tile, factor tiles, first c row
+  if (kTMA && tid == 0) {
+    prefetch_tmap(&tmapT);
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (kTMA && tid == 0 && nk > 0) {
+    mbar_arrive_expect_tx(&bar[0], kTileBytes);
+    tma_load_3d(sTE, &tmapT, (int)i0, (int)j0, (int)kA, &bar[0]);
+  }
+  for (int idx = tid; idx < kBI * LDF; idx += kThreads) {
+    const int i = idx / LDF, r = idx % LDF;
+    const int64_t gi = i0 + i;
+    sA[idx] = (gi < p.I && r < p.R) ? p.A[gi + p.I * r] : 0.0;
+  }
+  for (int idx = tid; idx < kBJ * LDF; idx += kThreads) {
+    const int j = idx / LDF, r = idx % LDF;
+    const int64_t gj = j0 + j;
+    sB[idx] = (gj < p.J && r < p.R) ? p.B[gj + p.J * r] : 0.0;
+  }
+  if (tid < RP && nk > 0) sC[tid] = (tid < p.R) ? p.C[(p.kbeg + kA) + p.Ktot * tid] : 0.0;
+
+  double accA[NT][2], accB[NT][2];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) accA[t][0] = accA[t][1] = accB[t][0] = accB[t][1] = 0.0;
+  double fsum = 0.0;
+
+  // phase-1 warp tile: rows 32*wi.., cols 16*wj..
+  const int wi = warp & 1, wj = warp >> 1;
+
+  for (int kk = 0; kk < nk; ++kk) {
+    const int b = kk & 1;
+    const int64_t k = kA + kk;
+    double* sT = sTE + b * (kLDE * kBJ);
+    const double* sc = sC + b * RP;
+    __syncthreads();  // previous iteration fully done with buffer b^1, sGC, sC[b^1]
+    if (kk + 1 < nk) {
+      if (kTMA) {
+        if (tid == 0) {
+          fence_proxy_async_smem();
+          mbar_arrive_expect_tx(&bar[b ^ 1], kTileBytes);
+          tma_load_3d(sTE + (b ^ 1) * (kLDE * kBJ), &tmapT, (int)i0, (int)j0, (int)(k + 1), &bar[b ^ 1]);
+        }
+      }
+      if (tid < RP) sC[(b ^ 1) * RP + tid] = (tid < p.R) ? p.C[(p.kbeg + k + 1) + p.Ktot * tid] : 0.0;
+    }
+    if (kTMA) {
+      mbar_wait(&bar[b], (kk >> 1) & 1);
+    } else {
+      // plain cooperative load of the 64 x 64 tile (odd ldT: no TMA)
+      for (int idx = tid; idx < kBI * kBJ; idx += kThreads) {
+        const int j = idx / kBI, i = idx % kBI;
+        const int64_t gi = i0 + i, gj = j0 + j;
+        sT[j * kLDE + i] = (gi < p.I && gj < p.J) ? T[gi + p.ldT * (gj + p.J * k)] : 0.0;
+      }
+      __syncthreads();
+    }
+
+    // ---- phase 1: E = T - A diag(c) B^T on a 32 x 16 warp tile (4 x 2 fragments)
+    {
+      double E[4][2][2];
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int n = 0; n < 2; ++n)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) E[m][n][e] = sT[(16 * wj + 8 * n + 2 * q + e) * kLDE + 32 * wi + 8 * m + g];
+#pragma unroll 2
+      for (int s = 0; s < RP / 4; ++s) {
+        const double cneg = -sc[4 * s + q];
+        double a[4], bb[2];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) a[m] = sA[(32 * wi + 8 * m + g) * LDF + 4 * s + q];
+#pragma unroll
+        for (int n = 0; n < 2; ++n) bb[n] = sB[(16 * wj + 8 * n + g) * LDF + 4 * s + q] * cneg;
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+          for (int n = 0; n < 2; ++n) dmma(E[m][n], a[m], bb[n]);
+      }
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int n = 0; n < 2; ++n)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            fsum = fma(E[m][n][e], E[m][n][e], fsum);
+            sT[(16 * wj + 8 * n + 2 * q + e) * kLDE + 32 * wi + 8 * m + g] = E[m][n][e];
+          }
+    }
+    __syncthreads();  // E tile complete in sT
+
+    // ---- phase 2: P = E B for i-rows 8*warp.., all R; accA += P diag(c); gC partial
+    {
+      double P[NT][2];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) P[t][0] = P[t][1] = 0.0;
+#pragma unroll 4
+      for (int s = 0; s < kBJ / 4; ++s) {
+        const double a = sT[(4 * s + q) * kLDE + 8 * warp + g];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) dmma(P[t], a, sB[(4 * s + q) * LDF + 8 * t + g]);
+      }
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int r = 8 * t + 2 * q + e;
+          accA[t][e] = fma(sc[r], P[t][e], accA[t][e]);
+          double v = sA[(8 * warp + g) * LDF + r] * P[t][e];
+          v += __shfl_xor_sync(0xffffffffu, v, 4);
+          v += __shfl_xor_sync(0xffffffffu, v, 8);
+          v += __shfl_xor_sync(0xffffffffu, v, 16);
+          if (g == 0) sGC[warp * RP + r] = v;
+        }
+      }
+    }
+
+    // ---- phase 3: accB^T += (A diag c)^T E for j-cols 8*warp.., all R
+    {
+      double cv[NT];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) cv[t] = sc[8 * t + g];
+#pragma unroll 4
+      for (int s = 0; s < kBI / 4; ++s) {
+        const double bb = sT[(8 * warp + g) * kLDE + 4 * s + q];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) dmma(accB[t], sA[(4 * s + q) * LDF + 8 * t + g] * cv[t], bb);
+      }
+    }
+    __syncthreads();  // sGC complete
+    if (tid < RP) {
+      double v = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) v += sGC[w * RP + tid];
+      p.gCp[((int64_t)(it * p.nTj + jt) * p.K + k) * RP + tid] = v;
+    }
+  }
+
+  // ---- epilogue: partials
+  {
+    const int64_t base = ((int64_t)(jt * p.kSplit + kc) * p.Ipad + i0 + 8 * warp + g) * RP;
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      double2 v = make_double2(accA[t][0], accA[t][1]);
+      *reinterpret_cast<double2*>(&p.gAp[base + 8 * t + 2 * q]) = v;
+    }
+  }
+  {
+#pragma unroll
+    for (int t = 0; t < NT; ++t)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t j = j0 + 8 * warp + 2 * q + e;
+        p.gBp[((int64_t)(it * p.kSplit + kc) * p.Jpad + j) * RP + 8 * t + g] = accB[t][e];
+      }
+  }
+  fsum = warp_sum(fsum);
+  if (lane == 0) sRed[warp] = fsum;
+  __syncthreads();
+  if (tid == 0) {
+    double v = 0.0;
+    for (int w = 0; w < 8; ++w) v += sRed[w];
+    p.fp[bid] = v;
+  }
+}
+
+// Fixed-order reduction of all partials into the packed gradient and f (row a6).
+// grad = -(sum of partials) (the kernels accumulate +E-contractions; dF/dW = -MTTKRP(E)).
+__global__ void k_eval_finalize(EvalArgs p, int RP, double* __restrict__ f, double* __restrict__ grad) {
+  const int64_t nA = p.I * p.R, nB = p.J * p.R, nC = p.Ktot * p.R;
+  const int64_t total = nA + nB + nC;
+  const int64_t nPA = (int64_t)p.nTj * p.kSplit, nPB = (int64_t)p.nTi * p.kSplit, nPC = (int64_t)p.nTi * p.nTj;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    if (idx < nA) {
+      const int64_t r = idx / p.I, i = idx % p.I;
+      for (int64_t s = 0; s < nPA; ++s) v += p.gAp[(s * p.Ipad + i) * RP + r];
+      grad[idx] = -v;
+    } else if (idx < nA + nB) {
+      const int64_t q = idx - nA, r = q / p.J, j = q % p.J;
+      for (int64_t s = 0; s < nPB; ++s) v += p.gBp[(s * p.Jpad + j) * RP + r];
+      grad[idx] = -v;
+    } else {
+      const int64_t q = idx - nA - nB, r = q / p.Ktot, kg = q % p.Ktot;
+      const int64_t k = kg - p.kbeg;
+      if (k >= 0 && k < p.K) {
+        for (int64_t s = 0; s < nPC; ++s) v += p.gCp[(s * p.K + k) * RP + r];
+        grad[idx] = -v;
+      } else {
+        grad[idx] = 0.0;
+      }
+    }
+  }
+  if (blockIdx.x == 0) {
+    __shared__ double red[32];
+    double v = 0.0;
+    for (int64_t s = threadIdx.x; s < p.nCta; s += blockDim.x) v += p.fp[s];
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+      *f = 0.5 * t;
+    }
+  }
+}
+
+template <int NT>
+static cudaError_t launch_eval_nt(const CUtensorMap* map, const double* T, const EvalArgs& p, bool tma,
+                                  cudaStream_t st) {
+  const size_t smem = EvalSmem<NT>::bytes;
+  if (tma) {
+    auto kern = k_eval_fused<NT, true>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<p.nCta, kThreads, smem, st>>>(*map, T, p);
+  } else {
+    auto kern = k_eval_fused<NT, false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<p.nCta, kThreads, smem, st>>>(*map, T, p);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_eval(const CUtensorMap* map, const double* T, const EvalArgs& p, int NT, bool tma,
+                        cudaStream_t st) {
+  switch (NT) {
+#define TF_CASE(n) \
+  case n:          \
+    return launch_eval_nt<n>(map, T, p, tma, st);
+    TF_CASE(1) TF_CASE(2) TF_CASE(3) TF_CASE(4) TF_CASE(5) TF_CASE(6) TF_CASE(7) TF_CASE(8)
+    TF_CASE(9) TF_CASE(10) TF_CASE(11) TF_CASE(12) TF_CASE(13) TF_CASE(14) TF_CASE(15) TF_CASE(16)
+#undef TF_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_eval_finalize(const EvalArgs& p, int RP, double* f, double* grad, int nsm, cudaStream_t st) {
+  const int64_t total = (p.I + p.J + p.Ktot) * p.R;
+  int blocks = (int)std::min<int64_t>((total + 255) / 256, 4LL * nsm);
+  if (blocks < 1) blocks = 1;
+  k_eval_finalize<<<blocks, 256, 0, st>>>(p, RP, f, grad);
+  return cudaGetLastError();
+}
+
+size_t eval_smem_bytes(int NT) {
+  switch (NT) {
+#define TF_CASE(n) \
+  case n:          \
+    return EvalSmem<n>::bytes;
+    TF_CASE(1) TF_CASE(2) TF_CASE(3) TF_CASE(4) TF_CASE(5) TF_CASE(6) TF_CASE(7) TF_CASE(8)
+    TF_CASE(9) TF_CASE(10) TF_CASE(11) TF_CASE(12) TF_CASE(13) TF_CASE(14) TF_CASE(15) TF_CASE(16)
+#undef TF_CASE
+    default:
+      return 0;
+  }
+}
+
+}  // namespace tfk

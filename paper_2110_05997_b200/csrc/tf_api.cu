@@ -1,0 +1,485 @@
+// C-ABI of the dGN evaluation hot path (include/tf.h): argument validation, context and workspace
+// management, work decomposition and launch orchestration. No arithmetic of the method happens here;
+// every step runs in the kernels of k_eval.cu / k_small.cu.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tf.h"
+#include "tf_internal.h"
+
+using namespace tfk;
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+struct tf_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int nsm = 148;
+  std::string err;
+  DevBuf gAp, gBp, gCp, fp;                 // eval partials
+  DevBuf gram_part;                         // Gram split-K partials
+  DevBuf mvG, mvS, mvPi, mvD, mvPart;       // matvec / CG scratch
+  DevBuf cgR, cgP, cgZ, cgState;            // CG vectors and state
+  DevBuf hostW, hostGrad, hostGradTmp, hostF, hostStage[2];  // host-streamed eval
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
+  CgState* cg_host = nullptr;               // pinned
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used_pairs = 0;
+  int64_t eval_launches = 0;
+  int64_t total_launches = 0;
+};
+
+namespace {
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+tf_status set_err(tf_ctx* c, tf_status s, const std::string& msg) {
+  if (c) c->err = msg;
+  return s;
+}
+
+tf_status cuda_err(tf_ctx* c, cudaError_t e, const char* where) {
+  return set_err(c, TF_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define TF_CUDA(c, expr)                                      \
+  do {                                                        \
+    cudaError_t e_ = (expr);                                  \
+    if (e_ != cudaSuccess) return cuda_err((c), e_, #expr);   \
+  } while (0)
+
+tf_status ensure(tf_ctx* c, DevBuf& b, size_t bytes) {
+  if (bytes == 0) bytes = 8;
+  if (b.cap >= bytes) return TF_OK;
+  if (b.p) {
+    cudaStreamSynchronize(c->stream);
+    cudaFree(b.p);
+    b.p = nullptr;
+    b.cap = 0;
+  }
+  cudaError_t e = cudaMalloc(&b.p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(c, TF_ERR_ALLOC, "workspace allocation of " + std::to_string(bytes) + " bytes failed: " +
+                                        cudaGetErrorString(e));
+  }
+  b.cap = bytes;
+  return TF_OK;
+}
+
+void free_buf(DevBuf& b) {
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+}
+
+tf_status check_dims(tf_ctx* c, tf_dims& d) {
+  if (!c) return TF_ERR_ARG;
+  if (d.ldT == 0) d.ldT = d.I;
+  if (d.K_total == 0) d.K_total = d.K + d.k_begin;
+  if (d.I < 1 || d.J < 1 || d.K < 1 || d.R < 1)
+    return set_err(c, TF_ERR_ARG, "dimensions must be >= 1 (I=" + std::to_string(d.I) + " J=" +
+                                      std::to_string(d.J) + " K=" + std::to_string(d.K) +
+                                      " R=" + std::to_string(d.R) + ")");
+  if (d.ldT < d.I) return set_err(c, TF_ERR_ARG, "ldT < I");
+  if (d.k_begin < 0 || d.k_begin + d.K > d.K_total) return set_err(c, TF_ERR_ARG, "k_begin + K > K_total");
+  if (d.R > TF_MAX_R) return set_err(c, TF_ERR_UNSUPPORTED, "R > TF_MAX_R (" + std::to_string(TF_MAX_R) + ")");
+  if (d.I > (1LL << 31) - 1 || d.J > (1LL << 31) - 1 || d.K_total > (1LL << 31) - 1)
+    return set_err(c, TF_ERR_UNSUPPORTED, "mode size >= 2^31");
+  return TF_OK;
+}
+
+Modes make_modes(const tf_dims& d, const double* w) {
+  Modes m;
+  m.R = d.R;
+  m.n[0] = d.I;
+  m.n[1] = d.J;
+  m.n[2] = d.K_total;
+  m.off[0] = 0;
+  m.off[1] = d.I * d.R;
+  m.off[2] = (d.I + d.J) * d.R;
+  for (int l = 0; l < 3; ++l) m.W[l] = w + m.off[l];
+  return m;
+}
+
+// Choose the number of k-chunks per (i-tile, j-tile): minimise waves * (slices per chunk + overhead),
+// where one CTA is resident per SM (the fused kernel uses ~190 KB of shared memory).
+int choose_ksplit(int64_t tiles, int64_t K, int nsm) {
+  const double overhead = 2.0;  // prologue + partial write-out, in slice-iterations
+  int best = 1;
+  double best_cost = 1e300;
+  const int64_t kmax = std::min<int64_t>(K, 4096);
+  for (int64_t ks = 1; ks <= kmax; ++ks) {
+    const int64_t chunk = (K + ks - 1) / ks;
+    const int64_t used = (K + chunk - 1) / chunk;  // non-empty chunks
+    if (used != ks) continue;
+    const int64_t units = tiles * ks;
+    const int64_t waves = (units + nsm - 1) / nsm;
+    const double cost = (double)waves * ((double)chunk + overhead);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = (int)ks;
+    }
+  }
+  return best;
+}
+
+tf_status grams_impl(tf_ctx* c, const tf_dims& d, const double* w, double* grams) {
+  Modes m = make_modes(d, w);
+  tf_status s = ensure(c, c->gram_part, (size_t)gram_partial_slots(m) * 3 * d.R * d.R * 8);
+  if (s) return s;
+  TF_CUDA(c, launch_grams_ws(m, (double*)c->gram_part.p, grams, c->stream));
+  c->total_launches += 2;
+  return TF_OK;
+}
+
+tf_status eval_impl(tf_ctx* c, const tf_dims& d, const double* T, const double* w, double* f, double* grad) {
+  const int NT = (int)((d.R + 7) / 8);
+  const int RP = 8 * NT;
+  EvalArgs p;
+  p.A = w;
+  p.B = w + d.I * d.R;
+  p.C = w + (d.I + d.J) * d.R;
+  p.I = d.I;
+  p.J = d.J;
+  p.K = d.K;
+  p.R = d.R;
+  p.ldT = d.ldT;
+  p.Ktot = d.K_total;
+  p.kbeg = d.k_begin;
+  p.nTi = (int)((d.I + 63) / 64);
+  p.nTj = (int)((d.J + 63) / 64);
+  p.Ipad = (int64_t)p.nTi * 64;
+  p.Jpad = (int64_t)p.nTj * 64;
+  const int64_t tiles = (int64_t)p.nTi * p.nTj;
+  p.kSplit = choose_ksplit(tiles, d.K, c->nsm);
+  p.kChunk = (d.K + p.kSplit - 1) / p.kSplit;
+  p.nCta = (int)(tiles * p.kSplit);
+  tf_status s;
+  if ((s = ensure(c, c->gAp, (size_t)p.nTj * p.kSplit * p.Ipad * RP * 8))) return s;
+  if ((s = ensure(c, c->gBp, (size_t)p.nTi * p.kSplit * p.Jpad * RP * 8))) return s;
+  if ((s = ensure(c, c->gCp, (size_t)tiles * d.K * RP * 8))) return s;
+  if ((s = ensure(c, c->fp, (size_t)p.nCta * 8))) return s;
+  p.gAp = (double*)c->gAp.p;
+  p.gBp = (double*)c->gBp.p;
+  p.gCp = (double*)c->gCp.p;
+  p.fp = (double*)c->fp.p;
+
+  CUtensorMap map;
+  memset(&map, 0, sizeof(map));
+  bool tma = (d.ldT % 2 == 0) && ((reinterpret_cast<uintptr_t>(T) & 15) == 0);
+  if (tma) {
+    EncodeTiledFn enc = get_encode_fn();
+    if (!enc) {
+      tma = false;
+    } else {
+      cuuint64_t gdim[3] = {(cuuint64_t)d.I, (cuuint64_t)d.J, (cuuint64_t)d.K};
+      cuuint64_t gstride[2] = {(cuuint64_t)d.ldT * 8, (cuuint64_t)d.ldT * d.J * 8};
+      cuuint32_t box[3] = {68, 64, 1};
+      cuuint32_t estr[3] = {1, 1, 1};
+      CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(T), gdim, gstride, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) tma = false;
+    }
+  }
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->timing) {
+    if (c->ev_used_pairs * 2 + 2 > c->ev_pool.size()) {
+      for (int i = 0; i < 64; ++i) {
+        cudaEvent_t ev;
+        TF_CUDA(c, cudaEventCreate(&ev));
+        c->ev_pool.push_back(ev);
+      }
+    }
+    e0 = c->ev_pool[c->ev_used_pairs * 2];
+    e1 = c->ev_pool[c->ev_used_pairs * 2 + 1];
+    c->ev_used_pairs++;
+    TF_CUDA(c, cudaEventRecord(e0, c->stream));
+  }
+  TF_CUDA(c, launch_eval(&map, T, p, NT, tma, c->stream));
+  if (c->timing) TF_CUDA(c, cudaEventRecord(e1, c->stream));
+  TF_CUDA(c, launch_eval_finalize(p, RP, f, grad, c->nsm, c->stream));
+  c->eval_launches += 1;
+  c->total_launches += 2;
+  return TF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tf_version(void) { return 1; }
+
+const char* tf_status_str(tf_status s) {
+  switch (s) {
+    case TF_OK: return "TF_OK";
+    case TF_ERR_ARG: return "TF_ERR_ARG";
+    case TF_ERR_ALIGN: return "TF_ERR_ALIGN";
+    case TF_ERR_UNSUPPORTED: return "TF_ERR_UNSUPPORTED";
+    case TF_ERR_CUDA: return "TF_ERR_CUDA";
+    case TF_ERR_NONFINITE: return "TF_ERR_NONFINITE";
+    case TF_ERR_ALLOC: return "TF_ERR_ALLOC";
+  }
+  return "TF_ERR_UNKNOWN";
+}
+
+const char* tf_last_error(const tf_ctx* ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
+
+tf_status tf_ctx_create(tf_ctx** out, int device, void* cuda_stream) {
+  if (!out) return TF_ERR_ARG;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return TF_ERR_CUDA;
+  }
+  if (cudaSetDevice(device) != cudaSuccess) return TF_ERR_CUDA;
+  tf_ctx* c = new tf_ctx();
+  c->device = device;
+  c->stream = static_cast<cudaStream_t>(cuda_stream);
+  cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device);
+  if (cudaMallocHost(&c->cg_host, sizeof(CgState)) != cudaSuccess) {
+    delete c;
+    return TF_ERR_ALLOC;
+  }
+  *out = c;
+  return TF_OK;
+}
+
+tf_status tf_ctx_destroy(tf_ctx* c) {
+  if (!c) return TF_ERR_ARG;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  DevBuf* bufs[] = {&c->gAp, &c->gBp, &c->gCp, &c->fp, &c->gram_part, &c->mvG, &c->mvS, &c->mvPi, &c->mvD,
+                    &c->mvPart, &c->cgR, &c->cgP, &c->cgZ, &c->cgState, &c->hostW, &c->hostGrad,
+                    &c->hostGradTmp, &c->hostF, &c->hostStage[0], &c->hostStage[1]};
+  for (DevBuf* b : bufs) free_buf(*b);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    if (c->ev_copied[i]) cudaEventDestroy(c->ev_copied[i]);
+    if (c->ev_used[i]) cudaEventDestroy(c->ev_used[i]);
+  }
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  if (c->cg_host) cudaFreeHost(c->cg_host);
+  delete c;
+  return TF_OK;
+}
+
+tf_status tf_ctx_set_stream(tf_ctx* c, void* s) {
+  if (!c) return TF_ERR_ARG;
+  c->stream = static_cast<cudaStream_t>(s);
+  return TF_OK;
+}
+
+tf_status tf_ctx_set_timing(tf_ctx* c, int enable) {
+  if (!c) return TF_ERR_ARG;
+  c->timing = enable != 0;
+  return TF_OK;
+}
+
+tf_status tf_ctx_kernel_stats(tf_ctx* c, double* ms, int64_t* eval_launches, int64_t* total, int reset) {
+  if (!c) return TF_ERR_ARG;
+  cudaSetDevice(c->device);
+  TF_CUDA(c, cudaStreamSynchronize(c->stream));
+  double t = 0.0;
+  for (size_t i = 0; i < c->ev_used_pairs; ++i) {
+    float x = 0.f;
+    TF_CUDA(c, cudaEventElapsedTime(&x, c->ev_pool[2 * i], c->ev_pool[2 * i + 1]));
+    t += x;
+  }
+  if (ms) *ms = t;
+  if (eval_launches) *eval_launches = (int64_t)c->ev_used_pairs;
+  if (total) *total = c->total_launches;
+  if (reset) {
+    c->ev_used_pairs = 0;
+    c->total_launches = 0;
+    c->eval_launches = 0;
+  }
+  return TF_OK;
+}
+
+tf_status tf_grams(tf_ctx* c, tf_dims d, const double* w, double* grams) {
+  tf_status s = check_dims(c, d);
+  if (s) return s;
+  if (!w || !grams) return set_err(c, TF_ERR_ARG, "null pointer");
+  cudaSetDevice(c->device);
+  return grams_impl(c, d, w, grams);
+}
+
+tf_status tf_hadamard(tf_ctx* c, int64_t R, const double* grams, double* pi) {
+  if (!c) return TF_ERR_ARG;
+  if (R < 1 || !grams || !pi) return set_err(c, TF_ERR_ARG, "bad argument");
+  cudaSetDevice(c->device);
+  TF_CUDA(c, launch_hadamard(R, grams, pi, c->stream));
+  c->total_launches += 1;
+  return TF_OK;
+}
+
+tf_status tf_cpd_eval(tf_ctx* c, tf_dims d, const double* T, const double* w, double* f, double* grad,
+                      double* grams) {
+  tf_status s = check_dims(c, d);
+  if (s) return s;
+  if (!T || !w || !f || !grad) return set_err(c, TF_ERR_ARG, "null pointer");
+  if (reinterpret_cast<uintptr_t>(T) & 7) return set_err(c, TF_ERR_ALIGN, "T not 8-byte aligned");
+  cudaSetDevice(c->device);
+  if ((s = eval_impl(c, d, T, w, f, grad))) return s;
+  if (grams) return grams_impl(c, d, w, grams);
+  return TF_OK;
+}
+
+tf_status tf_cpd_eval_host(tf_ctx* c, tf_dims d, const double* T_host, const double* w_host, double* f_host,
+                           double* grad_host) {
+  tf_status s = check_dims(c, d);
+  if (s) return s;
+  if (!T_host || !w_host || !f_host || !grad_host) return set_err(c, TF_ERR_ARG, "null pointer");
+  cudaSetDevice(c->device);
+  const int64_t n = d.R * (d.I + d.J + d.K_total);
+  const size_t slice_bytes = (size_t)d.ldT * d.J * 8;
+  const size_t slab_target = (size_t)512 << 20;
+  int64_t kslab = std::max<int64_t>(1, (int64_t)(slab_target / slice_bytes));
+  kslab = std::min<int64_t>(kslab, d.K);
+  if ((s = ensure(c, c->hostW, n * 8))) return s;
+  if ((s = ensure(c, c->hostGrad, n * 8))) return s;
+  if ((s = ensure(c, c->hostGradTmp, n * 8))) return s;
+  if ((s = ensure(c, c->hostF, 16))) return s;
+  for (int i = 0; i < 2; ++i)
+    if ((s = ensure(c, c->hostStage[i], kslab * slice_bytes))) return s;
+  if (!c->copy_stream) TF_CUDA(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    if (!c->ev_copied[i]) TF_CUDA(c, cudaEventCreateWithFlags(&c->ev_copied[i], cudaEventDisableTiming));
+    if (!c->ev_used[i]) TF_CUDA(c, cudaEventCreateWithFlags(&c->ev_used[i], cudaEventDisableTiming));
+  }
+  double* wd = (double*)c->hostW.p;
+  double* gacc = (double*)c->hostGrad.p;
+  double* gtmp = (double*)c->hostGradTmp.p;
+  double* fd = (double*)c->hostF.p;  // fd[0] accumulated f, fd[1] per-slab f
+  TF_CUDA(c, cudaMemcpyAsync(wd, w_host, n * 8, cudaMemcpyHostToDevice, c->stream));
+  TF_CUDA(c, cudaMemsetAsync(gacc, 0, n * 8, c->stream));
+  TF_CUDA(c, cudaMemsetAsync(fd, 0, 16, c->stream));
+  // the copy stream must not overwrite a stage before the compute stream is done with it
+  TF_CUDA(c, cudaEventRecord(c->ev_used[0], c->stream));
+  TF_CUDA(c, cudaEventRecord(c->ev_used[1], c->stream));
+  int slab = 0;
+  for (int64_t k0 = 0; k0 < d.K; k0 += kslab, ++slab) {
+    const int64_t kn = std::min<int64_t>(kslab, d.K - k0);
+    const int b = slab & 1;
+    TF_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->ev_used[b], 0));
+    TF_CUDA(c, cudaMemcpyAsync(c->hostStage[b].p, T_host + (size_t)k0 * d.ldT * d.J, kn * slice_bytes,
+                               cudaMemcpyHostToDevice, c->copy_stream));
+    TF_CUDA(c, cudaEventRecord(c->ev_copied[b], c->copy_stream));
+    TF_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_copied[b], 0));
+    tf_dims ds = d;
+    ds.K = kn;
+    ds.k_begin = d.k_begin + k0;
+    if ((s = eval_impl(c, ds, (const double*)c->hostStage[b].p, wd, fd + 1, gtmp))) return s;
+    TF_CUDA(c, cudaEventRecord(c->ev_used[b], c->stream));
+    TF_CUDA(c, launch_axpy1(n, gtmp, gacc, c->stream));
+    TF_CUDA(c, launch_axpy1(1, fd + 1, fd, c->stream));
+    c->total_launches += 2;
+  }
+  TF_CUDA(c, cudaMemcpyAsync(grad_host, gacc, n * 8, cudaMemcpyDeviceToHost, c->stream));
+  TF_CUDA(c, cudaMemcpyAsync(f_host, fd, 8, cudaMemcpyDeviceToHost, c->stream));
+  TF_CUDA(c, cudaStreamSynchronize(c->stream));
+  return TF_OK;
+}
+
+static tf_status matvec_ws(tf_ctx* c, const tf_dims& d, const Modes& m, MatvecWs& ws) {
+  const size_t RR = (size_t)d.R * d.R;
+  tf_status s;
+  if ((s = ensure(c, c->mvG, 3 * RR * 8))) return s;
+  if ((s = ensure(c, c->mvS, 3 * RR * 8))) return s;
+  if ((s = ensure(c, c->mvPi, 6 * RR * 8))) return s;
+  if ((s = ensure(c, c->mvD, 3 * d.R * 8))) return s;
+  const size_t part = (size_t)gram_partial_slots(m) * 3 * RR + (size_t)cg_partial_slots(m) + 16;
+  if ((s = ensure(c, c->mvPart, part * 8))) return s;
+  ws.G = (double*)c->mvG.p;
+  ws.S = (double*)c->mvS.p;
+  ws.pi = (double*)c->mvPi.p;
+  ws.dscale = (double*)c->mvD.p;
+  ws.partial = (double*)c->mvPart.p;
+  ws.nblk_dot = cg_partial_slots(m);
+  return TF_OK;
+}
+
+tf_status tf_gn_matvec(tf_ctx* c, tf_dims d, const double* grams, const double* w, const double* v, double lambda,
+                       double* y) {
+  tf_status s = check_dims(c, d);
+  if (s) return s;
+  if (!grams || !w || !v || !y) return set_err(c, TF_ERR_ARG, "null pointer");
+  if (v == y) return set_err(c, TF_ERR_ARG, "y must not alias v");
+  cudaSetDevice(c->device);
+  Modes m = make_modes(d, w);
+  MatvecWs ws;
+  if ((s = matvec_ws(c, d, m, ws))) return s;
+  TF_CUDA(c, launch_hadamard(d.R, grams, ws.pi, c->stream));
+  TF_CUDA(c, launch_matvec(m, v, lambda, ws, false, y, c->stream));
+  c->total_launches += 4;
+  return TF_OK;
+}
+
+tf_status tf_cg_solve(tf_ctx* c, tf_dims d, const double* grams, const double* w, const double* rhs, double lambda,
+                      int maxiter, double tol, int jacobi, double* x, int* iters_done, double* res2) {
+  tf_status s = check_dims(c, d);
+  if (s) return s;
+  if (!grams || !w || !rhs || !x) return set_err(c, TF_ERR_ARG, "null pointer");
+  if (maxiter < 0) return set_err(c, TF_ERR_ARG, "maxiter < 0");
+  cudaSetDevice(c->device);
+  Modes m = make_modes(d, w);
+  const int64_t n = d.R * (d.I + d.J + d.K_total);
+  MatvecWs ws;
+  if ((s = matvec_ws(c, d, m, ws))) return s;
+  if ((s = ensure(c, c->cgR, n * 8))) return s;
+  if ((s = ensure(c, c->cgP, n * 8))) return s;
+  if ((s = ensure(c, c->cgZ, n * 8))) return s;
+  if ((s = ensure(c, c->cgState, sizeof(CgState)))) return s;
+  double* r = (double*)c->cgR.p;
+  double* p = (double*)c->cgP.p;
+  double* z = (double*)c->cgZ.p;
+  CgState* st = (CgState*)c->cgState.p;
+  TF_CUDA(c, cudaMemsetAsync(st, 0, sizeof(CgState), c->stream));
+  TF_CUDA(c, launch_hadamard(d.R, grams, ws.pi, c->stream));
+  if (jacobi) TF_CUDA(c, launch_jacobi_scale(m, ws.pi, lambda, ws.dscale, c->stream));
+  double* dotp = ws.partial + (size_t)gram_partial_slots(m) * 3 * d.R * d.R;
+  TF_CUDA(c, launch_cg_init(n, rhs, jacobi ? ws.dscale : nullptr, m, x, r, p, dotp, ws.nblk_dot, st, c->stream));
+  c->total_launches += 2 + (jacobi ? 1 : 0);
+  for (int i = 0; i < maxiter; ++i) {
+    TF_CUDA(c, launch_cg_iteration(m, lambda, ws, jacobi != 0, tol, x, r, p, z, st, c->stream));
+    c->total_launches += 5;
+  }
+  TF_CUDA(c, launch_cg_finish(n, m, ws.dscale, jacobi != 0, x, c->stream));
+  if (jacobi) c->total_launches += 1;
+  TF_CUDA(c, cudaMemcpyAsync(c->cg_host, st, sizeof(CgState), cudaMemcpyDeviceToHost, c->stream));
+  TF_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (iters_done) *iters_done = c->cg_host->iters;
+  if (res2) *res2 = c->cg_host->rr;
+  if (c->cg_host->nonfinite)
+    return set_err(c, TF_ERR_NONFINITE,
+                   "CG: non-finite alpha/beta at iteration " + std::to_string(c->cg_host->nonfinite));
+  return TF_OK;
+}
+
+}  // extern "C"

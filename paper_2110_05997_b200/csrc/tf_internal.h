@@ -1,0 +1,81 @@
+// Internal declarations shared by the C-ABI host code and the kernels.
+#pragma once
+#include <algorithm>
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace tfk {
+
+struct EvalArgs {
+  const double* A;  // I x R column-major
+  const double* B;  // J x R
+  const double* C;  // K_total x R
+  int64_t I, J, K, R, ldT, Ktot, kbeg;
+  int nTi, nTj, kSplit, nCta;
+  int64_t kChunk, Ipad, Jpad;
+  double* gAp;  // [nTj*kSplit][Ipad][RP]
+  double* gBp;  // [nTi*kSplit][Jpad][RP]
+  double* gCp;  // [nTi*nTj][K][RP]
+  double* fp;   // [nCta]
+};
+
+cudaError_t launch_eval(const CUtensorMap* map, const double* T, const EvalArgs& p, int NT, bool tma,
+                        cudaStream_t st);
+cudaError_t launch_eval_finalize(const EvalArgs& p, int RP, double* f, double* grad, int nsm, cudaStream_t st);
+size_t eval_smem_bytes(int NT);
+
+// ---- small kernels (k_small.cu)
+struct Modes {
+  const double* W[3];
+  int64_t n[3];
+  int64_t off[3];  // offsets of the modes in a packed vector
+  int64_t R;
+};
+
+// grams[l] = W_l^T W_l (3 R x R, column-major); Gpart: gram_partial_slots(m) * 3 R^2 doubles of scratch
+cudaError_t launch_grams_ws(const Modes& m, double* Gpart, double* grams, cudaStream_t st);
+int gram_partial_slots(const Modes& m);
+int matvec_blocks(const Modes& m);
+int cg_partial_slots(const Modes& m);
+// pi = [Pi1 | Pi2 | Pi3 | Pi12 | Pi13 | Pi23]
+cudaError_t launch_hadamard(int64_t R, const double* grams, double* pi, cudaStream_t st);
+
+struct CgState {
+  double rr;      // ||r||^2 (current)
+  double alpha, beta, pz;
+  double rr0;
+  int iters;
+  int done;       // 1 once ||r||^2 < tol or non-finite
+  int nonfinite;  // iteration index (1-based) at which alpha/beta became non-finite, else 0
+  unsigned int counter;
+  unsigned int counter2;
+};
+
+struct MatvecWs {
+  double* G;       // 3 R x R : V_l^T W_l
+  double* S;       // 3 R x R : sum_{l' != l} Pi^(l,l') * G_l'
+  double* pi;      // 6 R x R
+  double* dscale;  // 3R : Jacobi scale per (mode, r) (1 if no Jacobi)
+  double* partial; // per-block partial sums
+  int nblk_dot;
+};
+
+// y = D (V Pi + W S + lambda V) with V = D v (D = diag(dscale) or identity).
+// Full matvec: G = V^T W, S, apply.
+cudaError_t launch_matvec(const Modes& m, const double* v, double lambda, const MatvecWs& ws, bool jacobi,
+                          double* y, cudaStream_t st);
+cudaError_t launch_jacobi_scale(const Modes& m, const double* pi, double lambda, double* dscale, cudaStream_t st);
+
+// CG pieces
+cudaError_t launch_cg_init(int64_t n, const double* rhs, const double* dscale, const Modes& m, double* x,
+                           double* r, double* p, double* partial, int nblk, CgState* st_dev, cudaStream_t st);
+cudaError_t launch_cg_iteration(const Modes& m, double lambda, const MatvecWs& ws, bool jacobi, double tol,
+                                double* x, double* r, double* p, double* z, CgState* st_dev, cudaStream_t st);
+cudaError_t launch_cg_finish(int64_t n, const Modes& m, const double* dscale, bool jacobi, double* x,
+                             cudaStream_t st);
+
+// y += x (n doubles), used by the host-streamed evaluation
+cudaError_t launch_axpy1(int64_t n, const double* x, double* y, cudaStream_t st);
+
+}  // namespace tfk

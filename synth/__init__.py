@@ -127,12 +127,14 @@ def _factor(kind: str, R: int, n: int, device, *parts) -> torch.Tensor:
     raise ValueError(kind)
 
 
-def _clean_slab(A_t, B_t, C_t, k0, k1) -> torch.Tensor:
+def _outer_BA(A_t, B_t) -> torch.Tensor:
+    """(R, J*I) rows b_r ⊗ a_r (i fastest) — the clean slice k is sum_r c_kr (b_r ⊗ a_r)."""
+    return (B_t[:, :, None] * A_t[:, None, :]).reshape(A_t.shape[0], -1)
+
+
+def _clean_slab(BA, C_t, k0, k1, J, I) -> torch.Tensor:
     """Clean slices [[A,B,C]][:, :, k0:k1] as a (k1-k0, J, I) tensor (workload recipe)."""
-    # (kb, J, I) = sum_r C[k,r] * B[j,r] * A[i,r]
-    Ck = C_t[:, k0:k1]                                   # (R, kb)
-    BA = (B_t[:, :, None] * A_t[:, None, :]).reshape(A_t.shape[0], -1)   # (R, J*I)
-    return (Ck.transpose(0, 1) @ BA).reshape(k1 - k0, B_t.shape[1], A_t.shape[1])
+    return (C_t[:, k0:k1].transpose(0, 1) @ BA).reshape(k1 - k0, J, I)
 
 
 @dataclass
@@ -174,10 +176,11 @@ def make_problem(name: str, device="cpu", seed: int = 0, k_range=None, slab: int
     need_norms = cfg.noise in ("snr_db", "sigma_T_frac")
     clean_sq = 0.0
     noise_sq = 0.0
+    BA = _outer_BA(A_t, B_t)
     if need_norms:
         for s0 in range(0, K, slab):
             s1 = min(K, s0 + slab)
-            X = _clean_slab(A_t, B_t, C_t, s0, s1)
+            X = _clean_slab(BA, C_t, s0, s1, J, I)
             clean_sq += float(torch.sum(X * X))
             if cfg.noise == "snr_db":
                 for k in range(s0, s1):
@@ -198,10 +201,11 @@ def make_problem(name: str, device="cpu", seed: int = 0, k_range=None, slab: int
     T = torch.empty((k1 - k0, J, I), dtype=torch.float64, device=dev)
     for s0 in range(k0, k1, slab):
         s1 = min(k1, s0 + slab)
-        T[s0 - k0:s1 - k0] = _clean_slab(A_t, B_t, C_t, s0, s1)
+        T[s0 - k0:s1 - k0] = _clean_slab(BA, C_t, s0, s1, J, I)
         for k in range(s0, s1):
             T[k - k0] += sigma * randn((J, I), dev, seed, name, "noise", k)
 
+    del BA
     pts = {}
     for p in cfg.points:
         if p == "true":

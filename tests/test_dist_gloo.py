@@ -1,0 +1,102 @@
+"""The K-sharded multi-rank path on CPU (gloo, world_size 2 and 3): partition, packing and the single
+SUM all-reduce of [grad | f] reproduce the full evaluation. The per-rank evaluator here is the oracle
+(tests may call it); the product passes the CUDA evaluator through the same ShardedEvaluator."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _oracle_eval_fn(d, T, w, f, g):
+    import oracle
+    I, J, K, R, Kt, k0 = d.I, d.J, d.K, d.R, d.K_total, d.k_begin
+    wn = w.numpy()
+    A = wn[:I * R]
+    B = wn[I * R:(I + J) * R]
+    C = wn[(I + J) * R:].reshape(R, Kt)[:, k0:k0 + K].reshape(-1)
+    fl, gl = oracle.cpd_eval(T.numpy().reshape(-1), np.concatenate([A, B, C]), I, J, K, R)
+    out = np.zeros(R * (I + J + Kt))
+    out[:(I + J) * R] = gl[:(I + J) * R]
+    out[(I + J) * R:].reshape(R, Kt)[:, k0:k0 + K] = gl[(I + J) * R:].reshape(R, K)
+    g.copy_(torch.from_numpy(out))
+    f.fill_(fl)
+
+
+def _worker(rank, world, port, dims, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import synth
+        from paper_2110_05997_b200.dist import ShardedEvaluator, shard_range
+        I, J, K, R = dims
+        k0, k1 = shard_range(K, rank, world)
+        P = synth.make_problem("c2", "cpu", dims=dims, k_range=(k0, k1))
+        ev = ShardedEvaluator(I, J, K, R, eval_fn=_oracle_eval_fn)
+        assert (ev.k0, ev.k1) == (k0, k1)
+        f, g = ev(P.T, P.w("random"))
+        q.put((rank, float(f.item()), g.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,dims", [(2, (13, 11, 7, 3)), (3, (9, 10, 8, 4))])
+def test_k_sharded_allreduce_gloo(world, dims):
+    pytest.importorskip("paper_2110_05997_b200")
+    import oracle
+    import synth
+    ctxm = mp.get_context("spawn")
+    q = ctxm.Queue()
+    port = _free_port()
+    procs = [ctxm.Process(target=_worker, args=(r, world, port, dims, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    I, J, K, R = dims
+    P = synth.make_problem("c2", "cpu", dims=dims)
+    fr, gr = oracle.cpd_eval(P.T.numpy().reshape(-1), P.w("random").numpy(), I, J, K, R)
+    for rank, f, g in res:
+        assert abs(f - fr) <= 1e-12 * abs(fr)
+        np.testing.assert_allclose(g, gr, rtol=1e-11, atol=1e-12 * np.abs(gr).max())
+    # every rank holds the identical reduced result
+    for _, f, g in res[1:]:
+        assert f == res[0][1] and np.array_equal(g, res[0][2])
+
+
+def test_shard_ranges_cover_and_balance():
+    from paper_2110_05997_b200.dist import shard_range
+    import synth
+    for K in (1, 7, 400, 500, 1200):
+        for world in (1, 2, 3, 4, 8):
+            rs = [shard_range(K, r, world) for r in range(world)]
+            assert rs[0][0] == 0 and rs[-1][1] == K
+            assert all(rs[i][1] == rs[i + 1][0] for i in range(world - 1))
+            sizes = [b - a for a, b in rs]
+            assert max(sizes) - min(sizes) <= 1
+            assert rs == [synth.shard_range(K, r, world) for r in range(world)]
+
+
+def test_sharded_generation_is_bit_identical():
+    """A K-shard generated alone equals the same slices of the full tensor (synth counter-based noise)."""
+    import synth
+    full = synth.make_problem("c3", "cpu", dims=(12, 9, 10, 3))
+    part = synth.make_problem("c3", "cpu", dims=(12, 9, 10, 3), k_range=(4, 7))
+    assert torch.equal(full.T[4:7], part.T)
+    assert torch.equal(full.w("random"), part.w("random"))

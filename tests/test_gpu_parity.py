@@ -1,0 +1,351 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle, element by element.
+
+Bar (north_star): relative error <= 1e-10 in fp64, ‖Δ‖/max(‖ref‖, floor) with the
+floors of DESIGN.md reading R14 (active only where the reference is ~0).
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from parity_util import TOL, f_floor, grad_floor, rel_err, to_np, within
+
+pytestmark = pytest.mark.gpu
+
+tf = pytest.importorskip("paper_2110_05997_b200")
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    c = tf.Context(0)
+    yield c
+    c.close()
+
+
+def run_eval(ctx, T_t, w_t, I, J, K, R, **kw):
+    d = tf.Dims(I, J, K, R, **kw)
+    T = T_t.cuda().contiguous()
+    w = w_t.cuda().contiguous()
+    f, g = ctx.tf_cpd_eval(d, T, w)
+    torch.cuda.synchronize()
+    return float(f.item()), to_np(g)
+
+
+def check_eval(ctx, T_np, w_np, I, J, K, R, tol=TOL):
+    T_t = torch.from_numpy(np.ascontiguousarray(T_np, dtype=np.float64))
+    w_t = torch.from_numpy(np.ascontiguousarray(w_np, dtype=np.float64))
+    f, g = run_eval(ctx, T_t, w_t, I, J, K, R)
+    fr, gr = oracle.cpd_eval(T_np, w_np, I, J, K, R)
+    okf, ef, bf = within([f], [fr], f_floor(T_np, fr), tol)
+    okg, eg, bg = within(g, gr, grad_floor(w_np, I, J, K, R), tol)
+    assert okf, ("f", ef, bf, f, fr)
+    assert okg, ("grad", eg, bg)
+    return ef, eg
+
+
+# ------------------------------------------------------------------------- configs c1, c2 (full oracle)
+@pytest.mark.parametrize("point", ["true", "perturbed"])
+def test_c1_eval(ctx, point):
+    P = synth.make_problem("c1", "cpu")
+    c = P.cfg
+    check_eval(ctx, to_np(P.T).reshape(-1), to_np(P.w(point)), c.I, c.J, c.K, c.R)
+
+
+def test_c2_eval(ctx):
+    P = synth.make_problem("c2", "cpu")
+    c = P.cfg
+    check_eval(ctx, to_np(P.T).reshape(-1), to_np(P.w("random")), c.I, c.J, c.K, c.R)
+
+
+@pytest.mark.parametrize("name,dims", [("c3", (130, 70, 40, 20)), ("c4", (200, 90, 33, 50)),
+                                       ("c5", (100, 77, 21, 100))])
+def test_reduced_recipes_eval(ctx, name, dims):
+    """c3-c5 recipes at sizes the oracle finishes in seconds, spanning several tiles and a ragged tail."""
+    P = synth.make_problem(name, "cpu", dims=dims)
+    I, J, K, R = dims
+    for point, w in P.points.items():
+        check_eval(ctx, to_np(P.T).reshape(-1), to_np(w), I, J, K, R)
+
+
+# ------------------------------------------------------------------------- shapes and edge cases
+@pytest.mark.parametrize("dims", [(1, 1, 1, 1), (2, 3, 1, 1), (64, 64, 2, 8), (65, 63, 3, 9), (3, 5, 7, 2),
+                                  (7, 129, 5, 4), (128, 1, 2, 16), (20, 20, 20, 128), (66, 70, 4, 104)])
+def test_shapes(ctx, dims):
+    I, J, K, R = dims
+    rng = np.random.default_rng(sum(dims))
+    T = rng.standard_normal(I * J * K)
+    w = rng.standard_normal(R * (I + J + K))
+    check_eval(ctx, T, w, I, J, K, R)
+
+
+def test_padded_leading_dimension(ctx):
+    """ldT > I (both an even ldT -> TMA path and an odd ldT -> cooperative-load path)."""
+    I, J, K, R = 30, 17, 6, 5
+    rng = np.random.default_rng(5)
+    t = rng.standard_normal((K, J, I))
+    w = rng.standard_normal(R * (I + J + K))
+    fr, gr = oracle.cpd_eval(t.reshape(-1), w, I, J, K, R)
+    for ldT in (32, 33):
+        Tp = np.zeros((K, J, ldT))
+        Tp[:, :, :I] = t
+        Tp[:, :, I:] = 1e300   # padding must never be read
+        Tt = torch.from_numpy(Tp.reshape(-1)).cuda()
+        f, g = ctx.tf_cpd_eval(tf.Dims(I, J, K, R, ldT=ldT), Tt, torch.from_numpy(w).cuda())
+        assert rel_err([f.item()], [fr]) <= TOL
+        assert rel_err(to_np(g), gr) <= TOL
+
+
+def test_k_sharded_partials_sum_to_full(ctx):
+    """shard partials [grad | f] summed elementwise equal the full evaluation."""
+    I, J, K, R = 50, 40, 23, 6
+    rng = np.random.default_rng(11)
+    t = rng.standard_normal((K, J, I))
+    w = torch.from_numpy(rng.standard_normal(R * (I + J + K))).cuda()
+    Tt = torch.from_numpy(t).cuda()
+    f_full, g_full = ctx.tf_cpd_eval(tf.Dims(I, J, K, R), Tt, w)
+    acc_f = torch.zeros(1, dtype=torch.float64, device="cuda")
+    acc_g = torch.zeros_like(g_full)
+    for world in (2, 3, 5):
+        acc_f.zero_()
+        acc_g.zero_()
+        for rank in range(world):
+            k0, k1 = synth.shard_range(K, rank, world)
+            f, g = ctx.tf_cpd_eval(tf.Dims(I, J, k1 - k0, R, K_total=K, k_begin=k0), Tt[k0:k1].contiguous(), w)
+            # rows of dF/dC outside the shard are exactly zero
+            gC = g[(I + J) * R:].view(R, K)
+            assert torch.all(gC[:, :k0] == 0) and torch.all(gC[:, k1:] == 0)
+            acc_f += f
+            acc_g += g
+        assert rel_err(to_np(acc_f), to_np(f_full)) <= 1e-12
+        assert rel_err(to_np(acc_g), to_np(g_full)) <= 1e-12
+    fr, gr = oracle.cpd_eval(t.reshape(-1), to_np(w), I, J, K, R)
+    assert rel_err(to_np(acc_g), gr) <= TOL
+
+
+def test_deterministic_bitwise(ctx):
+    P = synth.make_problem("c2", "cpu", dims=(96, 80, 50, 10))
+    T = P.T.cuda()
+    w = P.w("random").cuda()
+    d = tf.Dims(96, 80, 50, 10)
+    f1, g1 = ctx.tf_cpd_eval(d, T, w)
+    f1, g1 = f1.clone(), g1.clone()
+    for _ in range(3):
+        f2, g2 = ctx.tf_cpd_eval(d, T, w)
+        assert torch.equal(f1, f2) and torch.equal(g1, g2)
+
+
+def test_host_streamed_eval_matches_device(ctx):
+    P = synth.make_problem("c2", "cpu", dims=(64, 50, 40, 7))
+    d = tf.Dims(64, 50, 40, 7)
+    fh, gh = ctx.tf_cpd_eval_host(d, P.T.contiguous(), P.w("random").contiguous())
+    fr, gr = oracle.cpd_eval(to_np(P.T).reshape(-1), to_np(P.w("random")), 64, 50, 40, 7)
+    assert rel_err(to_np(fh), [fr]) <= TOL
+    assert rel_err(to_np(gh), gr) <= TOL
+
+
+# ------------------------------------------------------------------------- paper fixtures
+def _w_of(A, B, C):
+    return np.concatenate([A.T.reshape(-1), B.T.reshape(-1), C.T.reshape(-1)])
+
+
+def test_warmup_fixture(ctx, golden_dir):
+    g = json.load(open(os.path.join(golden_dir, "warmup.json")))
+    x, y = np.array(g["x"]), np.array(g["y"])
+    z = np.array(g["z_num"], dtype=np.float64) / g["z_den"]
+    X, Y, Z = np.meshgrid(x, y, z, indexing="ij")
+    t = (np.cos(1 - X) * np.sin(1 + Y ** 2) - np.sin(1 + X ** 2) * np.exp(X ** 2 + Y ** 2 + Z ** 2)
+         - np.cos(X) * np.log(1 + Z))
+    T = np.ascontiguousarray(t.transpose(2, 1, 0)).reshape(-1)
+    A = np.stack([np.cos(1 - x), -np.sin(1 + x ** 2) * np.exp(x ** 2), -np.cos(x)], axis=1)
+    B = np.stack([np.sin(1 + y ** 2), np.exp(y ** 2), np.ones_like(y)], axis=1)
+    C = np.stack([np.ones_like(z), np.exp(z ** 2), np.log(1 + z)], axis=1)
+    # at the true factors F and grad are ~0: the bound is the fp64 floor (reading R14)
+    check_eval(ctx, T, _w_of(A, B, C), 6, 5, 4, 3)
+    # at the paper's printed final CPD
+    Xp, Yp, Zp = (np.array(g[k]) for k in ("printed_X", "printed_Y", "printed_Z"))
+    check_eval(ctx, T, _w_of(Xp, Yp, Zp), 6, 5, 4, 3)
+
+
+@pytest.mark.parametrize("n", [10.0, 1000.0])
+def test_border_rank_fixture(ctx, n):
+    I, J, K = 3, 4, 2
+    e = lambda m, k: np.eye(m)[:, k]
+    t = (np.einsum("i,j,k->ijk", e(I, 0), e(J, 0), e(K, 1)) + np.einsum("i,j,k->ijk", e(I, 0), e(J, 1), e(K, 0))
+         + np.einsum("i,j,k->ijk", e(I, 1), e(J, 0), e(K, 0)))
+    A = np.stack([n * (e(I, 0) + e(I, 1) / n), -n * e(I, 0)], axis=1)
+    B = np.stack([e(J, 0) + e(J, 1) / n, e(J, 0)], axis=1)
+    C = np.stack([e(K, 0) + e(K, 1) / n, e(K, 0)], axis=1)
+    T = np.ascontiguousarray(t.transpose(2, 1, 0)).reshape(-1)
+    f, _ = run_eval(ctx, torch.from_numpy(T), torch.from_numpy(_w_of(A, B, C)), I, J, K, 2)
+    ref = 0.5 * (3.0 / n ** 2 + 1.0 / n ** 4)
+    assert abs(f - ref) <= 1e-10 * ref
+    check_eval(ctx, T, _w_of(A, B, C), I, J, K, 2)
+
+
+# ------------------------------------------------------------------------- Grams, Hadamard, matvec, CG
+def test_grams_and_hadamard(ctx):
+    I, J, K, R = 300, 45, 70, 37
+    rng = np.random.default_rng(3)
+    w = rng.standard_normal(R * (I + J + K))
+    d = tf.Dims(I, J, K, R)
+    wt = torch.from_numpy(w).cuda()
+    g = ctx.tf_grams(d, wt)
+    pi = ctx.tf_hadamard(R, g)
+    gr = oracle.grams(w, I, J, K, R)
+    assert rel_err(to_np(g), gr) <= TOL
+    assert rel_err(to_np(pi), oracle.hadamard_chains(gr, R)) <= TOL
+    # grams as the optional output of tf_cpd_eval
+    T = torch.from_numpy(rng.standard_normal(I * J * K)).cuda()
+    g2 = torch.empty_like(g)
+    ctx.tf_cpd_eval(d, T, wt, grams=g2)
+    assert torch.equal(g, g2)
+
+
+@pytest.mark.parametrize("dims", [(20, 20, 20, 3), (200, 200, 200, 10), (500, 300, 40, 20), (120, 80, 60, 100)])
+@pytest.mark.parametrize("lam", [0.0, 1e-3])
+def test_gn_matvec(ctx, dims, lam):
+    I, J, K, R = dims
+    rng = np.random.default_rng(I + R)
+    w = rng.standard_normal(R * (I + J + K))
+    v = rng.standard_normal(R * (I + J + K))
+    d = tf.Dims(I, J, K, R)
+    wt = torch.from_numpy(w).cuda()
+    g = ctx.tf_grams(d, wt)
+    y = ctx.tf_gn_matvec(d, g, wt, torch.from_numpy(v).cuda(), lam)
+    ref = oracle.gn_matvec_hv(w, v, lam, I, J, K, R)
+    assert rel_err(to_np(y), ref) <= TOL
+
+
+def test_gn_matvec_against_plain_route(ctx):
+    """Against the oracle's J-then-J^T route (no Grams) on c1."""
+    P = synth.make_problem("c1", "cpu")
+    c = P.cfg
+    w = to_np(P.w("perturbed"))
+    v = to_np(synth.random_vector(c.n, "cpu", "c1-matvec"))
+    d = tf.Dims(c.I, c.J, c.K, c.R)
+    wt = torch.from_numpy(w).cuda()
+    y = ctx.tf_gn_matvec(d, ctx.tf_grams(d, wt), wt, torch.from_numpy(v).cuda(), 1e-3)
+    assert rel_err(to_np(y), oracle.gn_matvec_plain(w, v, 1e-3, c.I, c.J, c.K, c.R)) <= TOL
+
+
+@pytest.mark.parametrize("jacobi", [False, True])
+@pytest.mark.parametrize("case", ["c1", "c3r"])
+def test_cg_per_iteration(ctx, case, jacobi):
+    """Every CG iterate x^(i), i = 1..10, against Alg. CG-dGN in the oracle (rhs = -grad, lambda = 1e-3)."""
+    if case == "c1":
+        P = synth.make_problem("c1", "cpu")
+        I, J, K, R = 20, 20, 20, 3
+        w = to_np(P.w("perturbed"))
+    else:
+        P = synth.make_problem("c3", "cpu", dims=(60, 50, 40, 20))
+        I, J, K, R = 60, 50, 40, 20
+        w = to_np(P.w("random"))
+    T = to_np(P.T).reshape(-1)
+    _, grad = oracle.cpd_eval(T, w, I, J, K, R)
+    rhs = -grad
+    lam = 1e-3
+    ref = oracle.cg(w, rhs, lam, 10, I, J, K, R, jacobi=jacobi, history=True)
+    d = tf.Dims(I, J, K, R)
+    wt = torch.from_numpy(w).cuda()
+    g = ctx.tf_grams(d, wt)
+    rt = torch.from_numpy(rhs).cuda()
+    for i in range(1, ref["iters"] + 1):
+        x, it, r2 = ctx.tf_cg_solve(d, g, wt, rt, lam, i, 0.0, jacobi)
+        assert it == i
+        e = rel_err(to_np(x), ref["x_hist"][i - 1])
+        assert e <= 1e-9, (i, e)      # CG drift grows with conditioning (SURVEY.md §7 hard part 10)
+        assert abs(r2 - ref["r2"][i - 1]) <= 1e-8 * ref["r2"][0]
+
+
+def test_cg_tolerance_stop(ctx):
+    P = synth.make_problem("c1", "cpu")
+    I, J, K, R = 20, 20, 20, 3
+    w = to_np(P.w("perturbed"))
+    _, grad = oracle.cpd_eval(to_np(P.T).reshape(-1), w, I, J, K, R)
+    d = tf.Dims(I, J, K, R)
+    wt = torch.from_numpy(w).cuda()
+    g = ctx.tf_grams(d, wt)
+    ref = oracle.cg(w, -grad, 1e-3, 200, I, J, K, R, tol=1e-6)
+    x, it, r2 = ctx.tf_cg_solve(d, g, wt, torch.from_numpy(-grad).cuda(), 1e-3, 200, 1e-6, False)
+    assert it == ref["iters"] and r2 < 1e-6
+    assert rel_err(to_np(x), ref["x"]) <= 1e-8
+
+
+# ------------------------------------------------------------------------- errors
+def test_argument_errors(ctx):
+    w = torch.zeros(30, dtype=torch.float64, device="cuda")
+    T = torch.zeros(8, dtype=torch.float64, device="cuda")
+    with pytest.raises(tf.TfError) as ei:
+        ctx.tf_cpd_eval(tf.Dims(2, 2, 2, 0), T, w)
+    assert ei.value.status == tf.TF_ERR_ARG
+    with pytest.raises(tf.TfError) as ei:
+        ctx.tf_cpd_eval(tf.Dims(2, 2, 2, 1, ldT=1), T, w)
+    assert ei.value.status == tf.TF_ERR_ARG
+    with pytest.raises(tf.TfError) as ei:
+        ctx.tf_cpd_eval(tf.Dims(2, 2, 2, 1, K_total=3, k_begin=2), T, w)
+    assert ei.value.status == tf.TF_ERR_ARG
+    big = torch.zeros(200 * 6, dtype=torch.float64, device="cuda")
+    with pytest.raises(tf.TfError) as ei:
+        ctx.tf_cpd_eval(tf.Dims(2, 2, 2, 200), T, big)
+    assert ei.value.status == tf.TF_ERR_UNSUPPORTED
+
+
+# ------------------------------------------------------------------------- full sizes, sampled outputs
+def _sampled_full_size(ctx, name, point, n_rows=2):
+    P = synth.make_problem(name, "cuda")
+    c = P.cfg
+    I, J, K, R = c.I, c.J, c.K, c.R
+    d = tf.Dims(I, J, K, R)
+    w = P.w(point)
+    f, g = ctx.tf_cpd_eval(d, P.T, w)
+    g = to_np(g)
+    wn = to_np(w)
+    A = wn[:I * R].reshape(R, I).T
+    B = wn[I * R:(I + J) * R].reshape(R, J).T
+    C = wn[(I + J) * R:].reshape(R, K).T
+    gA = g[:I * R].reshape(R, I).T
+    gB = g[I * R:(I + J) * R].reshape(R, J).T
+    gC = g[(I + J) * R:].reshape(R, K).T
+    rng = np.random.default_rng(7)
+    scale = float(np.linalg.norm(g))
+    for i in list(rng.choice(I, n_rows, replace=False)) + [I - 1]:
+        S = P.T[:, :, i].cpu().numpy().T          # (J, K) horizontal slice T[i,:,:]
+        _, row = oracle.slice_eval(S, A[i], B, C)
+        assert np.linalg.norm(gA[i] - row) <= TOL * max(np.linalg.norm(row), scale / math.sqrt(I))
+    for j in list(rng.choice(J, n_rows, replace=False)) + [J - 1]:
+        S = P.T[:, j, :].cpu().numpy().T          # (I, K) lateral slice
+        _, row = oracle.slice_eval(S, B[j], A, C)
+        assert np.linalg.norm(gB[j] - row) <= TOL * max(np.linalg.norm(row), scale / math.sqrt(J))
+    ks = list(rng.choice(K, n_rows, replace=False)) + [K - 1]
+    for k in ks:
+        S = P.T[k].cpu().numpy().T                # (I, J) frontal slice
+        fs, row = oracle.slice_eval(S, C[k], A, B)
+        assert np.linalg.norm(gC[k] - row) <= TOL * max(np.linalg.norm(row), scale / math.sqrt(K))
+        # the objective of one slice through the 1-slice sharded call, in the bench's launch configuration
+        f1, _ = ctx.tf_cpd_eval(tf.Dims(I, J, 1, R, K_total=K, k_begin=int(k)), P.T[k:k + 1], w)
+        assert abs(f1.item() - fs) <= TOL * fs
+    # f = sum of slice objectives (property at any size): compare with the per-slab sharded sum
+    parts = []
+    for k0 in range(0, K, max(1, K // 7)):
+        k1 = min(K, k0 + max(1, K // 7))
+        fp, _ = ctx.tf_cpd_eval(tf.Dims(I, J, k1 - k0, R, K_total=K, k_begin=k0), P.T[k0:k1], w)
+        parts.append(fp.item())
+    assert abs(sum(parts) - f.item()) <= 1e-12 * f.item()
+
+
+@pytest.mark.slow
+def test_c3_full_size_sampled(ctx):
+    _sampled_full_size(ctx, "c3", "true")
+    _sampled_full_size(ctx, "c3", "random")
+
+
+@pytest.mark.slow
+def test_c5_full_size_sampled(ctx):
+    _sampled_full_size(ctx, "c5", "random", n_rows=1)
