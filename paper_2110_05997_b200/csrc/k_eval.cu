@@ -40,16 +40,38 @@ struct EvalSmem {
   static constexpr size_t bytes = off_bar + 2 * 8;
 };
 
+// Butterfly sum over the 4 lanes that share g = lane/4 (lane bits 0..1) of N values per lane;
+// afterwards lane (g, q) holds N/4 sums: value j is index base(q) + j with
+// base(q) = (q>>1&1)*N/2 + (q&1)*N/4. N must be a multiple of 4.
+template <int N>
+__device__ __forceinline__ void butterfly4(double (&v)[N], int q) {
+  constexpr int H1 = N / 2, H2 = N / 4;
+  const bool b1 = (q >> 1) & 1, b0 = q & 1;
+#pragma unroll
+  for (int j = 0; j < H1; ++j) {
+    const double send = b1 ? v[j] : v[H1 + j];
+    const double keep = b1 ? v[H1 + j] : v[j];
+    v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+#pragma unroll
+  for (int j = 0; j < H2; ++j) {
+    const double send = b0 ? v[j] : v[H2 + j];
+    const double keep = b0 ? v[H2 + j] : v[j];
+    v[j] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+  }
+}
+
 template <int NT, bool kTMA>
 __global__ void __launch_bounds__(kThreads, 1)
     k_eval_fused(const __grid_constant__ CUtensorMap tmapT, const double* __restrict__ T, EvalArgs p) {
   using S = EvalSmem<NT>;
   constexpr int RP = S::RP;
   constexpr int LDF = S::LDF;
+  constexpr int NV = ((NT + 3) / 4) * 4;   // gC values per lane, padded for the butterfly
   extern __shared__ __align__(128) unsigned char smem[];
   double* sTE = reinterpret_cast<double*>(smem + S::off_te);
-  double* sA = reinterpret_cast<double*>(smem + S::off_a);
-  double* sB = reinterpret_cast<double*>(smem + S::off_b);
+  double* sAc = reinterpret_cast<double*>(smem + S::off_a);   // -A diag(c_k), rebuilt every slice
+  double* sB = reinterpret_cast<double*>(smem + S::off_b);    // B (unscaled)
   double* sC = reinterpret_cast<double*>(smem + S::off_c);
   double* sGC = reinterpret_cast<double*>(smem + S::off_gc);
   double* sRed = reinterpret_cast<double*>(smem + S::off_red);
@@ -65,7 +87,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t kB = min(p.K, kA + p.kChunk);
   const int nk = (int)max((int64_t)0, kB - kA);
 
-  // ---- prologue: barriers, first T tile, factor tiles, first c row
+  // ---- prologue: barriers, first T tile, B tile, this thread's slice of the A tile, first c row
   if (kTMA && tid == 0) {
     prefetch_tmap(&tmapT);
     mbar_init(&bar[0], 1);
@@ -77,16 +99,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_arrive_expect_tx(&bar[0], kTileBytes);
     tma_load_3d(sTE, &tmapT, (int)i0, (int)j0, (int)kA, &bar[0]);
   }
-  for (int idx = tid; idx < kBI * LDF; idx += kThreads) {
-    const int i = idx / LDF, r = idx % LDF;
-    const int64_t gi = i0 + i;
-    sA[idx] = (gi < p.I && r < p.R) ? p.A[gi + p.I * r] : 0.0;
-  }
   for (int idx = tid; idx < kBJ * LDF; idx += kThreads) {
     const int j = idx / LDF, r = idx % LDF;
     const int64_t gj = j0 + j;
     sB[idx] = (gj < p.J && r < p.R) ? p.B[gj + p.J * r] : 0.0;
   }
+  // Unscaled A, distributed: thread (warp, g, q) owns A[8*warp + 2q + e][8t + g] (the phase-2 P^T
+  // fragment positions), used for dF/dC and to rebuild sAc = -A diag(c_k) each slice.
+  double Areg[NT][2];
+#pragma unroll
+  for (int t = 0; t < NT; ++t)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int64_t gi = i0 + 8 * warp + 2 * q + e;
+      const int r = 8 * t + g;
+      Areg[t][e] = (gi < p.I && r < p.R) ? p.A[gi + p.I * r] : 0.0;
+    }
   if (tid < RP && nk > 0) sC[tid] = (tid < p.R) ? p.C[(p.kbeg + kA) + p.Ktot * tid] : 0.0;
 
   double accA[NT][2], accB[NT][2];
@@ -94,38 +122,46 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int t = 0; t < NT; ++t) accA[t][0] = accA[t][1] = accB[t][0] = accB[t][1] = 0.0;
   double fsum = 0.0;
 
-  // phase-1 warp tile: rows 32*wi.., cols 16*wj..
-  const int wi = warp & 1, wj = warp >> 1;
+  const int wi = warp & 1, wj = warp >> 1;   // phase-1 warp tile: rows 32*wi.., cols 16*wj..
 
   for (int kk = 0; kk < nk; ++kk) {
     const int b = kk & 1;
     const int64_t k = kA + kk;
     double* sT = sTE + b * (kLDE * kBJ);
     const double* sc = sC + b * RP;
-    __syncthreads();  // previous iteration fully done with buffer b^1, sGC, sC[b^1]
+    __syncthreads();  // S3 of the previous slice: buffer b^1, sAc, sGC, sC[b^1] are free
+    if (kk > 0 && tid < RP) {
+      double v = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) v += sGC[w * RP + tid];
+      p.gCp[((int64_t)(it * p.nTj + jt) * p.K + (k - 1)) * RP + tid] = v;
+    }
     if (kk + 1 < nk) {
-      if (kTMA) {
-        if (tid == 0) {
-          fence_proxy_async_smem();
-          mbar_arrive_expect_tx(&bar[b ^ 1], kTileBytes);
-          tma_load_3d(sTE + (b ^ 1) * (kLDE * kBJ), &tmapT, (int)i0, (int)j0, (int)(k + 1), &bar[b ^ 1]);
-        }
+      if (kTMA && tid == 0) {
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&bar[b ^ 1], kTileBytes);
+        tma_load_3d(sTE + (b ^ 1) * (kLDE * kBJ), &tmapT, (int)i0, (int)j0, (int)(k + 1), &bar[b ^ 1]);
       }
       if (tid < RP) sC[(b ^ 1) * RP + tid] = (tid < p.R) ? p.C[(p.kbeg + k + 1) + p.Ktot * tid] : 0.0;
     }
-    if (kTMA) {
-      mbar_wait(&bar[b], (kk >> 1) & 1);
-    } else {
-      // plain cooperative load of the 64 x 64 tile (odd ldT: no TMA)
+    // rebuild sAc = -A diag(c_k) from the register-resident A slice
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const double cr = -sc[8 * t + g];
+      sAc[(8 * warp + 2 * q) * LDF + 8 * t + g] = Areg[t][0] * cr;
+      sAc[(8 * warp + 2 * q + 1) * LDF + 8 * t + g] = Areg[t][1] * cr;
+    }
+    if (!kTMA) {
       for (int idx = tid; idx < kBI * kBJ; idx += kThreads) {
         const int j = idx / kBI, i = idx % kBI;
         const int64_t gi = i0 + i, gj = j0 + j;
         sT[j * kLDE + i] = (gi < p.I && gj < p.J) ? T[gi + p.ldT * (gj + p.J * k)] : 0.0;
       }
-      __syncthreads();
     }
+    __syncthreads();  // S1: sAc (and the non-TMA tile) complete
+    if (kTMA) mbar_wait(&bar[b], (kk >> 1) & 1);
 
-    // ---- phase 1: E = T - A diag(c) B^T on a 32 x 16 warp tile (4 x 2 fragments)
+    // ---- phase 1: E = T + (-A diag(c)) B^T on a 32 x 16 warp tile (4 x 2 fragments), no scaling in the loop
     {
       double E[4][2][2];
 #pragma unroll
@@ -134,14 +170,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int n = 0; n < 2; ++n)
 #pragma unroll
           for (int e = 0; e < 2; ++e) E[m][n][e] = sT[(16 * wj + 8 * n + 2 * q + e) * kLDE + 32 * wi + 8 * m + g];
-#pragma unroll 2
+      const double* pa = sAc + (32 * wi + g) * LDF + q;
+      const double* pb = sB + (16 * wj + g) * LDF + q;
+#pragma unroll
       for (int s = 0; s < RP / 4; ++s) {
-        const double cneg = -sc[4 * s + q];
         double a[4], bb[2];
 #pragma unroll
-        for (int m = 0; m < 4; ++m) a[m] = sA[(32 * wi + 8 * m + g) * LDF + 4 * s + q];
+        for (int m = 0; m < 4; ++m) a[m] = pa[8 * m * LDF + 4 * s];
 #pragma unroll
-        for (int n = 0; n < 2; ++n) bb[n] = sB[(16 * wj + 8 * n + g) * LDF + 4 * s + q] * cneg;
+        for (int n = 0; n < 2; ++n) bb[n] = pb[8 * n * LDF + 4 * s];
 #pragma unroll
         for (int m = 0; m < 4; ++m)
 #pragma unroll
@@ -157,63 +194,70 @@ __global__ void __launch_bounds__(kThreads, 1)
             sT[(16 * wj + 8 * n + 2 * q + e) * kLDE + 32 * wi + 8 * m + g] = E[m][n][e];
           }
     }
-    __syncthreads();  // E tile complete in sT
+    __syncthreads();  // S2: E tile complete in sT
 
-    // ---- phase 2: P = E B for i-rows 8*warp.., all R; accA += P diag(c); gC partial
+    // ---- phase 2: P^T_t = B_t^T E^T for i-cols 8*warp.. (t outer, E fragments held in registers);
+    //      accA^T += diag(c) P^T; gC partial = sum_i A o P
     {
-      double P[NT][2];
+      double ea[kBJ / 4];
 #pragma unroll
-      for (int t = 0; t < NT; ++t) P[t][0] = P[t][1] = 0.0;
-#pragma unroll 4
-      for (int s = 0; s < kBJ / 4; ++s) {
-        const double a = sT[(4 * s + q) * kLDE + 8 * warp + g];
+      for (int s = 0; s < kBJ / 4; ++s) ea[s] = sT[(4 * s + q) * kLDE + 8 * warp + g];
+      double gcv[NV];
 #pragma unroll
-        for (int t = 0; t < NT; ++t) dmma(P[t], a, sB[(4 * s + q) * LDF + 8 * t + g]);
-      }
+      for (int j = NT; j < NV; ++j) gcv[j] = 0.0;
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
+        double p0[2] = {0.0, 0.0}, p1[2] = {0.0, 0.0};
+        const double* pbt = sB + q * LDF + 8 * t + g;
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int r = 8 * t + 2 * q + e;
-          accA[t][e] = fma(sc[r], P[t][e], accA[t][e]);
-          double v = sA[(8 * warp + g) * LDF + r] * P[t][e];
-          v += __shfl_xor_sync(0xffffffffu, v, 4);
-          v += __shfl_xor_sync(0xffffffffu, v, 8);
-          v += __shfl_xor_sync(0xffffffffu, v, 16);
-          if (g == 0) sGC[warp * RP + r] = v;
+        for (int s = 0; s < kBJ / 4; s += 2) {
+          dmma(p0, pbt[(4 * s) * LDF], ea[s]);
+          dmma(p1, pbt[(4 * s + 4) * LDF], ea[s + 1]);
         }
+        const double cr = sc[8 * t + g];
+        const double P0 = p0[0] + p1[0], P1 = p0[1] + p1[1];   // P[i = 8w+2q+e][r = 8t+g]
+        accA[t][0] = fma(cr, P0, accA[t][0]);
+        accA[t][1] = fma(cr, P1, accA[t][1]);
+        gcv[t] = fma(Areg[t][0], P0, Areg[t][1] * P1);
+      }
+      butterfly4<NV>(gcv, q);
+      const int base = ((q >> 1) & 1) * (NV / 2) + (q & 1) * (NV / 4);
+#pragma unroll
+      for (int j = 0; j < NV / 4; ++j) {
+        const int t = base + j;
+        if (t < NT) sGC[warp * RP + 8 * t + g] = gcv[j];
       }
     }
 
-    // ---- phase 3: accB^T += (A diag c)^T E for j-cols 8*warp.., all R
+    // ---- phase 3: accB^T += (-A diag c)^T E for j-cols 8*warp.., all R (prescaled sAc: no DMUL)
     {
-      double cv[NT];
-#pragma unroll
-      for (int t = 0; t < NT; ++t) cv[t] = sc[8 * t + g];
+      const double* pe = sT + (8 * warp + g) * kLDE + q;
+      const double* pa = sAc + q * LDF + g;
 #pragma unroll 4
       for (int s = 0; s < kBI / 4; ++s) {
-        const double bb = sT[(8 * warp + g) * kLDE + 4 * s + q];
+        const double bb = pe[4 * s];
 #pragma unroll
-        for (int t = 0; t < NT; ++t) dmma(accB[t], sA[(4 * s + q) * LDF + 8 * t + g] * cv[t], bb);
+        for (int t = 0; t < NT; ++t) dmma(accB[t], pa[4 * s * LDF + 8 * t], bb);
       }
     }
-    __syncthreads();  // sGC complete
-    if (tid < RP) {
-      double v = 0.0;
+  }
+  __syncthreads();
+  if (nk > 0 && tid < RP) {
+    double v = 0.0;
 #pragma unroll
-      for (int w = 0; w < 8; ++w) v += sGC[w * RP + tid];
-      p.gCp[((int64_t)(it * p.nTj + jt) * p.K + k) * RP + tid] = v;
-    }
+    for (int w = 0; w < 8; ++w) v += sGC[w * RP + tid];
+    p.gCp[((int64_t)(it * p.nTj + jt) * p.K + (kB - 1)) * RP + tid] = v;
   }
 
-  // ---- epilogue: partials
+  // ---- epilogue: partials (accA: +sum E B diag c; accB: -sum (A diag c)^T E, i.e. dF/dB directly)
   {
-    const int64_t base = ((int64_t)(jt * p.kSplit + kc) * p.Ipad + i0 + 8 * warp + g) * RP;
 #pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      double2 v = make_double2(accA[t][0], accA[t][1]);
-      *reinterpret_cast<double2*>(&p.gAp[base + 8 * t + 2 * q]) = v;
-    }
+    for (int t = 0; t < NT; ++t)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t i = i0 + 8 * warp + 2 * q + e;
+        p.gAp[((int64_t)(jt * p.kSplit + kc) * p.Ipad + i) * RP + 8 * t + g] = accA[t][e];
+      }
   }
   {
 #pragma unroll
@@ -250,7 +294,7 @@ __global__ void k_eval_finalize(EvalArgs p, int RP, double* __restrict__ f, doub
     } else if (idx < nA + nB) {
       const int64_t q = idx - nA, r = q / p.J, j = q % p.J;
       for (int64_t s = 0; s < nPB; ++s) v += p.gBp[(s * p.Jpad + j) * RP + r];
-      grad[idx] = -v;
+      grad[idx] = v;
     } else {
       const int64_t q = idx - nA - nB, r = q / p.Ktot, kg = q % p.Ktot;
       const int64_t k = kg - p.kbeg;
