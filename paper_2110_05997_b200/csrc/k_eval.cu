@@ -33,11 +33,11 @@ struct EvalSmem {
   static constexpr size_t off_te = 0;                                   // 2 x [64][68] doubles
   static constexpr size_t off_a = off_te + 2 * (size_t)kTileBytes;      // [64][LDF]
   static constexpr size_t off_b = off_a + (size_t)kBI * LDF * 8;        // [64][LDF]
-  static constexpr size_t off_c = off_b + (size_t)kBJ * LDF * 8;        // 2 x [RP]
-  static constexpr size_t off_gc = off_c + 2 * (size_t)RP * 8;          // [8][RP]
-  static constexpr size_t off_red = off_gc + 8 * (size_t)RP * 8;        // [8]
-  static constexpr size_t off_bar = off_red + 8 * 8;                    // 2 mbarriers
-  static constexpr size_t bytes = off_bar + 2 * 8;
+  static constexpr size_t off_c = off_b + (size_t)kBJ * LDF * 8;        // 4 x [RP]  (ring of c_k rows)
+  static constexpr size_t off_gc = off_c + 4 * (size_t)RP * 8;          // 2 x [8][RP] (per-warp dF/dC partials)
+  static constexpr size_t off_red = off_gc + 2 * 8 * (size_t)RP * 8;    // [8]
+  static constexpr size_t off_bar = off_red + 8 * 8;                    // 4 mbarriers: full[2], p3done, aready
+  static constexpr size_t bytes = off_bar + 4 * 8;
 };
 
 // Butterfly sum over the 4 lanes that share g = lane/4 (lane bits 0..1) of N values per lane;
@@ -61,21 +61,38 @@ __device__ __forceinline__ void butterfly4(double (&v)[N], int q) {
   }
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Schedule of one CTA over its slices (one block-wide barrier per slice; the sAc hand-off uses two
+// 8-warp mbarriers whose waits sit after independent work, so they normally cost nothing):
+//   wait full[b] (T_k), wait aready (sAc_k)   | phase 1_k: E = T + sAc B^T, f
+//   __syncthreads (S2_k)                        | E complete; buffers of slice k-1 free -> TMA T_{k+1},
+//                                               | reduce sGC of slice k-1, prefetch c_{k+2}
+//   phase 3_k (reads sAc_k) ; arrive p3done     |
+//   phase 2_k, first half of the r-tiles        |
+//   wait p3done ; rebuild sAc_{k+1} ; arrive aready
+//   phase 2_k, second half ; dF/dC butterfly -> sGC[k%2]
 template <int NT, bool kTMA>
 __global__ void __launch_bounds__(kThreads, 1)
     k_eval_fused(const __grid_constant__ CUtensorMap tmapT, const double* __restrict__ T, EvalArgs p) {
   using S = EvalSmem<NT>;
   constexpr int RP = S::RP;
   constexpr int LDF = S::LDF;
-  constexpr int NV = ((NT + 3) / 4) * 4;   // gC values per lane, padded for the butterfly
+  constexpr int NV = ((NT + 3) / 4) * 4;   // dF/dC values per lane, padded for the butterfly
+  constexpr int NT1 = (NT + 1) / 2;        // r-tiles of phase 2 before the sAc hand-off
   extern __shared__ __align__(128) unsigned char smem[];
   double* sTE = reinterpret_cast<double*>(smem + S::off_te);
-  double* sAc = reinterpret_cast<double*>(smem + S::off_a);   // -A diag(c_k), rebuilt every slice
+  double* sAc = reinterpret_cast<double*>(smem + S::off_a);   // -A diag(c_k)
   double* sB = reinterpret_cast<double*>(smem + S::off_b);    // B (unscaled)
-  double* sC = reinterpret_cast<double*>(smem + S::off_c);
+  double* sC = reinterpret_cast<double*>(smem + S::off_c);    // c_k at sC[(k%4)*RP]
   double* sGC = reinterpret_cast<double*>(smem + S::off_gc);
   double* sRed = reinterpret_cast<double*>(smem + S::off_red);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::off_bar);
+  uint64_t* full = bar;          // [2] TMA completion per T/E buffer
+  uint64_t* p3done = bar + 2;    // all 8 warps finished reading sAc_k (phase 3)
+  uint64_t* aready = bar + 3;    // all 8 warps wrote their rows of sAc_{k+1}
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
   const int bid = blockIdx.x;
@@ -86,26 +103,43 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t kA = (int64_t)kc * p.kChunk;
   const int64_t kB = min(p.K, kA + p.kChunk);
   const int nk = (int)max((int64_t)0, kB - kA);
+  const int ks1 = (int)((p.R + 3) / 4);    // phase-1 k-steps actually needed (R padded to 4, not 8)
 
-  // ---- prologue: barriers, first T tile, B tile, this thread's slice of the A tile, first c row
-  if (kTMA && tid == 0) {
-    prefetch_tmap(&tmapT);
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+  auto load_c = [&](int64_t kloc, int slot) {
+    if (tid < RP) sC[slot * RP + tid] = (tid < p.R) ? p.C[(p.kbeg + kloc) + p.Ktot * tid] : 0.0;
+  };
+  auto load_tile_plain = [&](int64_t kloc, double* dst) {
+    for (int idx = tid; idx < kBI * kBJ; idx += kThreads) {
+      const int j = idx / kBI, i = idx % kBI;
+      const int64_t gi = i0 + i, gj = j0 + j;
+      dst[j * kLDE + i] = (gi < p.I && gj < p.J) ? T[gi + p.ldT * (gj + p.J * kloc)] : 0.0;
+    }
+  };
+
+  // ---- prologue
+  if (tid == 0) {
+    if (kTMA) prefetch_tmap(&tmapT);
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(p3done, 8);
+    mbar_init(aready, 8);
     fence_barrier_init();
   }
   __syncthreads();
-  if (kTMA && tid == 0 && nk > 0) {
-    mbar_arrive_expect_tx(&bar[0], kTileBytes);
-    tma_load_3d(sTE, &tmapT, (int)i0, (int)j0, (int)kA, &bar[0]);
+  if (kTMA && tid == 0) {
+    for (int u = 0; u < 2 && u < nk; ++u) {
+      mbar_arrive_expect_tx(&full[u], kTileBytes);
+      tma_load_3d(sTE + u * (kLDE * kBJ), &tmapT, (int)i0, (int)j0, (int)(kA + u), &full[u]);
+    }
   }
+  if (!kTMA && nk > 0) load_tile_plain(kA, sTE);
   for (int idx = tid; idx < kBJ * LDF; idx += kThreads) {
     const int j = idx / LDF, r = idx % LDF;
     const int64_t gj = j0 + j;
     sB[idx] = (gj < p.J && r < p.R) ? p.B[gj + p.J * r] : 0.0;
   }
-  // Unscaled A, distributed: thread (warp, g, q) owns A[8*warp + 2q + e][8t + g] (the phase-2 P^T
-  // fragment positions), used for dF/dC and to rebuild sAc = -A diag(c_k) each slice.
+  // Unscaled A, distributed over the CTA: thread (warp, g, q) owns A[8*warp + 2q + e][8t + g] (its
+  // phase-2 P^T fragment positions); used for dF/dC and to rebuild sAc = -A diag(c_k) each slice.
   double Areg[NT][2];
 #pragma unroll
   for (int t = 0; t < NT; ++t)
@@ -115,12 +149,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int r = 8 * t + g;
       Areg[t][e] = (gi < p.I && r < p.R) ? p.A[gi + p.I * r] : 0.0;
     }
-  if (tid < RP && nk > 0) sC[tid] = (tid < p.R) ? p.C[(p.kbeg + kA) + p.Ktot * tid] : 0.0;
+  auto rebuild_sAc = [&](const double* c) {
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      const double cr = -c[8 * t + g];
+      sAc[(8 * warp + 2 * q) * LDF + 8 * t + g] = Areg[t][0] * cr;
+      sAc[(8 * warp + 2 * q + 1) * LDF + 8 * t + g] = Areg[t][1] * cr;
+    }
+  };
+  if (nk > 0) {
+    for (int u = 0; u < 2 && u < nk; ++u) load_c(kA + u, u);
+    __syncthreads();
+    rebuild_sAc(sC);
+  }
+  __syncthreads();
 
   double accA[NT][2], accB[NT][2];
 #pragma unroll
   for (int t = 0; t < NT; ++t) accA[t][0] = accA[t][1] = accB[t][0] = accB[t][1] = 0.0;
-  double fsum = 0.0;
+  double fsum0 = 0.0, fsum1 = 0.0;
 
   const int wi = warp & 1, wj = warp >> 1;   // phase-1 warp tile: rows 32*wi.., cols 16*wj..
 
@@ -128,40 +175,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int b = kk & 1;
     const int64_t k = kA + kk;
     double* sT = sTE + b * (kLDE * kBJ);
-    const double* sc = sC + b * RP;
-    __syncthreads();  // S3 of the previous slice: buffer b^1, sAc, sGC, sC[b^1] are free
-    if (kk > 0 && tid < RP) {
-      double v = 0.0;
-#pragma unroll
-      for (int w = 0; w < 8; ++w) v += sGC[w * RP + tid];
-      p.gCp[((int64_t)(it * p.nTj + jt) * p.K + (k - 1)) * RP + tid] = v;
-    }
-    if (kk + 1 < nk) {
-      if (kTMA && tid == 0) {
-        fence_proxy_async_smem();
-        mbar_arrive_expect_tx(&bar[b ^ 1], kTileBytes);
-        tma_load_3d(sTE + (b ^ 1) * (kLDE * kBJ), &tmapT, (int)i0, (int)j0, (int)(k + 1), &bar[b ^ 1]);
-      }
-      if (tid < RP) sC[(b ^ 1) * RP + tid] = (tid < p.R) ? p.C[(p.kbeg + k + 1) + p.Ktot * tid] : 0.0;
-    }
-    // rebuild sAc = -A diag(c_k) from the register-resident A slice
-#pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      const double cr = -sc[8 * t + g];
-      sAc[(8 * warp + 2 * q) * LDF + 8 * t + g] = Areg[t][0] * cr;
-      sAc[(8 * warp + 2 * q + 1) * LDF + 8 * t + g] = Areg[t][1] * cr;
-    }
-    if (!kTMA) {
-      for (int idx = tid; idx < kBI * kBJ; idx += kThreads) {
-        const int j = idx / kBI, i = idx % kBI;
-        const int64_t gi = i0 + i, gj = j0 + j;
-        sT[j * kLDE + i] = (gi < p.I && gj < p.J) ? T[gi + p.ldT * (gj + p.J * k)] : 0.0;
-      }
-    }
-    __syncthreads();  // S1: sAc (and the non-TMA tile) complete
-    if (kTMA) mbar_wait(&bar[b], (kk >> 1) & 1);
+    const double* sc = sC + (kk & 3) * RP;
+    if (kTMA) mbar_wait(&full[b], (kk >> 1) & 1);
+    if (kk > 0) mbar_wait(aready, (kk - 1) & 1);
 
-    // ---- phase 1: E = T + (-A diag(c)) B^T on a 32 x 16 warp tile (4 x 2 fragments), no scaling in the loop
+    // ---- phase 1: E = T + (-A diag(c)) B^T on a 32 x 16 warp tile (4 x 2 fragments)
     {
       double E[4][2][2];
 #pragma unroll
@@ -174,30 +192,64 @@ __global__ void __launch_bounds__(kThreads, 1)
       const double* pb = sB + (16 * wj + g) * LDF + q;
 #pragma unroll
       for (int s = 0; s < RP / 4; ++s) {
-        double a[4], bb[2];
+        if (s < ks1) {
+          double a[4], bb[2];
 #pragma unroll
-        for (int m = 0; m < 4; ++m) a[m] = pa[8 * m * LDF + 4 * s];
+          for (int m = 0; m < 4; ++m) a[m] = pa[8 * m * LDF + 4 * s];
 #pragma unroll
-        for (int n = 0; n < 2; ++n) bb[n] = pb[8 * n * LDF + 4 * s];
+          for (int n = 0; n < 2; ++n) bb[n] = pb[8 * n * LDF + 4 * s];
 #pragma unroll
-        for (int m = 0; m < 4; ++m)
+          for (int m = 0; m < 4; ++m)
 #pragma unroll
-          for (int n = 0; n < 2; ++n) dmma(E[m][n], a[m], bb[n]);
+            for (int n = 0; n < 2; ++n) dmma(E[m][n], a[m], bb[n]);
+        }
       }
 #pragma unroll
       for (int m = 0; m < 4; ++m)
 #pragma unroll
-        for (int n = 0; n < 2; ++n)
+        for (int n = 0; n < 2; ++n) {
+          fsum0 = fma(E[m][n][0], E[m][n][0], fsum0);
+          fsum1 = fma(E[m][n][1], E[m][n][1], fsum1);
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            fsum = fma(E[m][n][e], E[m][n][e], fsum);
-            sT[(16 * wj + 8 * n + 2 * q + e) * kLDE + 32 * wi + 8 * m + g] = E[m][n][e];
-          }
+          for (int e = 0; e < 2; ++e) sT[(16 * wj + 8 * n + 2 * q + e) * kLDE + 32 * wi + 8 * m + g] = E[m][n][e];
+        }
     }
-    __syncthreads();  // S2: E tile complete in sT
+    __syncthreads();  // S2_k: E_k complete; every warp is past phases 2/3 of slice k-1
 
-    // ---- phase 2: P^T_t = B_t^T E^T for i-cols 8*warp.. (t outer, E fragments held in registers);
-    //      accA^T += diag(c) P^T; gC partial = sum_i A o P
+    if (kk + 1 < nk) {
+      if (kTMA) {
+        if (kk >= 1 && tid == 0) {   // slices 0 and 1 were issued in the prologue
+          fence_proxy_async_smem();
+          mbar_arrive_expect_tx(&full[b ^ 1], kTileBytes);
+          tma_load_3d(sTE + (b ^ 1) * (kLDE * kBJ), &tmapT, (int)i0, (int)j0, (int)(k + 1), &full[b ^ 1]);
+        }
+      }
+    }
+    if (kk > 0 && tid < RP) {
+      const double* gsrc = sGC + ((kk - 1) & 1) * 8 * RP;
+      double v = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) v += gsrc[w * RP + tid];
+      p.gCp[((int64_t)(it * p.nTj + jt) * p.K + (k - 1)) * RP + tid] = v;
+    }
+    if (kk + 2 < nk) load_c(k + 2, (kk + 2) & 3);
+
+    // ---- phase 3: accB^T += (-A diag c)^T E for j-cols 8*warp.., all R (prescaled sAc: no DMUL)
+    {
+      const double* pe = sT + (8 * warp + g) * kLDE + q;
+      const double* pa = sAc + q * LDF + g;
+#pragma unroll 4
+      for (int s = 0; s < kBI / 4; ++s) {
+        const double bb = pe[4 * s];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) dmma(accB[t], pa[4 * s * LDF + 8 * t], bb);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(p3done);
+
+    // ---- phase 2: P^T_t = B_t^T E^T for i-cols 8*warp.. (t outer, E fragments in registers);
+    //      accA^T += diag(c) P^T; dF/dC partial = sum_i A o P; the sAc hand-off sits between the halves
     {
       double ea[kBJ / 4];
 #pragma unroll
@@ -207,6 +259,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = NT; j < NV; ++j) gcv[j] = 0.0;
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
+        if (t == NT1 && kk + 1 < nk) {
+          mbar_wait(p3done, kk & 1);          // every warp is done reading sAc_k
+          rebuild_sAc(sC + ((kk + 1) & 3) * RP);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(aready);
+        }
         double p0[2] = {0.0, 0.0}, p1[2] = {0.0, 0.0};
         const double* pbt = sB + q * LDF + 8 * t + g;
 #pragma unroll
@@ -220,55 +278,52 @@ __global__ void __launch_bounds__(kThreads, 1)
         accA[t][1] = fma(cr, P1, accA[t][1]);
         gcv[t] = fma(Areg[t][0], P0, Areg[t][1] * P1);
       }
+      if (NT1 >= NT && kk + 1 < nk) {   // NT == 1: hand-off after the only tile
+        mbar_wait(p3done, kk & 1);
+        rebuild_sAc(sC + ((kk + 1) & 3) * RP);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(aready);
+      }
       butterfly4<NV>(gcv, q);
       const int base = ((q >> 1) & 1) * (NV / 2) + (q & 1) * (NV / 4);
+      double* gdst = sGC + (kk & 1) * 8 * RP + warp * RP;
 #pragma unroll
       for (int j = 0; j < NV / 4; ++j) {
         const int t = base + j;
-        if (t < NT) sGC[warp * RP + 8 * t + g] = gcv[j];
+        if (t < NT) gdst[8 * t + g] = gcv[j];
       }
     }
-
-    // ---- phase 3: accB^T += (-A diag c)^T E for j-cols 8*warp.., all R (prescaled sAc: no DMUL)
-    {
-      const double* pe = sT + (8 * warp + g) * kLDE + q;
-      const double* pa = sAc + q * LDF + g;
-#pragma unroll 4
-      for (int s = 0; s < kBI / 4; ++s) {
-        const double bb = pe[4 * s];
-#pragma unroll
-        for (int t = 0; t < NT; ++t) dmma(accB[t], pa[4 * s * LDF + 8 * t], bb);
-      }
+    if (!kTMA && kk + 1 < nk) {
+      __syncthreads();   // no TMA: everyone is done with buffer b^1 (slice k-1) and with the c ring
+      load_tile_plain(k + 1, sTE + (b ^ 1) * (kLDE * kBJ));
+      __syncthreads();
     }
   }
   __syncthreads();
   if (nk > 0 && tid < RP) {
+    const double* gsrc = sGC + ((nk - 1) & 1) * 8 * RP;
     double v = 0.0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) v += sGC[w * RP + tid];
+    for (int w = 0; w < 8; ++w) v += gsrc[w * RP + tid];
     p.gCp[((int64_t)(it * p.nTj + jt) * p.K + (kB - 1)) * RP + tid] = v;
   }
 
   // ---- epilogue: partials (accA: +sum E B diag c; accB: -sum (A diag c)^T E, i.e. dF/dB directly)
-  {
 #pragma unroll
-    for (int t = 0; t < NT; ++t)
+  for (int t = 0; t < NT; ++t)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int64_t i = i0 + 8 * warp + 2 * q + e;
-        p.gAp[((int64_t)(jt * p.kSplit + kc) * p.Ipad + i) * RP + 8 * t + g] = accA[t][e];
-      }
-  }
-  {
+    for (int e = 0; e < 2; ++e) {
+      const int64_t i = i0 + 8 * warp + 2 * q + e;
+      p.gAp[((int64_t)(jt * p.kSplit + kc) * p.Ipad + i) * RP + 8 * t + g] = accA[t][e];
+    }
 #pragma unroll
-    for (int t = 0; t < NT; ++t)
+  for (int t = 0; t < NT; ++t)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int64_t j = j0 + 8 * warp + 2 * q + e;
-        p.gBp[((int64_t)(it * p.kSplit + kc) * p.Jpad + j) * RP + 8 * t + g] = accB[t][e];
-      }
-  }
-  fsum = warp_sum(fsum);
+    for (int e = 0; e < 2; ++e) {
+      const int64_t j = j0 + 8 * warp + 2 * q + e;
+      p.gBp[((int64_t)(it * p.kSplit + kc) * p.Jpad + j) * RP + 8 * t + g] = accB[t][e];
+    }
+  double fsum = warp_sum(fsum0 + fsum1);
   if (lane == 0) sRed[warp] = fsum;
   __syncthreads();
   if (tid == 0) {

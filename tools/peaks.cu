@@ -41,6 +41,33 @@ __global__ void k_dfma(double* out, int iters) {
   if (s == 12345.678) out[0] = s;
 }
 
+// DMMA and DFMA interleaved in one warp: if the two share the FP64 datapath the mix is no faster
+// than the sum of the parts.
+template <int NACC, int NF>
+__global__ void k_mix(double* out, int iters) {
+  double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+  double c[NACC > 0 ? NACC : 1][2];
+  double x[NF > 0 ? NF : 1];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) { c[i][0] = 0.0; c[i][1] = 0.0; }
+#pragma unroll
+  for (int i = 0; i < NF; ++i) x[i] = i * 1e-3;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < NACC; ++i)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                   : "+d"(c[i][0]), "+d"(c[i][1]) : "d"(a), "d"(b));
+#pragma unroll
+    for (int i = 0; i < NF; ++i) x[i] = fma(x[i], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) s += c[i][0] + c[i][1];
+#pragma unroll
+  for (int i = 0; i < NF; ++i) s += x[i];
+  if (s == 12345.678) out[0] = s;
+}
+
 __global__ void k_read(const double2* __restrict__ p, size_t n, double* out) {
   double s = 0.0;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
@@ -90,6 +117,21 @@ int main(int argc, char** argv) {
     CK(cudaEventRecord(e0)); k_dmma<4><<<g, b>>>(out, iters); CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
     CK(cudaEventElapsedTime(&ms, e0, e1));
     printf(", \"dmma_4chain_ns_per_iter\": %.3f", ms * 1e6 / iters);
+  }
+  {
+    // mix: per iteration 8 DMMA (8*256 FMA per warp-thread-set) + NF DFMA per thread
+    int iters = 4000; dim3 g(nsm * 2), b(512);
+    float t_d, t_f, t_m;
+    k_mix<8, 0><<<g, b>>>(out, 10); CK(cudaDeviceSynchronize());
+    CK(cudaEventRecord(e0)); k_mix<8, 0><<<g, b>>>(out, iters); CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&t_d, e0, e1));
+    k_mix<0, 64><<<g, b>>>(out, 10); CK(cudaDeviceSynchronize());
+    CK(cudaEventRecord(e0)); k_mix<0, 64><<<g, b>>>(out, iters); CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&t_f, e0, e1));
+    k_mix<8, 64><<<g, b>>>(out, 10); CK(cudaDeviceSynchronize());
+    CK(cudaEventRecord(e0)); k_mix<8, 64><<<g, b>>>(out, iters); CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&t_m, e0, e1));
+    printf(", \"mix_dmma_only_ms\": %.3f, \"mix_dfma_only_ms\": %.3f, \"mix_both_ms\": %.3f", t_d, t_f, t_m);
   }
   double best_dfma = 0;
   for (int tpb : {256, 512, 1024}) {
