@@ -12,18 +12,25 @@ hdr, units, vals = rows[0], rows[1], rows[2]
 d = {h: (vals[i], units[i]) for i, h in enumerate(hdr)}
 
 
-def num(k):
+SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+         "ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "msecond": 1.0, "ms": 1.0, "nsecond": 1e-6, "second": 1e3}
+
+
+def num(k, to_base=False):
     try:
-        return float(d[k][0])
+        v = float(d[k][0])
     except Exception:
         return None
+    if to_base:
+        v *= SCALE.get(d[k][1], 1.0)
+    return v
 
 
 out = {
     "kernel": d.get("Kernel Name", ("?",))[0],
-    "gpu__time_duration_ms": num("gpu__time_duration.sum"),
-    "dram_bytes_read": num("dram__bytes_read.sum"),
-    "dram_bytes_write": num("dram__bytes_write.sum"),
+    "gpu__time_duration_ms": num("gpu__time_duration.sum", True),
+    "dram_bytes_read": num("dram__bytes_read.sum", True),
+    "dram_bytes_write": num("dram__bytes_write.sum", True),
     "dmma_pipe_active_pct": num("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active"),
     "tensor_pipe_realtime_pct_elapsed": num("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"),
     "fp64_pipe_pct": num("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
