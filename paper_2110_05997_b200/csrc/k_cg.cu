@@ -1,0 +1,516 @@
+// Persistent cooperative kernels for the Gauss-Newton matvec (Thm Hv, row a8) and Alg. CG-dGN (row a9).
+//
+// One launch runs the whole CG: every block stays resident (cooperative launch, one block per SM) and
+// the iteration is three grid-wide stages separated by grid barriers:
+//   G  (Gram)  G_l = V_l^T W_l,  V = D (r + beta p)           3 R x R outputs, DMMA, fixed-order
+//   Y  (apply) p <- r + beta p;  z = D (V Pi^(l) + W S_l + lambda V) with S_l = sum_{l'!=l} Pi^(l,l') * G_l'
+//              (Thm Hv; three-step Jacobi product PAPER.md:2690-2695); partial <p, z>
+//   U  (update) alpha = ||r||^2 / <p,z>; x += alpha p; r -= alpha z; partial ||r||^2  -> beta next stage
+// All scalars are recomputed by every block from per-block partials summed in a fixed order, so the
+// whole solve is deterministic and needs no host round trip.
+#include <cooperative_groups.h>
+#include <cstdio>
+#include <cstdlib>
+
+#include "tf_internal.h"
+#include "tf_device.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace tfk {
+
+unsigned long long* cg_debug_tstamp();
+constexpr int kCgThreads = 256;
+constexpr int kGramZ = 16;   // max row splits of one Gram output tile
+
+struct CgArgs {
+  Modes m;
+  const double* pi;       // 6 R x R
+  const double* dscale;   // 3R or nullptr
+  double lambda, tol;
+  int maxiter;
+  const double* rhs;      // CG right-hand side (w-coordinates)
+  const double* v;        // matvec input (matvec mode)
+  double* x;              // CG solution / matvec output y
+  double *r, *p, *z;      // CG vectors
+  double* G;              // kGramZ x 3 x R x R Gram partials
+  double* S;              // 3 x R x R
+  double* part;           // 2 * gridDim partials
+  CgState* st;
+  int mode;               // 0 = CG, 1 = single matvec y = (J^T J + lambda I) v
+  unsigned long long* tstamp;   // optional: block-0 globaltimer at each stage boundary (profiling)
+};
+
+__device__ __forceinline__ void stamp(const CgArgs& A, int slot) {
+  if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && slot < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    A.tstamp[slot] = t;
+  }
+}
+
+__device__ __forceinline__ int mode_of(const Modes& m, int64_t q) { return q >= m.off[2] ? 2 : (q >= m.off[1] ? 1 : 0); }
+
+// V element (a, r) of mode l: D_l[r] * (r_vec + beta * p)   (CG)   or   v   (matvec)
+struct VSrc {
+  const double* a;     // r vector or v
+  const double* b;     // p (CG) or nullptr
+  double beta;
+  const double* D;     // dscale or nullptr
+  __device__ __forceinline__ double raw(int64_t q) const { return b ? fma(beta, b[q], a[q]) : a[q]; }
+};
+
+// ---- stage G: G_l[r + R s] = sum_a V_l[a, r] W_l[a, s]; items (l, 32x32 output tile); the 8 warps
+// split the rows, each warp runs 4x4 DMMA fragments straight from L2 with 2 k-steps in flight, and the
+// 8 partial tiles are summed in a fixed order through shared memory (red: 8 x 1024 doubles).
+__device__ __forceinline__ int gram_splits(const Modes& m) {
+  const int nt = (int)((m.R + 31) / 32);
+  return max(1, min(kGramZ, (int)(gridDim.x / (3 * nt * nt))));
+}
+
+__device__ void stage_gram(const CgArgs& A, const VSrc& V, double* red) {
+  const Modes& m = A.m;
+  const int R = (int)m.R;
+  const int nt = (R + 31) / 32;
+  const int Z = gram_splits(m);
+  const int items = 3 * nt * nt * Z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    const int z = item % Z, li = item / Z;
+    const int l = li / (nt * nt), tt = li % (nt * nt);
+    const int r0 = (tt % nt) * 32, s0 = (tt / nt) * 32;
+    const int64_t n = m.n[l];
+    const double* W = m.W[l];
+    const int64_t off = m.off[l];
+    const double* D = V.D ? V.D + l * R : nullptr;
+    double acc[4][4][2] = {};
+    const int64_t rps = ((n + 4 * Z - 1) / (4 * Z)) * 4;          // rows per split
+    const int64_t zb = z * rps, ze = min(n, zb + rps);
+    const int64_t rpw = ((rps + 31) / 32) * 4;                    // rows per warp
+    const int64_t a_begin = zb + warp * rpw, a_end = min(ze, a_begin + rpw);
+    double dr[4];
+    bool rv[4], sv[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = r0 + 8 * i + g, sc = s0 + 8 * i + g;
+      rv[i] = r < R;
+      sv[i] = sc < R;
+      dr[i] = (D && rv[i]) ? D[r] : 1.0;
+    }
+#pragma unroll 4
+    for (int64_t a0 = a_begin; a0 < a_end; a0 += 4) {
+      const int64_t a = a0 + q;
+      const bool ok = a < a_end;
+      double fa[4], fb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        fa[i] = (ok && rv[i]) ? V.raw(off + a + n * (r0 + 8 * i + g)) * dr[i] : 0.0;
+        fb[i] = (ok && sv[i]) ? W[a + n * (s0 + 8 * i + g)] : 0.0;
+      }
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], fa[mi], fb[ni]);
+    }
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) red[warp * 1024 + ((mi * 4 + ni) * 2 + e) * 32 + lane] = acc[mi][ni][e];
+    __syncthreads();
+    for (int idx = threadIdx.x; idx < 1024; idx += blockDim.x) {
+      double sum = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) sum += red[w * 1024 + idx];
+      const int ln = idx & 31, e = (idx >> 5) & 1, ni = (idx >> 6) & 3, mi = (idx >> 8) & 3;
+      const int gg = ln >> 2, qq = ln & 3;
+      const int r = r0 + 8 * mi + gg, c = s0 + 8 * ni + 2 * qq + e;
+      if (r < R && c < R) A.G[((int64_t)z * 3 + l) * R * R + r + (int64_t)R * c] = sum;
+    }
+    __syncthreads();
+  }
+}
+
+// ---- stage S: S_l = sum_{l' != l} Pi^(l,l') * G_l' with G_l' = sum_z Gpart[z][l'] (fixed order).
+__device__ void stage_s(const CgArgs& A) {
+  const int64_t R = A.m.R, RR = R * R;
+  const int Z = gram_splits(A.m);
+  for (int64_t qi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; qi < RR; qi += (int64_t)gridDim.x * blockDim.x) {
+    double gsum[3] = {0.0, 0.0, 0.0};
+    for (int z = 0; z < Z; ++z)
+#pragma unroll
+      for (int l = 0; l < 3; ++l) gsum[l] += A.G[((int64_t)z * 3 + l) * RR + qi];
+    const double p12 = A.pi[3 * RR + qi], p13 = A.pi[4 * RR + qi], p23 = A.pi[5 * RR + qi];
+    A.S[qi] = p12 * gsum[1] + p13 * gsum[2];
+    A.S[RR + qi] = p12 * gsum[0] + p23 * gsum[2];
+    A.S[2 * RR + qi] = p13 * gsum[0] + p23 * gsum[1];
+  }
+}
+
+// ---- stage Y: for rows of mode l: y = D (V Pi^(l) + W S_l + lambda V) with V = D (r + beta p).
+// items (l, YR-row chunk, column half h). The operands of the whole 2R contraction are staged once into
+// shared memory with cp.async (8-byte LDGSTS, zero-fill for padding, all copies of a thread in flight at
+// once): sXr/sXp/sW = rows of r, p, W (YR x R4), sM = [Pi^(l) ; S_l] columns of the half (2R4 x 8*NTH).
+// Warp w: m-tile w % (YR/8), n-tiles w / (YR/8) + (8*8/YR) j. If write_p != nullptr the raw V values (the
+// new CG direction) are written after a block barrier. Returns the block's partial sum of raw(V) . y.
+__device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+               "r"(valid ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+template <int NT>
+__host__ __device__ constexpr int apply_rows() { return NT > 13 ? 16 : 32; }
+
+template <int NT>
+__host__ __device__ constexpr size_t apply_smem_doubles(int R4) {
+  return (size_t)3 * apply_rows<NT>() * (R4 + 4) + (size_t)(2 * R4) * (8 * ((NT + 1) / 2) + 4);
+}
+
+template <int NT>
+__device__ double stage_apply(const CgArgs& A, const VSrc& V, double* y, double* write_p, double* smem) {
+  constexpr int YR = apply_rows<NT>();       // rows per item (32, or 16 for R > 104)
+  constexpr int MT = YR / 8;                 // m-tiles per item
+  constexpr int WG = 8 / MT;                 // warps sharing one m-tile
+  constexpr int NTH = (NT + 1) / 2;          // n-tiles per column half
+  constexpr int NTW = (NTH + WG - 1) / WG;   // n-tiles per warp
+  constexpr int LDM = 8 * NTH + 4;
+  const Modes& m = A.m;
+  const int R = (int)m.R;
+  const int64_t RR = (int64_t)R * R;
+  const int R4 = 4 * ((R + 3) / 4);
+  const int LDX = R4 + 4;                    // 4 mod 8 in doubles -> conflict-free A fragments
+  double* sXr = smem;                        // [YR][LDX]
+  double* sXp = sXr + YR * LDX;
+  double* sW = sXp + YR * LDX;
+  double* sM = sW + YR * LDX;                // [2 R4][LDM]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const int mt = warp % MT, tw = warp / MT;
+  const int nh = NT > 1 ? 2 : 1;
+  int items = 0, chunks[3];
+  for (int l = 0; l < 3; ++l) {
+    chunks[l] = (int)((m.n[l] + YR - 1) / YR) * nh;
+    items += chunks[l];
+  }
+  const double bet = V.b ? V.beta : 0.0;
+  double dsum = 0.0;
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    int l = 0, c = item;
+    while (c >= chunks[l]) {
+      c -= chunks[l];
+      ++l;
+    }
+    const int h = c % nh;
+    const int64_t a0 = (int64_t)(c / nh) * YR;
+    const int64_t n = m.n[l];
+    const int64_t off = m.off[l];
+    const double* W = m.W[l];
+    const double* P = A.pi + l * RR;
+    const double* Sl = A.S + l * RR;
+    const double* D = V.D ? V.D + l * R : nullptr;
+    const int t0 = h * NTH;
+    const int s_lo = 8 * t0;
+    const double* va = V.a + off;
+    const double* vb = V.b ? V.b + off : V.a + off;
+    __syncthreads();   // previous item consumed the staging buffers
+    for (int idx = threadIdx.x; idx < YR * R4; idx += blockDim.x) {
+      const int a = idx % YR, kk = idx / YR;
+      const bool ok = kk < R && a0 + a < n;
+      const int64_t ix = ok ? a0 + a + n * kk : 0;
+      cp_async8(&sXr[a * LDX + kk], va + ix, ok);
+      cp_async8(&sXp[a * LDX + kk], vb + ix, ok && V.b != nullptr);
+      cp_async8(&sW[a * LDX + kk], W + ix, ok);
+    }
+    for (int idx = threadIdx.x; idx < R4 * 8 * NTH; idx += blockDim.x) {
+      const int kk = idx % R4, cc = idx / R4;
+      const bool ok = kk < R && s_lo + cc < R;
+      const int64_t ix = ok ? kk + (int64_t)R * (s_lo + cc) : 0;
+      cp_async8(&sM[kk * LDM + cc], P + ix, ok);
+      cp_async8(&sM[(R4 + kk) * LDM + cc], Sl + ix, ok);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    double acc[NTW][2] = {};
+    const int row = 8 * mt + g;
+    // V Pi^(l): A fragment = D_r (r + beta p)
+#pragma unroll 4
+    for (int ks = 0; ks < R4 / 4; ++ks) {
+      const int r = 4 * ks + q;
+      const double dr = D ? D[min(r, R - 1)] : 1.0;
+      const double fa = dr * fma(bet, sXp[row * LDX + r], sXr[row * LDX + r]);
+#pragma unroll
+      for (int j = 0; j < NTW; ++j) {
+        const int tl = tw + WG * j;
+        if (tl < NTH && t0 + tl < NT) dmma(acc[j], fa, sM[r * LDM + 8 * tl + g]);
+      }
+    }
+    // W S_l
+#pragma unroll 4
+    for (int ks = 0; ks < R4 / 4; ++ks) {
+      const int r = 4 * ks + q;
+      const double fa = sW[row * LDX + r];
+#pragma unroll
+      for (int j = 0; j < NTW; ++j) {
+        const int tl = tw + WG * j;
+        if (tl < NTH && t0 + tl < NT) dmma(acc[j], fa, sM[(R4 + r) * LDM + 8 * tl + g]);
+      }
+    }
+    // epilogue: row a = a0 + 8 mt + g, cols s = 8 (t0 + tl) + 2q + e
+    const int64_t arow = a0 + row;
+    const bool rok = arow < n;
+    double pnew[NTW][2];
+#pragma unroll
+    for (int j = 0; j < NTW; ++j) {
+      const int tl = tw + WG * j;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        pnew[j][e] = 0.0;
+        const int sc = 8 * (t0 + tl) + 2 * q + e;
+        if (tl < NTH && rok && sc < R) {
+          const double pr = fma(bet, sXp[row * LDX + sc], sXr[row * LDX + sc]);
+          const double ds = D ? D[sc] : 1.0;
+          const double yv = ds * fma(A.lambda, ds * pr, acc[j][e]);
+          y[off + arow + n * sc] = yv;
+          dsum = fma(pr, yv, dsum);
+          pnew[j][e] = pr;
+        }
+      }
+    }
+    if (write_p) {
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < NTW; ++j) {
+        const int tl = tw + WG * j;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int sc = 8 * (t0 + tl) + 2 * q + e;
+          if (tl < NTH && rok && sc < R) write_p[off + arow + n * sc] = pnew[j][e];
+        }
+      }
+    }
+  }
+  return dsum;
+}
+
+__device__ __forceinline__ double block_reduce(double v, double* red) {
+  v = warp_sum(v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int i = 0; i < kCgThreads / 32; ++i) t += red[i];
+  __syncthreads();
+  return t;   // every thread gets the same value
+}
+
+// every block sums the per-block partials in the same fixed order
+__device__ __forceinline__ double grid_total(const double* part, double* red) {
+  double v = 0.0;
+  for (int i = threadIdx.x; i < gridDim.x; i += blockDim.x) v += part[i];
+  return block_reduce(v, red);
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kCgThreads, 1) k_cg_persistent(CgArgs A) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double cg_smem[];
+  double* red = cg_smem;
+  const Modes& m = A.m;
+  const int R = (int)m.R;
+  const int64_t n = m.R * (m.n[0] + m.n[1] + m.n[2]);
+  const int64_t tid_g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  double* part0 = A.part;
+  double* part1 = A.part + gridDim.x;
+
+  if (A.mode == 1) {   // single matvec: y = (J^T J + lambda I) v
+    VSrc V{A.v, nullptr, 0.0, nullptr};
+    stage_gram(A, V, red);
+    grid.sync();
+    stage_s(A);
+    grid.sync();
+    stage_apply<NT>(A, V, A.x, nullptr, cg_smem);
+    return;
+  }
+
+  // init: x = 0, r = D rhs, p = 0 (so p_new = r + 0 * p = r), rr = ||r||^2
+  double s = 0.0;
+  for (int64_t qi = tid_g; qi < n; qi += stride) {
+    double d = 1.0;
+    if (A.dscale) {
+      const int l = mode_of(m, qi);
+      d = A.dscale[l * R + (qi - m.off[l]) / m.n[l]];
+    }
+    const double v = A.rhs[qi] * d;
+    A.x[qi] = 0.0;
+    A.r[qi] = v;
+    A.p[qi] = 0.0;
+    s = fma(v, v, s);
+  }
+  s = block_reduce(s, red);
+  if (threadIdx.x == 0) part1[blockIdx.x] = s;
+  grid.sync();
+  double rr = grid_total(part1, red);
+  double beta = 0.0;
+  int iters = 0, nonfinite = 0;
+  for (int it = 1; it <= A.maxiter; ++it) {
+    VSrc V{A.r, A.p, beta, A.dscale};
+    const int sb = 8 * (it - 1);
+    stamp(A, sb + 0);
+    stage_gram(A, V, red);
+    stamp(A, sb + 1);
+    grid.sync();
+    stamp(A, sb + 2);
+    stage_s(A);
+    grid.sync();
+    stamp(A, sb + 3);
+    // z = B p_new, p <- p_new, partial <p, z>
+    const double pz_part = stage_apply<NT>(A, V, A.z, A.p, cg_smem);
+    stamp(A, sb + 4);
+    const double pzb = block_reduce(pz_part, red);
+    if (threadIdx.x == 0) part0[blockIdx.x] = pzb;
+    grid.sync();
+    const double pz = grid_total(part0, red);
+    const double alpha = rr / pz;
+    if (!isfinite(alpha)) {
+      nonfinite = it;
+      break;
+    }
+    stamp(A, sb + 5);
+    double s2 = 0.0;
+    for (int64_t q0 = tid_g; q0 < n; q0 += 4 * stride) {
+      double xp[4], xx[4], xz[4], xr[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t qi = min(q0 + u * stride, n - 1);
+        xp[u] = A.p[qi];
+        xx[u] = A.x[qi];
+        xz[u] = A.z[qi];
+        xr[u] = A.r[qi];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t qi = q0 + u * stride;
+        if (qi < n) {
+          A.x[qi] = fma(alpha, xp[u], xx[u]);
+          const double rn = fma(-alpha, xz[u], xr[u]);
+          A.r[qi] = rn;
+          s2 = fma(rn, rn, s2);
+        }
+      }
+    }
+    s2 = block_reduce(s2, red);
+    if (threadIdx.x == 0) part1[blockIdx.x] = s2;
+    grid.sync();
+    stamp(A, sb + 6);
+    const double rr_new = grid_total(part1, red);
+    beta = rr_new / rr;
+    rr = rr_new;
+    iters = it;
+    if (!isfinite(beta)) {
+      nonfinite = it;
+      break;
+    }
+    if (rr_new < A.tol) break;
+  }
+  // x in w-coordinates: x = D x_hat
+  if (A.dscale) {
+    for (int64_t qi = tid_g; qi < n; qi += stride) {
+      const int l = mode_of(m, qi);
+      A.x[qi] *= A.dscale[l * R + (qi - m.off[l]) / m.n[l]];
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    A.st->rr = rr;
+    A.st->iters = iters;
+    A.st->nonfinite = nonfinite;
+    A.st->done = 1;
+  }
+}
+
+template <int NT>
+static cudaError_t launch_persistent_nt(const CgArgs& a, int nsm, cudaStream_t st) {
+  auto kern = k_cg_persistent<NT>;
+  const int R4 = (int)(4 * ((a.m.R + 3) / 4));
+  const size_t smem = 8 * std::max<size_t>(8 * 1024, apply_smem_doubles<NT>(R4));
+  cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (ea != cudaSuccess) return ea;
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kCgThreads, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  dim3 grid(nsm), block(kCgThreads);
+  CgArgs args = a;
+  void* params[] = {&args};
+  return cudaLaunchCooperativeKernel((const void*)kern, grid, block, params, smem, st);
+}
+
+cudaError_t launch_cg_persistent(const Modes& m, const double* pi, const double* dscale, double lambda, double tol,
+                                 int maxiter, const double* rhs, const double* v, double* x, double* r, double* p,
+                                 double* z, double* G, double* S, double* part, CgState* st_dev, int mode, int nsm,
+                                 cudaStream_t st) {
+  CgArgs a;
+  a.S = S;
+  a.tstamp = cg_debug_tstamp();
+  a.m = m;
+  a.pi = pi;
+  a.dscale = dscale;
+  a.lambda = lambda;
+  a.tol = tol;
+  a.maxiter = maxiter;
+  a.rhs = rhs;
+  a.v = v;
+  a.x = x;
+  a.r = r;
+  a.p = p;
+  a.z = z;
+  a.G = G;
+  a.part = part;
+  a.st = st_dev;
+  a.mode = mode;
+  const int NT = (int)((m.R + 7) / 8);
+  switch (NT) {
+#define TF_CASE(k) \
+  case k:          \
+    return launch_persistent_nt<k>(a, nsm, st);
+    TF_CASE(1) TF_CASE(2) TF_CASE(3) TF_CASE(4) TF_CASE(5) TF_CASE(6) TF_CASE(7) TF_CASE(8)
+    TF_CASE(9) TF_CASE(10) TF_CASE(11) TF_CASE(12) TF_CASE(13) TF_CASE(14) TF_CASE(15) TF_CASE(16)
+#undef TF_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+size_t cg_gram_partial_doubles(int64_t R) { return (size_t)kGramZ * 3 * R * R; }
+
+// Development aid: if TF_CG_TSTAMP is set, block 0 of the persistent CG records %globaltimer at the stage
+// boundaries of the first iterations into a device buffer, printed by tf_cg_debug_dump().
+static unsigned long long* g_tstamp = nullptr;
+unsigned long long* cg_debug_tstamp() {
+  static bool init = false;
+  if (!init) {
+    init = true;
+    if (getenv("TF_CG_TSTAMP")) cudaMalloc(&g_tstamp, 64 * sizeof(unsigned long long));
+  }
+  return g_tstamp;
+}
+
+}  // namespace tfk
+
+extern "C" void tf_cg_debug_dump(void) {
+  if (!tfk::g_tstamp) return;
+  unsigned long long h[64];
+  cudaDeviceSynchronize();
+  cudaMemcpy(h, tfk::g_tstamp, sizeof(h), cudaMemcpyDeviceToHost);
+  for (int it = 0; it < 3; ++it) {
+    const unsigned long long* b = h + 8 * it;
+    printf("iter %d: gram %.2f us, sync %.2f, S+sync %.2f, apply %.2f, sync+alpha %.2f, update %.2f us\n", it + 1,
+           (b[1] - b[0]) * 1e-3, (b[2] - b[1]) * 1e-3, (b[3] - b[2]) * 1e-3, (b[4] - b[3]) * 1e-3,
+           (b[5] - b[4]) * 1e-3, (b[6] - b[5]) * 1e-3);
+  }
+}

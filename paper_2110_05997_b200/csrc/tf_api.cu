@@ -1,6 +1,6 @@
 // C-ABI of the dGN evaluation hot path (include/tf.h): argument validation, context and workspace
 // management, work decomposition and launch orchestration. No arithmetic of the method happens here;
-// every step runs in the kernels of k_eval.cu / k_small.cu.
+// every step runs in the kernels of k_eval.cu, k_cg.cu and k_small.cu.
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -410,11 +410,11 @@ tf_status tf_cpd_eval_host(tf_ctx* c, tf_dims d, const double* T_host, const dou
 static tf_status matvec_ws(tf_ctx* c, const tf_dims& d, const Modes& m, MatvecWs& ws) {
   const size_t RR = (size_t)d.R * d.R;
   tf_status s;
-  if ((s = ensure(c, c->mvG, 3 * RR * 8))) return s;
+  if ((s = ensure(c, c->mvG, cg_gram_partial_doubles(d.R) * 8))) return s;
   if ((s = ensure(c, c->mvS, 3 * RR * 8))) return s;
   if ((s = ensure(c, c->mvPi, 6 * RR * 8))) return s;
   if ((s = ensure(c, c->mvD, 3 * d.R * 8))) return s;
-  const size_t part = (size_t)gram_partial_slots(m) * 3 * RR + (size_t)cg_partial_slots(m) + 16;
+  const size_t part = (size_t)gram_partial_slots(m) * 3 * RR + (size_t)cg_partial_slots(m) + 2 * (size_t)c->nsm + 16;
   if ((s = ensure(c, c->mvPart, part * 8))) return s;
   ws.G = (double*)c->mvG.p;
   ws.S = (double*)c->mvS.p;
@@ -436,8 +436,9 @@ tf_status tf_gn_matvec(tf_ctx* c, tf_dims d, const double* grams, const double* 
   MatvecWs ws;
   if ((s = matvec_ws(c, d, m, ws))) return s;
   TF_CUDA(c, launch_hadamard(d.R, grams, ws.pi, c->stream));
-  TF_CUDA(c, launch_matvec(m, v, lambda, ws, false, y, c->stream));
-  c->total_launches += 4;
+  TF_CUDA(c, launch_cg_persistent(m, ws.pi, nullptr, lambda, 0.0, 0, nullptr, v, y, nullptr, nullptr, nullptr, ws.G,
+                                  ws.S, ws.partial, nullptr, 1, c->nsm, c->stream));
+  c->total_launches += 2;
   return TF_OK;
 }
 
@@ -463,15 +464,9 @@ tf_status tf_cg_solve(tf_ctx* c, tf_dims d, const double* grams, const double* w
   TF_CUDA(c, cudaMemsetAsync(st, 0, sizeof(CgState), c->stream));
   TF_CUDA(c, launch_hadamard(d.R, grams, ws.pi, c->stream));
   if (jacobi) TF_CUDA(c, launch_jacobi_scale(m, ws.pi, lambda, ws.dscale, c->stream));
-  double* dotp = ws.partial + (size_t)gram_partial_slots(m) * 3 * d.R * d.R;
-  TF_CUDA(c, launch_cg_init(n, rhs, jacobi ? ws.dscale : nullptr, m, x, r, p, dotp, ws.nblk_dot, st, c->stream));
+  TF_CUDA(c, launch_cg_persistent(m, ws.pi, jacobi ? ws.dscale : nullptr, lambda, tol, maxiter, rhs, nullptr, x, r, p,
+                                  z, ws.G, ws.S, ws.partial, st, 0, c->nsm, c->stream));
   c->total_launches += 2 + (jacobi ? 1 : 0);
-  for (int i = 0; i < maxiter; ++i) {
-    TF_CUDA(c, launch_cg_iteration(m, lambda, ws, jacobi != 0, tol, x, r, p, z, st, c->stream));
-    c->total_launches += 5;
-  }
-  TF_CUDA(c, launch_cg_finish(n, m, ws.dscale, jacobi != 0, x, c->stream));
-  if (jacobi) c->total_launches += 1;
   TF_CUDA(c, cudaMemcpyAsync(c->cg_host, st, sizeof(CgState), cudaMemcpyDeviceToHost, c->stream));
   TF_CUDA(c, cudaStreamSynchronize(c->stream));
   if (iters_done) *iters_done = c->cg_host->iters;

@@ -36,8 +36,17 @@ struct Modes {
 // grams[l] = W_l^T W_l (3 R x R, column-major); Gpart: gram_partial_slots(m) * 3 R^2 doubles of scratch
 cudaError_t launch_grams_ws(const Modes& m, double* Gpart, double* grams, cudaStream_t st);
 int gram_partial_slots(const Modes& m);
-int matvec_blocks(const Modes& m);
 int cg_partial_slots(const Modes& m);
+cudaError_t launch_jacobi_scale(const Modes& m, const double* pi, double lambda, double* dscale, cudaStream_t st);
+
+struct MatvecWs {
+  double* G;       // Gram partials of the persistent kernel
+  double* S;       // 3 R x R : sum_{l' != l} Pi^(l,l') * G_l'
+  double* pi;      // 6 R x R
+  double* dscale;  // 3R : Jacobi scale per (mode, r)
+  double* partial; // per-block partial sums
+  int nblk_dot;
+};
 // pi = [Pi1 | Pi2 | Pi3 | Pi12 | Pi13 | Pi23]
 cudaError_t launch_hadamard(int64_t R, const double* grams, double* pi, cudaStream_t st);
 
@@ -52,28 +61,13 @@ struct CgState {
   unsigned int counter2;
 };
 
-struct MatvecWs {
-  double* G;       // 3 R x R : V_l^T W_l
-  double* S;       // 3 R x R : sum_{l' != l} Pi^(l,l') * G_l'
-  double* pi;      // 6 R x R
-  double* dscale;  // 3R : Jacobi scale per (mode, r) (1 if no Jacobi)
-  double* partial; // per-block partial sums
-  int nblk_dot;
-};
-
-// y = D (V Pi + W S + lambda V) with V = D v (D = diag(dscale) or identity).
-// Full matvec: G = V^T W, S, apply.
-cudaError_t launch_matvec(const Modes& m, const double* v, double lambda, const MatvecWs& ws, bool jacobi,
-                          double* y, cudaStream_t st);
-cudaError_t launch_jacobi_scale(const Modes& m, const double* pi, double lambda, double* dscale, cudaStream_t st);
-
-// CG pieces
-cudaError_t launch_cg_init(int64_t n, const double* rhs, const double* dscale, const Modes& m, double* x,
-                           double* r, double* p, double* partial, int nblk, CgState* st_dev, cudaStream_t st);
-cudaError_t launch_cg_iteration(const Modes& m, double lambda, const MatvecWs& ws, bool jacobi, double tol,
-                                double* x, double* r, double* p, double* z, CgState* st_dev, cudaStream_t st);
-cudaError_t launch_cg_finish(int64_t n, const Modes& m, const double* dscale, bool jacobi, double* x,
-                             cudaStream_t st);
+// Persistent cooperative CG (mode 0) or single GN matvec y = (J^T J + lambda I) v into x (mode 1).
+// part: 2 * nsm doubles; G: 3 R^2; st_dev receives iters / final ||r||^2 / non-finite iteration.
+cudaError_t launch_cg_persistent(const Modes& m, const double* pi, const double* dscale, double lambda, double tol,
+                                 int maxiter, const double* rhs, const double* v, double* x, double* r, double* p,
+                                 double* z, double* G, double* S, double* part, CgState* st_dev, int mode, int nsm,
+                                 cudaStream_t st);
+size_t cg_gram_partial_doubles(int64_t R);
 
 // y += x (n doubles), used by the host-streamed evaluation
 cudaError_t launch_axpy1(int64_t n, const double* x, double* y, cudaStream_t st);

@@ -208,7 +208,8 @@ def test_grams_and_hadamard(ctx):
     assert torch.equal(g, g2)
 
 
-@pytest.mark.parametrize("dims", [(20, 20, 20, 3), (200, 200, 200, 10), (500, 300, 40, 20), (120, 80, 60, 100)])
+@pytest.mark.parametrize("dims", [(20, 20, 20, 3), (200, 200, 200, 10), (500, 300, 40, 20), (120, 80, 60, 100),
+                                  (61, 47, 33, 120), (7, 5, 3, 1), (1, 1, 1, 9)])
 @pytest.mark.parametrize("lam", [0.0, 1e-3])
 def test_gn_matvec(ctx, dims, lam):
     I, J, K, R = dims
@@ -236,16 +237,20 @@ def test_gn_matvec_against_plain_route(ctx):
 
 
 @pytest.mark.parametrize("jacobi", [False, True])
-@pytest.mark.parametrize("case", ["c1", "c3r"])
+@pytest.mark.parametrize("case", ["c1", "c3r", "r120"])
 def test_cg_per_iteration(ctx, case, jacobi):
     """Every CG iterate x^(i), i = 1..10, against Alg. CG-dGN in the oracle (rhs = -grad, lambda = 1e-3)."""
     if case == "c1":
         P = synth.make_problem("c1", "cpu")
         I, J, K, R = 20, 20, 20, 3
         w = to_np(P.w("perturbed"))
-    else:
+    elif case == "c3r":
         P = synth.make_problem("c3", "cpu", dims=(60, 50, 40, 20))
         I, J, K, R = 60, 50, 40, 20
+        w = to_np(P.w("random"))
+    else:   # R > 104 exercises the 16-row apply tiles of the persistent CG kernel
+        P = synth.make_problem("c5", "cpu", dims=(37, 29, 23, 120))
+        I, J, K, R = 37, 29, 23, 120
         w = to_np(P.w("random"))
     T = to_np(P.T).reshape(-1)
     _, grad = oracle.cpd_eval(T, w, I, J, K, R)
