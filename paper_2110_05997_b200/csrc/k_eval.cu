@@ -20,23 +20,31 @@
 
 namespace tfk {
 
-constexpr int kBI = 64;         // tile rows (i)
-constexpr int kBJ = 64;         // tile cols (j)
-constexpr int kLDE = 68;        // smem leading dim of a T/E tile [j][i]; 68 = 4 mod 16 -> conflict-free frags
-constexpr int kThreads = 256;   // 8 warps
-constexpr int kTileBytes = kLDE * kBJ * 8;   // one TMA box 68 x 64 doubles
+// Tile geometry: a CTA owns a BT x BT tile (BT = 64: 8 warps, 1 CTA/SM; BT = 32: 4 warps, 2 CTAs/SM).
+template <int BT>
+struct EvalTile {
+  static constexpr int BI = BT, BJ = BT;
+  static constexpr int LDE = BT + 4;             // smem leading dim of a T/E tile [j][i]; 4 mod 16 -> conflict-free
+  static constexpr int NW = BT / 8;              // warps: one 8-row i-tile (phase 2) / 8-col j-tile (phase 3) each
+  static constexpr int THREADS = NW * 32;
+  static constexpr int WC = NW / 2;              // phase-1 warp grid 2 x WC
+  static constexpr int MF = BT / 16;             // phase-1 m-fragments per warp (rows BT/2)
+  static constexpr int NF = 2;                   // phase-1 n-fragments per warp (cols 16)
+  static constexpr int TILE_BYTES = LDE * BJ * 8;   // one TMA box LDE x BJ doubles
+};
 
-template <int NT>
+template <int NT, int BT>
 struct EvalSmem {
+  using G = EvalTile<BT>;
   static constexpr int RP = 8 * NT;          // padded rank
   static constexpr int LDF = 8 * NT + 4;     // factor tile leading dim (4 mod 16 in doubles)
-  static constexpr size_t off_te = 0;                                   // 2 x [64][68] doubles
-  static constexpr size_t off_a = off_te + 2 * (size_t)kTileBytes;      // [64][LDF]
-  static constexpr size_t off_b = off_a + (size_t)kBI * LDF * 8;        // [64][LDF]
-  static constexpr size_t off_c = off_b + (size_t)kBJ * LDF * 8;        // 4 x [RP]  (ring of c_k rows)
-  static constexpr size_t off_gc = off_c + 4 * (size_t)RP * 8;          // 2 x [8][RP] (per-warp dF/dC partials)
-  static constexpr size_t off_red = off_gc + 2 * 8 * (size_t)RP * 8;    // [8]
-  static constexpr size_t off_bar = off_red + 8 * 8;                    // 4 mbarriers: full[2], p3done, aready
+  static constexpr size_t off_te = 0;                                     // 2 x [BJ][LDE] doubles
+  static constexpr size_t off_a = off_te + 2 * (size_t)G::TILE_BYTES;     // [BI][LDF]
+  static constexpr size_t off_b = off_a + (size_t)G::BI * LDF * 8;        // [BJ][LDF]
+  static constexpr size_t off_c = off_b + (size_t)G::BJ * LDF * 8;        // 4 x [RP]  (ring of c_k rows)
+  static constexpr size_t off_gc = off_c + 4 * (size_t)RP * 8;            // 2 x [NW][RP] (per-warp dF/dC partials)
+  static constexpr size_t off_red = off_gc + 2 * G::NW * (size_t)RP * 8;  // [NW]
+  static constexpr size_t off_bar = off_red + G::NW * 8;                  // 4 mbarriers: full[2], p3done, aready
   static constexpr size_t bytes = off_bar + 4 * 8;
 };
 
@@ -74,10 +82,14 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 //   phase 2_k, first half of the r-tiles        |
 //   wait p3done ; rebuild sAc_{k+1} ; arrive aready
 //   phase 2_k, second half ; dF/dC butterfly -> sGC[k%2]
-template <int NT, bool kTMA>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int NT, bool kTMA, int BT>
+__global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
     k_eval_fused(const __grid_constant__ CUtensorMap tmapT, const double* __restrict__ T, EvalArgs p) {
-  using S = EvalSmem<NT>;
+  using S = EvalSmem<NT, BT>;
+  using Gm = EvalTile<BT>;
+  constexpr int kBI = Gm::BI, kBJ = Gm::BJ, kLDE = Gm::LDE, NW = Gm::NW, kThreads = Gm::THREADS;
+  constexpr int MF = Gm::MF, NF = Gm::NF;
+  constexpr int kTileBytes = Gm::TILE_BYTES;
   constexpr int RP = S::RP;
   constexpr int LDF = S::LDF;
   constexpr int NV = ((NT + 3) / 4) * 4;   // dF/dC values per lane, padded for the butterfly
@@ -121,8 +133,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (kTMA) prefetch_tmap(&tmapT);
     mbar_init(&full[0], 1);
     mbar_init(&full[1], 1);
-    mbar_init(p3done, 8);
-    mbar_init(aready, 8);
+    mbar_init(p3done, NW);
+    mbar_init(aready, NW);
     fence_barrier_init();
   }
   __syncthreads();
@@ -169,7 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int t = 0; t < NT; ++t) accA[t][0] = accA[t][1] = accB[t][0] = accB[t][1] = 0.0;
   double fsum0 = 0.0, fsum1 = 0.0;
 
-  const int wi = warp & 1, wj = warp >> 1;   // phase-1 warp tile: rows 32*wi.., cols 16*wj..
+  const int wi = warp & 1, wj = warp >> 1;   // phase-1 warp tile: rows (BT/2)*wi.., cols 16*wj..
 
   for (int kk = 0; kk < nk; ++kk) {
     const int b = kk & 1;
@@ -179,39 +191,41 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (kTMA) mbar_wait(&full[b], (kk >> 1) & 1);
     if (kk > 0) mbar_wait(aready, (kk - 1) & 1);
 
-    // ---- phase 1: E = T + (-A diag(c)) B^T on a 32 x 16 warp tile (4 x 2 fragments)
+    // ---- phase 1: E = T + (-A diag(c)) B^T on a (BT/2) x 16 warp tile (MF x 2 fragments)
     {
-      double E[4][2][2];
+      double E[MF][NF][2];
 #pragma unroll
-      for (int m = 0; m < 4; ++m)
+      for (int m = 0; m < MF; ++m)
 #pragma unroll
-        for (int n = 0; n < 2; ++n)
+        for (int n = 0; n < NF; ++n)
 #pragma unroll
-          for (int e = 0; e < 2; ++e) E[m][n][e] = sT[(16 * wj + 8 * n + 2 * q + e) * kLDE + 32 * wi + 8 * m + g];
-      const double* pa = sAc + (32 * wi + g) * LDF + q;
+          for (int e = 0; e < 2; ++e)
+            E[m][n][e] = sT[(16 * wj + 8 * n + 2 * q + e) * kLDE + (kBI / 2) * wi + 8 * m + g];
+      const double* pa = sAc + ((kBI / 2) * wi + g) * LDF + q;
       const double* pb = sB + (16 * wj + g) * LDF + q;
 #pragma unroll
       for (int s = 0; s < RP / 4; ++s) {
         if (s < ks1) {
-          double a[4], bb[2];
+          double a[MF], bb[NF];
 #pragma unroll
-          for (int m = 0; m < 4; ++m) a[m] = pa[8 * m * LDF + 4 * s];
+          for (int m = 0; m < MF; ++m) a[m] = pa[8 * m * LDF + 4 * s];
 #pragma unroll
-          for (int n = 0; n < 2; ++n) bb[n] = pb[8 * n * LDF + 4 * s];
+          for (int n = 0; n < NF; ++n) bb[n] = pb[8 * n * LDF + 4 * s];
 #pragma unroll
-          for (int m = 0; m < 4; ++m)
+          for (int m = 0; m < MF; ++m)
 #pragma unroll
-            for (int n = 0; n < 2; ++n) dmma(E[m][n], a[m], bb[n]);
+            for (int n = 0; n < NF; ++n) dmma(E[m][n], a[m], bb[n]);
         }
       }
 #pragma unroll
-      for (int m = 0; m < 4; ++m)
+      for (int m = 0; m < MF; ++m)
 #pragma unroll
-        for (int n = 0; n < 2; ++n) {
+        for (int n = 0; n < NF; ++n) {
           fsum0 = fma(E[m][n][0], E[m][n][0], fsum0);
           fsum1 = fma(E[m][n][1], E[m][n][1], fsum1);
 #pragma unroll
-          for (int e = 0; e < 2; ++e) sT[(16 * wj + 8 * n + 2 * q + e) * kLDE + 32 * wi + 8 * m + g] = E[m][n][e];
+          for (int e = 0; e < 2; ++e)
+            sT[(16 * wj + 8 * n + 2 * q + e) * kLDE + (kBI / 2) * wi + 8 * m + g] = E[m][n][e];
         }
     }
     __syncthreads();  // S2_k: E_k complete; every warp is past phases 2/3 of slice k-1
@@ -226,10 +240,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (kk > 0 && tid < RP) {
-      const double* gsrc = sGC + ((kk - 1) & 1) * 8 * RP;
+      const double* gsrc = sGC + ((kk - 1) & 1) * NW * RP;
       double v = 0.0;
 #pragma unroll
-      for (int w = 0; w < 8; ++w) v += gsrc[w * RP + tid];
+      for (int w = 0; w < NW; ++w) v += gsrc[w * RP + tid];
       p.gCp[((int64_t)(it * p.nTj + jt) * p.K + (k - 1)) * RP + tid] = v;
     }
     if (kk + 2 < nk) load_c(k + 2, (kk + 2) & 3);
@@ -286,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       butterfly4<NV>(gcv, q);
       const int base = ((q >> 1) & 1) * (NV / 2) + (q & 1) * (NV / 4);
-      double* gdst = sGC + (kk & 1) * 8 * RP + warp * RP;
+      double* gdst = sGC + (kk & 1) * NW * RP + warp * RP;
 #pragma unroll
       for (int j = 0; j < NV / 4; ++j) {
         const int t = base + j;
@@ -301,10 +315,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncthreads();
   if (nk > 0 && tid < RP) {
-    const double* gsrc = sGC + ((nk - 1) & 1) * 8 * RP;
+    const double* gsrc = sGC + ((nk - 1) & 1) * NW * RP;
     double v = 0.0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) v += gsrc[w * RP + tid];
+    for (int w = 0; w < NW; ++w) v += gsrc[w * RP + tid];
     p.gCp[((int64_t)(it * p.nTj + jt) * p.K + (kB - 1)) * RP + tid] = v;
   }
 
@@ -328,37 +342,39 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (tid == 0) {
     double v = 0.0;
-    for (int w = 0; w < 8; ++w) v += sRed[w];
+    for (int w = 0; w < NW; ++w) v += sRed[w];
     p.fp[bid] = v;
   }
 }
 
-// Fixed-order reduction of all partials into the packed gradient and f (row a6).
-// grad = -(sum of partials) (the kernels accumulate +E-contractions; dF/dW = -MTTKRP(E)).
+// Fixed-order reduction of all partials into the packed gradient and f (row a6). Threads run along r
+// (contiguous in the partial buffers) so the partial reads coalesce; the packed gradient writes are strided
+// but small. grad blocks: dF/dA = -sum accA, dF/dB = +sum accB (accB already holds -(A diag c)^T E),
+// dF/dC = -sum gC partials (rows outside the local slices are written 0).
 __global__ void k_eval_finalize(EvalArgs p, int RP, double* __restrict__ f, double* __restrict__ grad) {
-  const int64_t nA = p.I * p.R, nB = p.J * p.R, nC = p.Ktot * p.R;
+  const int64_t R = p.R;
+  const int64_t nA = p.I * R, nB = p.J * R, nC = p.Ktot * R;
   const int64_t total = nA + nB + nC;
   const int64_t nPA = (int64_t)p.nTj * p.kSplit, nPB = (int64_t)p.nTi * p.kSplit, nPC = (int64_t)p.nTi * p.nTj;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     double v = 0.0;
     if (idx < nA) {
-      const int64_t r = idx / p.I, i = idx % p.I;
+      const int64_t i = idx / R, r = idx % R;
       for (int64_t s = 0; s < nPA; ++s) v += p.gAp[(s * p.Ipad + i) * RP + r];
-      grad[idx] = -v;
+      grad[i + p.I * r] = -v;
     } else if (idx < nA + nB) {
-      const int64_t q = idx - nA, r = q / p.J, j = q % p.J;
+      const int64_t qq = idx - nA, j = qq / R, r = qq % R;
       for (int64_t s = 0; s < nPB; ++s) v += p.gBp[(s * p.Jpad + j) * RP + r];
-      grad[idx] = v;
+      grad[nA + j + p.J * r] = v;
     } else {
-      const int64_t q = idx - nA - nB, r = q / p.Ktot, kg = q % p.Ktot;
+      const int64_t qq = idx - nA - nB, kg = qq / R, r = qq % R;
       const int64_t k = kg - p.kbeg;
       if (k >= 0 && k < p.K) {
         for (int64_t s = 0; s < nPC; ++s) v += p.gCp[(s * p.K + k) * RP + r];
-        grad[idx] = -v;
-      } else {
-        grad[idx] = 0.0;
+        v = -v;
       }
+      grad[nA + nB + kg + p.Ktot * r] = v;
     }
   }
   if (blockIdx.x == 0) {
@@ -376,30 +392,43 @@ __global__ void k_eval_finalize(EvalArgs p, int RP, double* __restrict__ f, doub
   }
 }
 
-template <int NT>
+template <int NT, int BT>
 static cudaError_t launch_eval_nt(const CUtensorMap* map, const double* T, const EvalArgs& p, bool tma,
                                   cudaStream_t st) {
-  const size_t smem = EvalSmem<NT>::bytes;
+  const size_t smem = EvalSmem<NT, BT>::bytes;
+  constexpr int threads = EvalTile<BT>::THREADS;
   if (tma) {
-    auto kern = k_eval_fused<NT, true>;
+    auto kern = k_eval_fused<NT, true, BT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<p.nCta, kThreads, smem, st>>>(*map, T, p);
+    kern<<<p.nCta, threads, smem, st>>>(*map, T, p);
   } else {
-    auto kern = k_eval_fused<NT, false>;
+    auto kern = k_eval_fused<NT, false, BT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<p.nCta, kThreads, smem, st>>>(*map, T, p);
+    kern<<<p.nCta, threads, smem, st>>>(*map, T, p);
   }
   return cudaGetLastError();
 }
 
-cudaError_t launch_eval(const CUtensorMap* map, const double* T, const EvalArgs& p, int NT, bool tma,
+cudaError_t launch_eval(const CUtensorMap* map, const double* T, const EvalArgs& p, int NT, bool tma, int BT,
                         cudaStream_t st) {
+  if (BT == 32) {
+    switch (NT) {
+#define TF_CASE(n) \
+  case n:          \
+    return launch_eval_nt<n, 32>(map, T, p, tma, st);
+      TF_CASE(1) TF_CASE(2) TF_CASE(3) TF_CASE(4) TF_CASE(5) TF_CASE(6) TF_CASE(7) TF_CASE(8)
+      TF_CASE(9) TF_CASE(10) TF_CASE(11) TF_CASE(12) TF_CASE(13) TF_CASE(14) TF_CASE(15) TF_CASE(16)
+#undef TF_CASE
+      default:
+        return cudaErrorInvalidValue;
+    }
+  }
   switch (NT) {
 #define TF_CASE(n) \
   case n:          \
-    return launch_eval_nt<n>(map, T, p, tma, st);
+    return launch_eval_nt<n, 64>(map, T, p, tma, st);
     TF_CASE(1) TF_CASE(2) TF_CASE(3) TF_CASE(4) TF_CASE(5) TF_CASE(6) TF_CASE(7) TF_CASE(8)
     TF_CASE(9) TF_CASE(10) TF_CASE(11) TF_CASE(12) TF_CASE(13) TF_CASE(14) TF_CASE(15) TF_CASE(16)
 #undef TF_CASE
@@ -416,11 +445,11 @@ cudaError_t launch_eval_finalize(const EvalArgs& p, int RP, double* f, double* g
   return cudaGetLastError();
 }
 
-size_t eval_smem_bytes(int NT) {
+size_t eval_smem_bytes(int NT, int BT) {
   switch (NT) {
 #define TF_CASE(n) \
   case n:          \
-    return EvalSmem<n>::bytes;
+    return BT == 32 ? EvalSmem<n, 32>::bytes : EvalSmem<n, 64>::bytes;
     TF_CASE(1) TF_CASE(2) TF_CASE(3) TF_CASE(4) TF_CASE(5) TF_CASE(6) TF_CASE(7) TF_CASE(8)
     TF_CASE(9) TF_CASE(10) TF_CASE(11) TF_CASE(12) TF_CASE(13) TF_CASE(14) TF_CASE(15) TF_CASE(16)
 #undef TF_CASE

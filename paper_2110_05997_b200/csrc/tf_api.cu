@@ -2,6 +2,7 @@
 // management, work decomposition and launch orchestration. No arithmetic of the method happens here;
 // every step runs in the kernels of k_eval.cu, k_cg.cu and k_small.cu.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -156,9 +157,21 @@ tf_status grams_impl(tf_ctx* c, const tf_dims& d, const double* w, double* grams
   return TF_OK;
 }
 
+// Tile size of the fused kernel: TF_EVAL_TILE=32|64 overrides (development); default 64.
+int eval_tile() {
+  static int bt = 0;
+  if (!bt) {
+    const char* e = getenv("TF_EVAL_TILE");
+    bt = (e && atoi(e) == 32) ? 32 : 64;
+  }
+  return bt;
+}
+
 tf_status eval_impl(tf_ctx* c, const tf_dims& d, const double* T, const double* w, double* f, double* grad) {
   const int NT = (int)((d.R + 7) / 8);
   const int RP = 8 * NT;
+  const int BT = eval_tile();
+  const int ctas_per_sm = BT == 32 ? 2 : 1;
   EvalArgs p;
   p.A = w;
   p.B = w + d.I * d.R;
@@ -170,12 +183,12 @@ tf_status eval_impl(tf_ctx* c, const tf_dims& d, const double* T, const double* 
   p.ldT = d.ldT;
   p.Ktot = d.K_total;
   p.kbeg = d.k_begin;
-  p.nTi = (int)((d.I + 63) / 64);
-  p.nTj = (int)((d.J + 63) / 64);
-  p.Ipad = (int64_t)p.nTi * 64;
-  p.Jpad = (int64_t)p.nTj * 64;
+  p.nTi = (int)((d.I + BT - 1) / BT);
+  p.nTj = (int)((d.J + BT - 1) / BT);
+  p.Ipad = (int64_t)p.nTi * BT;
+  p.Jpad = (int64_t)p.nTj * BT;
   const int64_t tiles = (int64_t)p.nTi * p.nTj;
-  p.kSplit = choose_ksplit(tiles, d.K, c->nsm);
+  p.kSplit = choose_ksplit(tiles, d.K, c->nsm * ctas_per_sm);
   p.kChunk = (d.K + p.kSplit - 1) / p.kSplit;
   p.nCta = (int)(tiles * p.kSplit);
   tf_status s;
@@ -198,7 +211,7 @@ tf_status eval_impl(tf_ctx* c, const tf_dims& d, const double* T, const double* 
     } else {
       cuuint64_t gdim[3] = {(cuuint64_t)d.I, (cuuint64_t)d.J, (cuuint64_t)d.K};
       cuuint64_t gstride[2] = {(cuuint64_t)d.ldT * 8, (cuuint64_t)d.ldT * d.J * 8};
-      cuuint32_t box[3] = {68, 64, 1};
+      cuuint32_t box[3] = {(cuuint32_t)(BT + 4), (cuuint32_t)BT, 1};
       cuuint32_t estr[3] = {1, 1, 1};
       CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(T), gdim, gstride, box, estr,
                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -220,7 +233,7 @@ tf_status eval_impl(tf_ctx* c, const tf_dims& d, const double* T, const double* 
     c->ev_used_pairs++;
     TF_CUDA(c, cudaEventRecord(e0, c->stream));
   }
-  TF_CUDA(c, launch_eval(&map, T, p, NT, tma, c->stream));
+  TF_CUDA(c, launch_eval(&map, T, p, NT, tma, BT, c->stream));
   if (c->timing) TF_CUDA(c, cudaEventRecord(e1, c->stream));
   TF_CUDA(c, launch_eval_finalize(p, RP, f, grad, c->nsm, c->stream));
   c->eval_launches += 1;

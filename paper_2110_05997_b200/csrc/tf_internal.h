@@ -20,10 +20,10 @@ struct EvalArgs {
   double* fp;   // [nCta]
 };
 
-cudaError_t launch_eval(const CUtensorMap* map, const double* T, const EvalArgs& p, int NT, bool tma,
+cudaError_t launch_eval(const CUtensorMap* map, const double* T, const EvalArgs& p, int NT, bool tma, int BT,
                         cudaStream_t st);
 cudaError_t launch_eval_finalize(const EvalArgs& p, int RP, double* f, double* grad, int nsm, cudaStream_t st);
-size_t eval_smem_bytes(int NT);
+size_t eval_smem_bytes(int NT, int BT);
 
 // ---- small kernels (k_small.cu)
 struct Modes {
