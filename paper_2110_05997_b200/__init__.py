@@ -19,7 +19,7 @@ from dataclasses import dataclass
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtf.so")
+LIB_PATH = os.environ.get("TF_LIB_PATH") or os.path.join(_HERE, "libtf.so")   # TF_LIB_PATH: dev builds only
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

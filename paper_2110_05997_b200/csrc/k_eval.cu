@@ -15,6 +15,8 @@
 // A CTA owns one (i-tile, j-tile) and a contiguous range of slices; accA/accB stay in registers
 // over the range and are written once as partials; k_eval_finalize reduces all partials in a
 // fixed order (deterministic, bitwise reproducible).
+#include <cstdio>
+
 #include "tf_internal.h"
 #include "tf_device.cuh"
 
@@ -82,6 +84,19 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 //   phase 2_k, first half of the r-tiles        |
 //   wait p3done ; rebuild sAc_{k+1} ; arrive aready
 //   phase 2_k, second half ; dF/dC butterfly -> sGC[k%2]
+#ifdef TF_EVAL_PROFILE
+// Development timeline: CTA 0, lane 0 of every warp records clock64 at 8 points of its first 16 slices.
+__device__ unsigned long long g_eval_tl[16 * 16 * 8];
+#define TL(kk, pt)                                                                                          \
+  do {                                                                                                      \
+    if (blockIdx.x == 0 && lane == 0 && (kk) < 16) g_eval_tl[((kk) * 16 + warp) * 8 + (pt)] = clock64(); \
+  } while (0)
+#else
+#define TL(kk, pt) \
+  do {             \
+  } while (0)
+#endif
+
 template <int NT, bool kTMA, int BT>
 __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
     k_eval_fused(const __grid_constant__ CUtensorMap tmapT, const double* __restrict__ T, EvalArgs p) {
@@ -188,8 +203,10 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
     const int64_t k = kA + kk;
     double* sT = sTE + b * (kLDE * kBJ);
     const double* sc = sC + (kk & 3) * RP;
+    TL(kk, 0);
     if (kTMA) mbar_wait(&full[b], (kk >> 1) & 1);
     if (kk > 0) mbar_wait(aready, (kk - 1) & 1);
+    TL(kk, 1);
 
     // ---- phase 1: E = T + (-A diag(c)) B^T on a (BT/2) x 16 warp tile (MF x 2 fragments)
     {
@@ -228,7 +245,9 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
             sT[(16 * wj + 8 * n + 2 * q + e) * kLDE + (kBI / 2) * wi + 8 * m + g] = E[m][n][e];
         }
     }
+    TL(kk, 2);
     __syncthreads();  // S2_k: E_k complete; every warp is past phases 2/3 of slice k-1
+    TL(kk, 3);
 
     if (kk + 1 < nk) {
       if (kTMA) {
@@ -261,6 +280,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(p3done);
+    TL(kk, 4);
 
     // ---- phase 2: P^T_t = B_t^T E^T for i-cols 8*warp.. (t outer, E fragments in registers);
     //      accA^T += diag(c) P^T; dF/dC partial = sum_i A o P; the sAc hand-off sits between the halves
@@ -274,7 +294,9 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
         if (t == NT1 && kk + 1 < nk) {
+          TL(kk, 5);
           mbar_wait(p3done, kk & 1);          // every warp is done reading sAc_k
+          TL(kk, 6);
           rebuild_sAc(sC + ((kk + 1) & 3) * RP);
           __syncwarp();
           if (lane == 0) mbar_arrive(aready);
@@ -298,6 +320,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(aready);
       }
+      TL(kk, 7);
       butterfly4<NV>(gcv, q);
       const int base = ((q >> 1) & 1) * (NV / 2) + (q & 1) * (NV / 4);
       double* gdst = sGC + (kk & 1) * NW * RP + warp * RP;
@@ -459,3 +482,21 @@ size_t eval_smem_bytes(int NT, int BT) {
 }
 
 }  // namespace tfk
+
+#ifdef TF_EVAL_PROFILE
+extern "C" void tf_eval_timeline_dump(void) {
+  unsigned long long h[16 * 16 * 8];
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(h, tfk::g_eval_tl, sizeof(h));
+  const char* names[8] = {"top", "waits", "ph1 end", "S2", "ph3 end", "ph2 half", "p3done", "ph2 end"};
+  for (int kk = 2; kk < 6; ++kk) {
+    printf("slice %d (cycles from warp0 top):\n", kk);
+    const unsigned long long t0 = h[(kk * 16 + 0) * 8 + 0];
+    for (int w = 0; w < 8; ++w) {
+      printf("  w%d:", w);
+      for (int pt = 0; pt < 8; ++pt) printf(" %s=%lld", names[pt], (long long)(h[(kk * 16 + w) * 8 + pt] - t0));
+      printf("\n");
+    }
+  }
+}
+#endif

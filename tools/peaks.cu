@@ -41,6 +41,36 @@ __global__ void k_dfma(double* out, int iters) {
   if (s == 12345.678) out[0] = s;
 }
 
+// DMMA with a 4 x 2 fragment tile per warp (distinct A and B operand registers, 8 accumulators), the
+// pattern of the fused kernel's phase 1; operands are perturbed every iteration so nothing is hoisted.
+__global__ void k_dmma_tile(double* out, int iters) {
+  double a[4], b[2], c[4][2][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) a[i] = 1.0 + (threadIdx.x + i) * 1e-9;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) b[i] = 1.0 - (threadIdx.x + i) * 1e-9;
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int n = 0; n < 2; ++n) c[m][n][0] = c[m][n][1] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int n = 0; n < 2; ++n)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c[m][n][0]), "+d"(c[m][n][1]) : "d"(a[m]), "d"(b[n]));
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = __longlong_as_double(__double_as_longlong(a[i]) ^ 1);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int n = 0; n < 2; ++n) s += c[m][n][0] + c[m][n][1];
+  if (s == 12345.678) out[0] = s;
+}
+
 // DMMA and DFMA interleaved in one warp: if the two share the FP64 datapath the mix is no faster
 // than the sum of the parts.
 template <int NACC, int NF>
@@ -101,6 +131,16 @@ int main(int argc, char** argv) {
       if (tf > best_dmma) best_dmma = tf;
     }
   }
+  for (int tpb : {256, 512}) {
+    int iters = 4000; dim3 g(nsm), b(tpb);
+    k_dmma_tile<<<g, b>>>(out, 10); CK(cudaDeviceSynchronize());
+    CK(cudaEventRecord(e0)); k_dmma_tile<<<g, b>>>(out, iters); CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    double flops = 2.0 * 256 * 8 * (double)iters * (g.x * (tpb / 32));
+    double tf = flops / (ms * 1e-3) / 1e12;
+    printf(", \"dmma_tile4x2_tpb%d_tflops\": %.2f", tpb, tf);
+    if (tf > best_dmma) best_dmma = tf;
+  }
   // DMMA single-warp-per-SMSP chain latency probe: 1 acc chain, 4 warps per SM
   {
     int iters = 20000; dim3 g(nsm), b(128);
@@ -119,17 +159,17 @@ int main(int argc, char** argv) {
     printf(", \"dmma_4chain_ns_per_iter\": %.3f", ms * 1e6 / iters);
   }
   {
-    // mix: per iteration 8 DMMA (8*256 FMA per warp-thread-set) + NF DFMA per thread
-    int iters = 4000; dim3 g(nsm * 2), b(512);
+    // mix: per iteration 8 DMMA (8 x 256 FMA per warp) and/or 32 DFMA per thread (32 x 32 FMA per warp)
+    int iters = 4000; dim3 g(nsm), b(256);
     float t_d, t_f, t_m;
     k_mix<8, 0><<<g, b>>>(out, 10); CK(cudaDeviceSynchronize());
     CK(cudaEventRecord(e0)); k_mix<8, 0><<<g, b>>>(out, iters); CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
     CK(cudaEventElapsedTime(&t_d, e0, e1));
-    k_mix<0, 64><<<g, b>>>(out, 10); CK(cudaDeviceSynchronize());
-    CK(cudaEventRecord(e0)); k_mix<0, 64><<<g, b>>>(out, iters); CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
+    k_mix<0, 32><<<g, b>>>(out, 10); CK(cudaDeviceSynchronize());
+    CK(cudaEventRecord(e0)); k_mix<0, 32><<<g, b>>>(out, iters); CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
     CK(cudaEventElapsedTime(&t_f, e0, e1));
-    k_mix<8, 64><<<g, b>>>(out, 10); CK(cudaDeviceSynchronize());
-    CK(cudaEventRecord(e0)); k_mix<8, 64><<<g, b>>>(out, iters); CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
+    k_mix<8, 32><<<g, b>>>(out, 10); CK(cudaDeviceSynchronize());
+    CK(cudaEventRecord(e0)); k_mix<8, 32><<<g, b>>>(out, iters); CK(cudaEventRecord(e1)); CK(cudaEventSynchronize(e1));
     CK(cudaEventElapsedTime(&t_m, e0, e1));
     printf(", \"mix_dmma_only_ms\": %.3f, \"mix_dfma_only_ms\": %.3f, \"mix_both_ms\": %.3f", t_d, t_f, t_m);
   }
@@ -162,6 +202,8 @@ int main(int argc, char** argv) {
       if (gbs > best_bw) best_bw = gbs;
     }
   }
+  int clk_khz = 0; cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
+  printf(", \"sm_clock_attr_mhz\": %d", clk_khz / 1000);
   printf(", \"best_dmma_tflops\": %.2f, \"best_dfma_tflops\": %.2f, \"read_hbm_gbs\": %.1f}\n", best_dmma, best_dfma, best_bw);
   CK(cudaFree(buf));
   return 0;
