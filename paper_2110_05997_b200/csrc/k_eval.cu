@@ -374,6 +374,19 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
 // (contiguous in the partial buffers) so the partial reads coalesce; the packed gradient writes are strided
 // but small. grad blocks: dF/dA = -sum accA, dF/dB = +sum accB (accB already holds -(A diag c)^T E),
 // dF/dC = -sum gC partials (rows outside the local slices are written 0).
+// Ordered sum of n partials x[s * stride] with 8 loads in flight (fixed left-to-right order of the partial
+// sums within each of the 8 lanes, then lanes combined in order: deterministic for given n).
+__device__ __forceinline__ double ordered_sum8(const double* __restrict__ x, int64_t n, int64_t stride) {
+  double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  int64_t s = 0;
+  for (; s + 8 <= n; s += 8) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] += x[(s + u) * stride];
+  }
+  for (int u = 0; s < n; ++s, ++u) acc[u] += x[s * stride];
+  return ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+}
+
 __global__ void k_eval_finalize(EvalArgs p, int RP, double* __restrict__ f, double* __restrict__ grad) {
   const int64_t R = p.R;
   const int64_t nA = p.I * R, nB = p.J * R, nC = p.Ktot * R;
@@ -381,22 +394,17 @@ __global__ void k_eval_finalize(EvalArgs p, int RP, double* __restrict__ f, doub
   const int64_t nPA = (int64_t)p.nTj * p.kSplit, nPB = (int64_t)p.nTi * p.kSplit, nPC = (int64_t)p.nTi * p.nTj;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    double v = 0.0;
     if (idx < nA) {
       const int64_t i = idx / R, r = idx % R;
-      for (int64_t s = 0; s < nPA; ++s) v += p.gAp[(s * p.Ipad + i) * RP + r];
-      grad[i + p.I * r] = -v;
+      grad[i + p.I * r] = -ordered_sum8(p.gAp + i * RP + r, nPA, p.Ipad * RP);
     } else if (idx < nA + nB) {
       const int64_t qq = idx - nA, j = qq / R, r = qq % R;
-      for (int64_t s = 0; s < nPB; ++s) v += p.gBp[(s * p.Jpad + j) * RP + r];
-      grad[nA + j + p.J * r] = v;
+      grad[nA + j + p.J * r] = ordered_sum8(p.gBp + j * RP + r, nPB, p.Jpad * RP);
     } else {
       const int64_t qq = idx - nA - nB, kg = qq / R, r = qq % R;
       const int64_t k = kg - p.kbeg;
-      if (k >= 0 && k < p.K) {
-        for (int64_t s = 0; s < nPC; ++s) v += p.gCp[(s * p.K + k) * RP + r];
-        v = -v;
-      }
+      double v = 0.0;
+      if (k >= 0 && k < p.K) v = -ordered_sum8(p.gCp + k * RP + r, nPC, p.K * RP);
       grad[nA + nB + kg + p.Ktot * r] = v;
     }
   }
