@@ -54,12 +54,13 @@ def lib():
             L = ctypes.CDLL(build())
             L.oracle_eval.argtypes = [_i64] * 4 + [_d] * 4 + [_d] * 4 + [ctypes.c_int]
             L.oracle_slice_eval.argtypes = [_i64, _i64, _i64, _d, _i64, _i64, _d, _d, _i64, _d, _i64, _d, _d]
-            L.oracle_gn_matvec_plain.argtypes = [_i64] * 4 + [_d] * 4 + [ctypes.c_double, _d, ctypes.c_int]
+            L.oracle_gn_matvec_plain.argtypes = [_i64] * 4 + [_d] * 4 + [ctypes.c_double, _d, _d, ctypes.c_int]
             L.oracle_grams.argtypes = [_i64] * 4 + [_d] * 4
             L.oracle_pi.argtypes = [_i64, _d, _d]
-            L.oracle_gn_matvec_hv.argtypes = [_i64] * 4 + [_d] * 4 + [ctypes.c_double, _d]
+            L.oracle_gn_matvec_hv.argtypes = [_i64] * 4 + [_d] * 4 + [ctypes.c_double, _d, _d]
+            L.oracle_reg_gamma.argtypes = [_i64] * 4 + [_d] * 4
             L.oracle_jtj_diag.argtypes = [_i64] * 4 + [_d] * 4
-            L.oracle_cg.argtypes = ([_i64] * 4 + [_d] * 4 + [ctypes.c_double, ctypes.c_int, ctypes.c_double,
+            L.oracle_cg.argtypes = ([_i64] * 4 + [_d] * 4 + [ctypes.c_double, _d, ctypes.c_int, ctypes.c_double,
                                     ctypes.c_int] + [_d] * 5 + [ctypes.POINTER(ctypes.c_int)])
             _lib = L
     return _lib
@@ -121,12 +122,18 @@ def slice_eval(S, x, X, Y):
     return f.value, g
 
 
-def gn_matvec_plain(w, v, lam, I, J, K, R, nthreads: int = 0):
-    """(J^T J + lam I) v via u = J v then J^T u (Lemma partialf), O(IJKR)."""
+def _damp(damp):
+    return None if damp is None else _np(damp).reshape(-1)
+
+
+def gn_matvec_plain(w, v, lam, I, J, K, R, nthreads: int = 0, damp=None):
+    """(J^T J + lam D) v via u = J v then J^T u (Lemma partialf), O(IJKR). D = diag(damp) per (mode, r)."""
     A, B, C = _split(w, I, J, K, R)
     v = _np(v).reshape(-1)
     y = np.zeros_like(v)
-    rc = lib().oracle_gn_matvec_plain(I, J, K, R, _p(A), _p(B), _p(C), _p(v), float(lam), _p(y), nthreads)
+    d = _damp(damp)
+    rc = lib().oracle_gn_matvec_plain(I, J, K, R, _p(A), _p(B), _p(C), _p(v), float(lam),
+                                      None if d is None else _p(d), _p(y), nthreads)
     if rc:
         raise RuntimeError(f"oracle_gn_matvec_plain rc={rc}")
     return y
@@ -148,13 +155,23 @@ def hadamard_chains(grams_, R):
     return out
 
 
-def gn_matvec_hv(w, v, lam, I, J, K, R):
-    """(J^T J + lam I) v by Thm Hv."""
+def gn_matvec_hv(w, v, lam, I, J, K, R, damp=None):
+    """(J^T J + lam D) v by Thm Hv; D = diag(damp) per (mode, r), None = I."""
     A, B, C = _split(w, I, J, K, R)
     v = _np(v).reshape(-1)
     y = np.zeros_like(v)
-    lib().oracle_gn_matvec_hv(I, J, K, R, _p(A), _p(B), _p(C), _p(v), float(lam), _p(y))
+    d = _damp(damp)
+    lib().oracle_gn_matvec_hv(I, J, K, R, _p(A), _p(B), _p(C), _p(v), float(lam), None if d is None else _p(d),
+                              _p(y))
     return y
+
+
+def reg_gamma(w, I, J, K, R):
+    """Tensor Fox's diagonal regularizer gamma = [gamma_X | gamma_Y | gamma_Z], 3R."""
+    A, B, C = _split(w, I, J, K, R)
+    g = np.zeros(3 * R)
+    lib().oracle_reg_gamma(I, J, K, R, _p(A), _p(B), _p(C), _p(g))
+    return g
 
 
 def jtj_diag(w, I, J, K, R):
@@ -164,8 +181,9 @@ def jtj_diag(w, I, J, K, R):
     return d
 
 
-def cg(w, rhs, lam, maxiter, I, J, K, R, tol=0.0, jacobi=False, history=False):
-    """Alg. CG-dGN. Returns dict(x, iters, r2, alpha, beta[, x_hist])."""
+def cg(w, rhs, lam, maxiter, I, J, K, R, tol=0.0, jacobi=False, history=False, damp=None):
+    """Alg. CG-dGN on (J^T J + lam D); D = diag(damp) per (mode, r), None = I.
+    Returns dict(x, iters, r2, alpha, beta[, x_hist])."""
     A, B, C = _split(w, I, J, K, R)
     rhs = _np(rhs).reshape(-1)
     n = rhs.size
@@ -174,7 +192,9 @@ def cg(w, rhs, lam, maxiter, I, J, K, R, tol=0.0, jacobi=False, history=False):
     xh = np.zeros(m * n) if history else None
     r2, al, be = np.zeros(m), np.zeros(m), np.zeros(m)
     it = ctypes.c_int()
-    rc = lib().oracle_cg(I, J, K, R, _p(A), _p(B), _p(C), _p(rhs), float(lam), int(maxiter), float(tol),
+    d = _damp(damp)
+    rc = lib().oracle_cg(I, J, K, R, _p(A), _p(B), _p(C), _p(rhs), float(lam), None if d is None else _p(d),
+                         int(maxiter), float(tol),
                          int(bool(jacobi)), _p(x), _p(xh) if history else None, _p(r2), _p(al), _p(be),
                          ctypes.byref(it))
     out = {"x": x, "iters": it.value, "r2": r2[:it.value], "alpha": al[:it.value], "beta": be[:it.value],

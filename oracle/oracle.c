@@ -156,7 +156,7 @@ int oracle_slice_eval(int64_t n1, int64_t n2, int64_t R, const double *S, int64_
  */
 int oracle_gn_matvec_plain(int64_t I, int64_t J, int64_t K, int64_t R,
                            const double *A, const double *B, const double *C,
-                           const double *v, double lambda, double *y, int nthreads) {
+                           const double *v, double lambda, const double *damp, double *y, int nthreads) {
   if (I < 1 || J < 1 || K < 1 || R < 1) return 1;
   const double *vA = v, *vB = v + I * R, *vC = v + (I + J) * R;
   int nt = clamp_threads(nthreads);
@@ -192,14 +192,19 @@ int oracle_gn_matvec_plain(int64_t I, int64_t J, int64_t K, int64_t R,
   for (int64_t q = 0; q < I * R; ++q) {
     ld s = 0.0L;
     for (int t = 0; t < nt; ++t) s += pA[(size_t)t * I * R + q];
-    y[q] = (double)(s + (ld)lambda * (ld)vA[q]);
+    const ld dmp = damp ? (ld)damp[q / I] : 1.0L;
+    y[q] = (double)(s + (ld)lambda * dmp * (ld)vA[q]);
   }
   for (int64_t q = 0; q < J * R; ++q) {
     ld s = 0.0L;
     for (int t = 0; t < nt; ++t) s += pB[(size_t)t * J * R + q];
-    y[I * R + q] = (double)(s + (ld)lambda * (ld)vB[q]);
+    const ld dmp = damp ? (ld)damp[R + q / J] : 1.0L;
+    y[I * R + q] = (double)(s + (ld)lambda * dmp * (ld)vB[q]);
   }
-  for (int64_t q = 0; q < K * R; ++q) y[(I + J) * R + q] = (double)(yC[q] + (ld)lambda * (ld)vC[q]);
+  for (int64_t q = 0; q < K * R; ++q) {
+    const ld dmp = damp ? (ld)damp[2 * R + q / K] : 1.0L;
+    y[(I + J) * R + q] = (double)(yC[q] + (ld)lambda * dmp * (ld)vC[q]);
+  }
   free(pA); free(pB); free(yC);
   return 0;
 }
@@ -258,7 +263,7 @@ int oracle_pi(int64_t R, const double *grams, double *pi) {
  * then y = vec(Y) + lambda v. Written with explicit loops in the theorem's order.
  */
 static void hv_ld(int64_t I, int64_t J, int64_t K, int64_t R, const double *A, const double *B,
-                  const double *C, const ld *v, ld lambda, ld *y) {
+                  const double *C, const ld *v, ld lambda, const double *damp, ld *y) {
   const int64_t dims[3] = {I, J, K};
   const double *W[3] = {A, B, C};
   int64_t off[3] = {0, I * R, (I + J) * R};
@@ -280,7 +285,8 @@ static void hv_ld(int64_t I, int64_t J, int64_t K, int64_t R, const double *A, c
       for (int64_t s = 0; s < R; ++s) {
         ld acc = 0.0L;
         for (int64_t r = 0; r < R; ++r) acc += V1[a + n1 * r] * P1[r + R * s];
-        Y[a + n1 * s] = acc + lambda * V1[a + n1 * s];
+        const ld dmp = damp ? (ld)damp[l1 * R + s] : 1.0L;  /* (J^T J + lambda D) v, D = diag(damp) */
+        Y[a + n1 * s] = acc + lambda * dmp * V1[a + n1 * s];
       }
     /* Case 1: W^(l') (Pi^(l',l'') * (V^(l'')T W^(l''))) */
     for (int l2 = 0; l2 < 3; ++l2) {
@@ -308,13 +314,47 @@ static void hv_ld(int64_t I, int64_t J, int64_t K, int64_t R, const double *A, c
 }
 
 int oracle_gn_matvec_hv(int64_t I, int64_t J, int64_t K, int64_t R, const double *A, const double *B,
-                        const double *C, const double *v, double lambda, double *y) {
+                        const double *C, const double *v, double lambda, const double *damp, double *y) {
   int64_t n = R * (I + J + K);
   ld *vl = (ld *)malloc(sizeof(ld) * n), *yl = (ld *)malloc(sizeof(ld) * n);
   for (int64_t q = 0; q < n; ++q) vl[q] = v[q];
-  hv_ld(I, J, K, R, A, B, C, vl, (ld)lambda, yl);
+  hv_ld(I, J, K, R, A, B, C, vl, (ld)lambda, damp, yl);
   for (int64_t q = 0; q < n; ++q) y[q] = (double)yl[q];
   free(vl); free(yl);
+  return 0;
+}
+
+/*
+ * Diagonal regularizer of Tensor Fox (Section "Diagonal regularization"), L = 3:
+ *   G = max{ max_r' ||Y_r'|| ||Z_r'||, max_r' ||X_r'|| ||Z_r'||, max_r' ||X_r'|| ||Y_r'|| }
+ *   gamma_X^(r) = ||Y_r|| ||Z_r|| G,  gamma_Y^(r) = ||X_r|| ||Z_r|| G,  gamma_Z^(r) = ||X_r|| ||Y_r|| G
+ * with X, Y, Z = A, B, C and ||.|| the 2-norm of a factor column. gamma = [gX | gY | gZ], 3R values;
+ * D = diag(gamma_l^(r) I_{I_l}) in w-layout.
+ */
+int oracle_reg_gamma(int64_t I, int64_t J, int64_t K, int64_t R, const double *A, const double *B, const double *C,
+                     double *gamma) {
+  const int64_t dims[3] = {I, J, K};
+  const double *W[3] = {A, B, C};
+  ld *nrm = (ld *)malloc(sizeof(ld) * 3 * R);
+  for (int l = 0; l < 3; ++l)
+    for (int64_t r = 0; r < R; ++r) {
+      ld s = 0.0L;
+      for (int64_t a = 0; a < dims[l]; ++a) s += (ld)W[l][a + dims[l] * r] * (ld)W[l][a + dims[l] * r];
+      nrm[l * R + r] = sqrtl(s);
+    }
+  ld G = 0.0L;
+  for (int64_t r = 0; r < R; ++r) {
+    const ld yz = nrm[R + r] * nrm[2 * R + r], xz = nrm[r] * nrm[2 * R + r], xy = nrm[r] * nrm[R + r];
+    if (yz > G) G = yz;
+    if (xz > G) G = xz;
+    if (xy > G) G = xy;
+  }
+  for (int64_t r = 0; r < R; ++r) {
+    gamma[r] = (double)(nrm[R + r] * nrm[2 * R + r] * G);
+    gamma[R + r] = (double)(nrm[r] * nrm[2 * R + r] * G);
+    gamma[2 * R + r] = (double)(nrm[r] * nrm[R + r] * G);
+  }
+  free(nrm);
   return 0;
 }
 
@@ -355,10 +395,10 @@ int oracle_jtj_diag(int64_t I, int64_t J, int64_t K, int64_t R, const double *A,
 }
 
 /*
- * Alg. CG-dGN with D = I (damping lambda*I, DESIGN.md
- * reading R2) and M = I (jacobi = 0) or M = diag(J^T J) + lambda I (jacobi = 1,
- * PAPER.md:2655-2660, 4549-4567):
- *   B = M^{-1/2} (J^T J + lambda I) M^{-1/2};  x0 = 0;  r0 = M^{-1/2} rhs;  p0 = r0
+ * Alg. CG-dGN with damping lambda*D (D = diag(damp) per (mode, r); damp = NULL
+ * is D = I, the north star's lambda*I, reading R2) and M = I (jacobi = 0) or
+ * M = diag(J^T J) + lambda diag(D) (jacobi = 1):
+ *   B = M^{-1/2} (J^T J + lambda D) M^{-1/2};  x0 = 0;  r0 = M^{-1/2} rhs;  p0 = r0
  *   for i = 1..maxiter:
  *     z = B p;  alpha = ||r||^2 / <p, z>;  x += alpha p;  r -= alpha z;
  *     eps = ||r||^2;  beta = eps / ||r_old||^2;  p = r + beta p;  if eps < tol: break
@@ -368,7 +408,8 @@ int oracle_jtj_diag(int64_t I, int64_t J, int64_t K, int64_t R, const double *A,
  * Returns 5 if alpha or beta is not finite.
  */
 int oracle_cg(int64_t I, int64_t J, int64_t K, int64_t R, const double *A, const double *B,
-              const double *C, const double *rhs, double lambda, int maxiter, double tol, int jacobi,
+              const double *C, const double *rhs, double lambda, const double *damp, int maxiter, double tol,
+              int jacobi,
               double *x_out, double *x_hist, double *r2_hist, double *alpha_hist, double *beta_hist,
               int *iters) {
   int64_t n = R * (I + J + K);
@@ -376,8 +417,16 @@ int oracle_cg(int64_t I, int64_t J, int64_t K, int64_t R, const double *A, const
   ld *z = (ld *)malloc(sizeof(ld) * n), *tmp = (ld *)malloc(sizeof(ld) * n), *minv = (ld *)malloc(sizeof(ld) * n);
   int status = 0;
   if (jacobi) {
+    /* M = diag(J^T J) + lambda diag(D) */
     jtj_diag_ld(I, J, K, R, A, B, C, minv);
-    for (int64_t q = 0; q < n; ++q) minv[q] = 1.0L / sqrtl(minv[q] + (ld)lambda);
+    const int64_t dims[3] = {I, J, K}, off[3] = {0, I * R, (I + J) * R};
+    for (int l = 0; l < 3; ++l)
+      for (int64_t r = 0; r < R; ++r)
+        for (int64_t a = 0; a < dims[l]; ++a) {
+          const int64_t q = off[l] + a + dims[l] * r;
+          const ld dmp = damp ? (ld)damp[l * R + r] : 1.0L;
+          minv[q] = 1.0L / sqrtl(minv[q] + (ld)lambda * dmp);
+        }
   } else {
     for (int64_t q = 0; q < n; ++q) minv[q] = 1.0L;
   }
@@ -387,7 +436,7 @@ int oracle_cg(int64_t I, int64_t J, int64_t K, int64_t R, const double *A, const
   for (int i = 1; i <= maxiter; ++i) {
     /* z = B p in three steps */
     for (int64_t q = 0; q < n; ++q) tmp[q] = minv[q] * p[q];
-    hv_ld(I, J, K, R, A, B, C, tmp, (ld)lambda, z);
+    hv_ld(I, J, K, R, A, B, C, tmp, (ld)lambda, damp, z);
     for (int64_t q = 0; q < n; ++q) z[q] *= minv[q];
     ld pz = 0.0L;
     for (int64_t q = 0; q < n; ++q) pz += p[q] * z[q];

@@ -396,3 +396,75 @@ def test_cg_large_damping_limit():
     lam = 1e9
     out = oracle.cg(w, rhs, lam, 3, I, J, K, R)
     np.testing.assert_allclose(out["x"] * lam, rhs, rtol=0, atol=1e-5 * np.abs(rhs).max())
+
+
+# --------------------------------------------------------------------------- diagonal regularizer D (NEXT #1)
+def _expand_damp(d, I, J, K, R):
+    """Per-(mode, r) values -> the diagonal of D in w-layout (gamma_l^(r) I_{I_l})."""
+    return np.concatenate([np.repeat(d[:R], I), np.repeat(d[R:2 * R], J), np.repeat(d[2 * R:], K)])
+
+
+def test_reg_gamma_makes_jtj_diagonally_dominant():
+    """adding gamma to the diagonal makes every row of J^T J + D dominate each of its
+    off-diagonal entries: (J^T J)_ii + gamma_i >= |(J^T J)_ij| for all j (the paper's sufficient choice)."""
+    for (I, J, K, R, seed) in [(4, 3, 2, 3, 0), (3, 5, 4, 2, 1), (2, 2, 2, 4, 2)]:
+        rng = np.random.default_rng(seed)
+        w = rng.standard_normal(R * (I + J + K)) * rng.uniform(0.2, 3.0, R * (I + J + K))
+        Jm = jac.jacobian_entrywise(w, I, J, K, R)
+        H = Jm.T @ Jm
+        D = _expand_damp(oracle.reg_gamma(w, I, J, K, R), I, J, K, R)
+        off = np.abs(H - np.diag(np.diag(H)))
+        assert np.all(np.diag(H) + D >= off.max(axis=1) * (1 - 1e-12))
+        # and gamma is not vacuous: without it dominance fails for these random factors
+        assert not np.all(np.diag(H) >= off.max(axis=1))
+
+
+def test_reg_gamma_norm_balanced_closed_form():
+    """Norm-balanced factors (||X_r|| = ||Y_r|| = ||Z_r|| = a_r): gamma_l^(r) = a_r^2 max_r' a_r'^2."""
+    I, J, K, R = 5, 4, 3, 3
+    rng = np.random.default_rng(7)
+    a = np.array([0.5, 2.0, 1.3])
+    cols = []
+    for n in (I, J, K):
+        M = rng.standard_normal((n, R))
+        cols.append(M / np.linalg.norm(M, axis=0) * a)
+    w = w_of(*cols)
+    g = oracle.reg_gamma(w, I, J, K, R)
+    ref = a ** 2 * np.max(a ** 2)
+    np.testing.assert_allclose(g, np.concatenate([ref, ref, ref]), rtol=1e-14)
+
+
+@pytest.mark.parametrize("lam", [0.0, 1e-3, 0.7])
+def test_damped_matvec_against_explicit(lam):
+    """(J^T J + lam D) v with D = diag(gamma), Thm Hv and plain routes vs explicit."""
+    I, J, K, R = 4, 3, 3, 2
+    rng = np.random.default_rng(11)
+    w = rng.standard_normal(R * (I + J + K))
+    v = rng.standard_normal(R * (I + J + K))
+    gam = oracle.reg_gamma(w, I, J, K, R)
+    Jm = jac.jacobian_entrywise(w, I, J, K, R)
+    ref = Jm.T @ (Jm @ v) + lam * _expand_damp(gam, I, J, K, R) * v
+    np.testing.assert_allclose(oracle.gn_matvec_hv(w, v, lam, I, J, K, R, damp=gam), ref, rtol=1e-12,
+                               atol=1e-13 * np.abs(ref).max())
+    np.testing.assert_allclose(oracle.gn_matvec_plain(w, v, lam, I, J, K, R, damp=gam), ref, rtol=1e-12,
+                               atol=1e-13 * np.abs(ref).max())
+
+
+@pytest.mark.parametrize("jacobi", [False, True])
+def test_damped_cg_full_length_equals_dense_solve(jacobi):
+    """CG on M^{-1/2}(J^T J + mu D)M^{-1/2} with M = diag(J^T J) + mu diag(D) reaches
+    the dense solution of (J^T J + mu D) x = rhs."""
+    I, J, K, R = 3, 2, 2, 2
+    mu = 0.3
+    rng = np.random.default_rng(5)
+    w = rng.standard_normal(R * (I + J + K))
+    rhs = rng.standard_normal(R * (I + J + K))
+    gam = oracle.reg_gamma(w, I, J, K, R)
+    Jm = jac.jacobian_entrywise(w, I, J, K, R)
+    H = Jm.T @ Jm + mu * np.diag(_expand_damp(gam, I, J, K, R))
+    out = oracle.cg(w, rhs, mu, 60, I, J, K, R, tol=1e-26, jacobi=jacobi, damp=gam)
+    np.testing.assert_allclose(out["x"], np.linalg.solve(H, rhs), rtol=1e-9, atol=1e-11)
+    # with Jacobi the preconditioned diagonal is exactly 1 (first step: alpha uses B_ii = 1)
+    if jacobi:
+        m = 1.0 / np.sqrt(np.diag(H))
+        np.testing.assert_allclose((m[:, None] * H * m[None, :]).diagonal(), 1.0, rtol=1e-14)
