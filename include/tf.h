@@ -121,6 +121,26 @@ tf_status tf_cg_solve(tf_ctx *ctx, tf_dims d, const double *grams, const double 
                       double lambda, int maxiter, double tol, int jacobi, double *x, int *iters_done,
                       double *res2);
 
+/* NEXT #1 -- Tensor Fox's own damping ("Diagonal regularization"): the CG system
+ * is (J^T J + mu D) x = rhs with D = diag(gamma_l^(r) I_{I_l}) and
+ *   G = max_r' max{ ||Y_r'|| ||Z_r'||, ||X_r'|| ||Z_r'||, ||X_r'|| ||Y_r'|| },
+ *   gamma_X^(r) = ||Y_r|| ||Z_r|| G,  gamma_Y^(r) = ||X_r|| ||Z_r|| G,  gamma_Z^(r) = ||X_r|| ||Y_r|| G
+ * (X, Y, Z = A, B, C), which makes every row of J^T J + D dominate its off-diagonal entries. */
+
+/* gamma (3*R doubles, device) = [gamma_X | gamma_Y | gamma_Z] from the Grams (||W_r||^2 = pi^(l)_rr). */
+tf_status tf_reg_gamma(tf_ctx *ctx, int64_t R, const double *grams, double *gamma);
+
+/* y = (J^T J + mu D) v, D = diag over (mode, r) of damp (3*R doubles, device; NULL = identity, i.e.
+ * tf_gn_matvec). Same layouts and rules as tf_gn_matvec. */
+tf_status tf_gn_matvec_damped(tf_ctx *ctx, tf_dims d, const double *grams, const double *w, const double *v, double mu,
+                              const double *damp, double *y);
+
+/* Alg. CG-dGN on (J^T J + mu D) x = rhs; with jacobi != 0 the preconditioner is
+ * M = diag(J^T J) + mu diag(D). damp NULL = identity (tf_cg_solve). */
+tf_status tf_cg_solve_damped(tf_ctx *ctx, tf_dims d, const double *grams, const double *w, const double *rhs,
+                             double mu, const double *damp, int maxiter, double tol, int jacobi, double *x,
+                             int *iters_done, double *res2);
+
 /* Instrumentation (bench.py): when enabled, the fused evaluation kernel is
  * bracketed by CUDA events on the ctx stream; tf_ctx_kernel_stats synchronizes
  * and returns the summed device time (ms) and count of the fused-kernel launches

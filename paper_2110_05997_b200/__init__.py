@@ -49,13 +49,17 @@ _lib.tf_cpd_eval_host.argtypes = [_vp, TfDims, _vp, _vp, _vp, _vp]
 _lib.tf_gn_matvec.argtypes = [_vp, TfDims, _vp, _vp, _vp, ctypes.c_double, _vp]
 _lib.tf_cg_solve.argtypes = [_vp, TfDims, _vp, _vp, _vp, ctypes.c_double, ctypes.c_int, ctypes.c_double,
                              ctypes.c_int, _vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)]
+_lib.tf_reg_gamma.argtypes = [_vp, ctypes.c_int64, _vp, _vp]
+_lib.tf_gn_matvec_damped.argtypes = [_vp, TfDims, _vp, _vp, _vp, ctypes.c_double, _vp, _vp]
+_lib.tf_cg_solve_damped.argtypes = [_vp, TfDims, _vp, _vp, _vp, ctypes.c_double, _vp, ctypes.c_int, ctypes.c_double,
+                                    ctypes.c_int, _vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)]
 _lib.tf_ctx_set_timing.argtypes = [_vp, ctypes.c_int]
 _lib.tf_ctx_kernel_stats.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64),
                                      ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
 
 EXPORTED = ["tf_ctx_create", "tf_ctx_destroy", "tf_ctx_set_stream", "tf_status_str", "tf_last_error", "tf_version",
             "tf_grams", "tf_hadamard", "tf_cpd_eval", "tf_cpd_eval_host", "tf_gn_matvec", "tf_cg_solve",
-            "tf_ctx_set_timing", "tf_ctx_kernel_stats"]
+            "tf_reg_gamma", "tf_gn_matvec_damped", "tf_cg_solve_damped", "tf_ctx_set_timing", "tf_ctx_kernel_stats"]
 
 TF_OK, TF_ERR_ARG, TF_ERR_ALIGN, TF_ERR_UNSUPPORTED, TF_ERR_CUDA, TF_ERR_NONFINITE, TF_ERR_ALLOC = range(7)
 MAX_R = 128
@@ -211,6 +215,48 @@ class Context:
         r2 = ctypes.c_double()
         self._check(_lib.tf_cg_solve(self._h, d.c(), _ptr(grams), _ptr(w), _ptr(rhs), float(lam), int(maxiter),
                                      float(tol), int(bool(jacobi)), _ptr(x), ctypes.byref(it), ctypes.byref(r2)))
+        return x, it.value, r2.value
+
+    def tf_reg_gamma(self, R: int, grams: torch.Tensor, gamma: torch.Tensor | None = None) -> torch.Tensor:
+        """Tensor Fox's diagonal regularizer gamma (3R) from the Grams."""
+        _dev(grams, "grams", 3 * R * R)
+        if gamma is None:
+            gamma = torch.empty(3 * R, dtype=torch.float64, device=grams.device)
+        _dev(gamma, "gamma", 3 * R)
+        self._check(_lib.tf_reg_gamma(self._h, R, _ptr(grams), _ptr(gamma)))
+        return gamma
+
+    def tf_gn_matvec_damped(self, d: Dims, grams: torch.Tensor, w: torch.Tensor, v: torch.Tensor, mu: float,
+                            damp: torch.Tensor | None, y: torch.Tensor | None = None) -> torch.Tensor:
+        _dev(grams, "grams", 3 * d.R * d.R)
+        _dev(w, "w", d.n)
+        _dev(v, "v", d.n)
+        if damp is not None:
+            _dev(damp, "damp", 3 * d.R)
+        if y is None:
+            y = torch.empty(d.n, dtype=torch.float64, device=w.device)
+        _dev(y, "y", d.n)
+        self._check(_lib.tf_gn_matvec_damped(self._h, d.c(), _ptr(grams), _ptr(w), _ptr(v), float(mu), _ptr(damp),
+                                             _ptr(y)))
+        return y
+
+    def tf_cg_solve_damped(self, d: Dims, grams: torch.Tensor, w: torch.Tensor, rhs: torch.Tensor, mu: float,
+                           damp: torch.Tensor | None, maxiter: int, tol: float = 0.0, jacobi: bool = False,
+                           x: torch.Tensor | None = None):
+        """Returns (x, iters_done, ||r||^2) for (J^T J + mu D) x = rhs."""
+        _dev(grams, "grams", 3 * d.R * d.R)
+        _dev(w, "w", d.n)
+        _dev(rhs, "rhs", d.n)
+        if damp is not None:
+            _dev(damp, "damp", 3 * d.R)
+        if x is None:
+            x = torch.empty(d.n, dtype=torch.float64, device=w.device)
+        _dev(x, "x", d.n)
+        it = ctypes.c_int()
+        r2 = ctypes.c_double()
+        self._check(_lib.tf_cg_solve_damped(self._h, d.c(), _ptr(grams), _ptr(w), _ptr(rhs), float(mu), _ptr(damp),
+                                            int(maxiter), float(tol), int(bool(jacobi)), _ptr(x), ctypes.byref(it),
+                                            ctypes.byref(r2)))
         return x, it.value, r2.value
 
     def set_timing(self, enable: bool):

@@ -26,7 +26,8 @@ constexpr int kGramZ = 16;   // max row splits of one Gram output tile
 struct CgArgs {
   Modes m;
   const double* pi;       // 6 R x R
-  const double* dscale;   // 3R or nullptr
+  const double* dscale;   // 3R or nullptr: Jacobi scaling M^{-1/2} per (mode, r)
+  const double* damp;     // 3R or nullptr: damping matrix D per (mode, r) (the paper's gamma; nullptr = I)
   double lambda, tol;
   int maxiter;
   const double* rhs;      // CG right-hand side (w-coordinates)
@@ -273,7 +274,8 @@ __device__ double stage_apply(const CgArgs& A, const VSrc& V, double* y, double*
         if (tl < NTH && rok && sc < R) {
           const double pr = fma(bet, sXp[row * LDX + sc], sXr[row * LDX + sc]);
           const double ds = D ? D[sc] : 1.0;
-          const double yv = ds * fma(A.lambda, ds * pr, acc[j][e]);
+          const double lam = A.damp ? A.lambda * A.damp[l * R + sc] : A.lambda;
+          const double yv = ds * fma(lam, ds * pr, acc[j][e]);
           y[off + arow + n * sc] = yv;
           dsum = fma(pr, yv, dsum);
           pnew[j][e] = pr;
@@ -450,7 +452,8 @@ static cudaError_t launch_persistent_nt(const CgArgs& a, int nsm, cudaStream_t s
   return cudaLaunchCooperativeKernel((const void*)kern, grid, block, params, smem, st);
 }
 
-cudaError_t launch_cg_persistent(const Modes& m, const double* pi, const double* dscale, double lambda, double tol,
+cudaError_t launch_cg_persistent(const Modes& m, const double* pi, const double* dscale, const double* damp,
+                                 double lambda, double tol,
                                  int maxiter, const double* rhs, const double* v, double* x, double* r, double* p,
                                  double* z, double* G, double* S, double* part, CgState* st_dev, int mode, int nsm,
                                  cudaStream_t st) {
@@ -460,6 +463,7 @@ cudaError_t launch_cg_persistent(const Modes& m, const double* pi, const double*
   a.m = m;
   a.pi = pi;
   a.dscale = dscale;
+  a.damp = damp;
   a.lambda = lambda;
   a.tol = tol;
   a.maxiter = maxiter;

@@ -100,11 +100,38 @@ __global__ void k_hadamard(int64_t R, const double* __restrict__ g, double* __re
   }
 }
 
-__global__ void k_jacobi_scale(int64_t R, const double* __restrict__ pi, double lambda, double* __restrict__ d) {
+__global__ void k_jacobi_scale(int64_t R, const double* __restrict__ pi, double lambda, const double* __restrict__ damp,
+                               double* __restrict__ d) {
   const int64_t RR = R * R;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < 3 * R; q += (int64_t)gridDim.x * blockDim.x) {
     const int64_t l = q / R, r = q % R;
-    d[q] = 1.0 / sqrt(pi[l * RR + r + R * r] + lambda);  // M_(l,a,r) = Pi^(l)_rr + lambda
+    // M_(l,a,r) = Pi^(l)_rr + lambda * D_(l,r)   (D = I when damp == nullptr)
+    d[q] = 1.0 / sqrt(pi[l * RR + r + R * r] + lambda * (damp ? damp[q] : 1.0));
+  }
+}
+
+// Tensor Fox's diagonal regularizer from the Grams: ||W_r|| = sqrt(pi^(l)_rr),
+// G = max_r max{||Y_r|| ||Z_r||, ||X_r|| ||Z_r||, ||X_r|| ||Y_r||}, gamma_X^(r) = ||Y_r|| ||Z_r|| G, ...
+// One block; the max is order-independent, so the result is deterministic.
+__global__ void k_reg_gamma(int64_t R, const double* __restrict__ grams, double* __restrict__ gamma) {
+  __shared__ double red[32];
+  const int64_t RR = R * R;
+  double m = 0.0;
+  for (int64_t r = threadIdx.x; r < R; r += blockDim.x) {
+    const double x = sqrt(grams[r + R * r]), y = sqrt(grams[RR + r + R * r]), z = sqrt(grams[2 * RR + r + R * r]);
+    m = fmax(m, fmax(y * z, fmax(x * z, x * y)));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  double G = 0.0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) G = fmax(G, red[i]);
+  for (int64_t r = threadIdx.x; r < R; r += blockDim.x) {
+    const double x = sqrt(grams[r + R * r]), y = sqrt(grams[RR + r + R * r]), z = sqrt(grams[2 * RR + r + R * r]);
+    gamma[r] = y * z * G;
+    gamma[R + r] = x * z * G;
+    gamma[2 * R + r] = x * y * G;
   }
 }
 
@@ -152,8 +179,14 @@ cudaError_t launch_hadamard(int64_t R, const double* grams, double* pi, cudaStre
   return cudaGetLastError();
 }
 
-cudaError_t launch_jacobi_scale(const Modes& m, const double* pi, double lambda, double* dscale, cudaStream_t st) {
-  k_jacobi_scale<<<(int)((3 * m.R + 255) / 256), 256, 0, st>>>(m.R, pi, lambda, dscale);
+cudaError_t launch_jacobi_scale(const Modes& m, const double* pi, double lambda, const double* damp, double* dscale,
+                                cudaStream_t st) {
+  k_jacobi_scale<<<(int)((3 * m.R + 255) / 256), 256, 0, st>>>(m.R, pi, lambda, damp, dscale);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reg_gamma(int64_t R, const double* grams, double* gamma, cudaStream_t st) {
+  k_reg_gamma<<<1, 256, 0, st>>>(R, grams, gamma);
   return cudaGetLastError();
 }
 

@@ -438,8 +438,17 @@ static tf_status matvec_ws(tf_ctx* c, const tf_dims& d, const Modes& m, MatvecWs
   return TF_OK;
 }
 
-tf_status tf_gn_matvec(tf_ctx* c, tf_dims d, const double* grams, const double* w, const double* v, double lambda,
-                       double* y) {
+tf_status tf_reg_gamma(tf_ctx* c, int64_t R, const double* grams, double* gamma) {
+  if (!c) return TF_ERR_ARG;
+  if (R < 1 || R > TF_MAX_R || !grams || !gamma) return set_err(c, TF_ERR_ARG, "bad argument");
+  cudaSetDevice(c->device);
+  TF_CUDA(c, launch_reg_gamma(R, grams, gamma, c->stream));
+  c->total_launches += 1;
+  return TF_OK;
+}
+
+tf_status tf_gn_matvec_damped(tf_ctx* c, tf_dims d, const double* grams, const double* w, const double* v, double lambda,
+                              const double* damp, double* y) {
   tf_status s = check_dims(c, d);
   if (s) return s;
   if (!grams || !w || !v || !y) return set_err(c, TF_ERR_ARG, "null pointer");
@@ -449,14 +458,20 @@ tf_status tf_gn_matvec(tf_ctx* c, tf_dims d, const double* grams, const double* 
   MatvecWs ws;
   if ((s = matvec_ws(c, d, m, ws))) return s;
   TF_CUDA(c, launch_hadamard(d.R, grams, ws.pi, c->stream));
-  TF_CUDA(c, launch_cg_persistent(m, ws.pi, nullptr, lambda, 0.0, 0, nullptr, v, y, nullptr, nullptr, nullptr, ws.G,
-                                  ws.S, ws.partial, nullptr, 1, c->nsm, c->stream));
+  TF_CUDA(c, launch_cg_persistent(m, ws.pi, nullptr, damp, lambda, 0.0, 0, nullptr, v, y, nullptr, nullptr, nullptr,
+                                  ws.G, ws.S, ws.partial, nullptr, 1, c->nsm, c->stream));
   c->total_launches += 2;
   return TF_OK;
 }
 
-tf_status tf_cg_solve(tf_ctx* c, tf_dims d, const double* grams, const double* w, const double* rhs, double lambda,
-                      int maxiter, double tol, int jacobi, double* x, int* iters_done, double* res2) {
+tf_status tf_gn_matvec(tf_ctx* c, tf_dims d, const double* grams, const double* w, const double* v, double lambda,
+                       double* y) {
+  return tf_gn_matvec_damped(c, d, grams, w, v, lambda, nullptr, y);
+}
+
+tf_status tf_cg_solve_damped(tf_ctx* c, tf_dims d, const double* grams, const double* w, const double* rhs,
+                             double lambda, const double* damp, int maxiter, double tol, int jacobi, double* x,
+                             int* iters_done, double* res2) {
   tf_status s = check_dims(c, d);
   if (s) return s;
   if (!grams || !w || !rhs || !x) return set_err(c, TF_ERR_ARG, "null pointer");
@@ -476,9 +491,9 @@ tf_status tf_cg_solve(tf_ctx* c, tf_dims d, const double* grams, const double* w
   CgState* st = (CgState*)c->cgState.p;
   TF_CUDA(c, cudaMemsetAsync(st, 0, sizeof(CgState), c->stream));
   TF_CUDA(c, launch_hadamard(d.R, grams, ws.pi, c->stream));
-  if (jacobi) TF_CUDA(c, launch_jacobi_scale(m, ws.pi, lambda, ws.dscale, c->stream));
-  TF_CUDA(c, launch_cg_persistent(m, ws.pi, jacobi ? ws.dscale : nullptr, lambda, tol, maxiter, rhs, nullptr, x, r, p,
-                                  z, ws.G, ws.S, ws.partial, st, 0, c->nsm, c->stream));
+  if (jacobi) TF_CUDA(c, launch_jacobi_scale(m, ws.pi, lambda, damp, ws.dscale, c->stream));
+  TF_CUDA(c, launch_cg_persistent(m, ws.pi, jacobi ? ws.dscale : nullptr, damp, lambda, tol, maxiter, rhs, nullptr, x,
+                                  r, p, z, ws.G, ws.S, ws.partial, st, 0, c->nsm, c->stream));
   c->total_launches += 2 + (jacobi ? 1 : 0);
   TF_CUDA(c, cudaMemcpyAsync(c->cg_host, st, sizeof(CgState), cudaMemcpyDeviceToHost, c->stream));
   TF_CUDA(c, cudaStreamSynchronize(c->stream));
@@ -488,6 +503,11 @@ tf_status tf_cg_solve(tf_ctx* c, tf_dims d, const double* grams, const double* w
     return set_err(c, TF_ERR_NONFINITE,
                    "CG: non-finite alpha/beta at iteration " + std::to_string(c->cg_host->nonfinite));
   return TF_OK;
+}
+
+tf_status tf_cg_solve(tf_ctx* c, tf_dims d, const double* grams, const double* w, const double* rhs, double lambda,
+                      int maxiter, double tol, int jacobi, double* x, int* iters_done, double* res2) {
+  return tf_cg_solve_damped(c, d, grams, w, rhs, lambda, nullptr, maxiter, tol, jacobi, x, iters_done, res2);
 }
 
 }  // extern "C"

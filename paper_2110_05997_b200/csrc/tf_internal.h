@@ -37,7 +37,9 @@ struct Modes {
 cudaError_t launch_grams_ws(const Modes& m, double* Gpart, double* grams, cudaStream_t st);
 int gram_partial_slots(const Modes& m);
 int cg_partial_slots(const Modes& m);
-cudaError_t launch_jacobi_scale(const Modes& m, const double* pi, double lambda, double* dscale, cudaStream_t st);
+cudaError_t launch_jacobi_scale(const Modes& m, const double* pi, double lambda, const double* damp, double* dscale,
+                                cudaStream_t st);
+cudaError_t launch_reg_gamma(int64_t R, const double* grams, double* gamma, cudaStream_t st);
 
 struct MatvecWs {
   double* G;       // Gram partials of the persistent kernel
@@ -63,7 +65,8 @@ struct CgState {
 
 // Persistent cooperative CG (mode 0) or single GN matvec y = (J^T J + lambda I) v into x (mode 1).
 // part: 2 * nsm doubles; G: 3 R^2; st_dev receives iters / final ||r||^2 / non-finite iteration.
-cudaError_t launch_cg_persistent(const Modes& m, const double* pi, const double* dscale, double lambda, double tol,
+cudaError_t launch_cg_persistent(const Modes& m, const double* pi, const double* dscale, const double* damp,
+                                 double lambda, double tol,
                                  int maxiter, const double* rhs, const double* v, double* x, double* r, double* p,
                                  double* z, double* G, double* S, double* part, CgState* st_dev, int mode, int nsm,
                                  cudaStream_t st);

@@ -354,3 +354,49 @@ def test_c3_full_size_sampled(ctx):
 @pytest.mark.slow
 def test_c5_full_size_sampled(ctx):
     _sampled_full_size(ctx, "c5", "random", n_rows=1)
+
+
+# ------------------------------------------------------------------------- NEXT #1: the paper's damping D
+def test_reg_gamma(ctx):
+    for (I, J, K, R) in [(30, 20, 10, 4), (200, 90, 40, 100), (5, 5, 5, 1)]:
+        rng = np.random.default_rng(R)
+        w = rng.standard_normal(R * (I + J + K)) * 1.7
+        d = tf.Dims(I, J, K, R)
+        wt = torch.from_numpy(w).cuda()
+        gam = ctx.tf_reg_gamma(R, ctx.tf_grams(d, wt))
+        assert rel_err(to_np(gam), oracle.reg_gamma(w, I, J, K, R)) <= TOL
+
+
+@pytest.mark.parametrize("dims", [(20, 20, 20, 3), (120, 80, 60, 100), (61, 47, 33, 120)])
+def test_gn_matvec_damped(ctx, dims):
+    I, J, K, R = dims
+    rng = np.random.default_rng(I + 3 * R)
+    w = rng.standard_normal(R * (I + J + K))
+    v = rng.standard_normal(R * (I + J + K))
+    d = tf.Dims(I, J, K, R)
+    wt = torch.from_numpy(w).cuda()
+    g = ctx.tf_grams(d, wt)
+    gam = ctx.tf_reg_gamma(R, g)
+    y = ctx.tf_gn_matvec_damped(d, g, wt, torch.from_numpy(v).cuda(), 0.37, gam)
+    ref = oracle.gn_matvec_hv(w, v, 0.37, I, J, K, R, damp=oracle.reg_gamma(w, I, J, K, R))
+    assert rel_err(to_np(y), ref) <= TOL
+
+
+@pytest.mark.parametrize("jacobi", [False, True])
+def test_cg_damped_per_iteration(ctx, jacobi):
+    """Alg. CG-dGN on (J^T J + mu D) with Tensor Fox's gamma, every iterate."""
+    P = synth.make_problem("c3", "cpu", dims=(60, 50, 40, 20))
+    I, J, K, R = 60, 50, 40, 20
+    w = to_np(P.w("true"))
+    _, grad = oracle.cpd_eval(to_np(P.T).reshape(-1), w, I, J, K, R)
+    mu = 0.05
+    gam = oracle.reg_gamma(w, I, J, K, R)
+    ref = oracle.cg(w, -grad, mu, 8, I, J, K, R, jacobi=jacobi, history=True, damp=gam)
+    d = tf.Dims(I, J, K, R)
+    wt = torch.from_numpy(w).cuda()
+    g = ctx.tf_grams(d, wt)
+    gt = ctx.tf_reg_gamma(R, g)
+    for i in range(1, ref["iters"] + 1):
+        x, it, r2 = ctx.tf_cg_solve_damped(d, g, wt, torch.from_numpy(-grad).cuda(), mu, gt, i, 0.0, jacobi)
+        assert it == i
+        assert rel_err(to_np(x), ref["x_hist"][i - 1]) <= 1e-9, i
