@@ -62,6 +62,8 @@ def lib():
             L.oracle_jtj_diag.argtypes = [_i64] * 4 + [_d] * 4
             L.oracle_cg.argtypes = ([_i64] * 4 + [_d] * 4 + [ctypes.c_double, _d, ctypes.c_int, ctypes.c_double,
                                     ctypes.c_int] + [_d] * 5 + [ctypes.POINTER(ctypes.c_int)])
+            L.oracle_dgn.argtypes = ([_i64] * 4 + [_d, _d, ctypes.c_int, ctypes.c_double, ctypes.c_double] +
+                                     [ctypes.c_int] * 3 + [ctypes.POINTER(ctypes.c_int)] * 3 + [_d, _d, ctypes.c_int])
             _lib = L
     return _lib
 
@@ -202,3 +204,21 @@ def cg(w, rhs, lam, maxiter, I, J, K, R, tol=0.0, jacobi=False, history=False, d
     if history:
         out["x_hist"] = xh.reshape(m, n)[:it.value]
     return out
+
+
+def dgn(T, w0, I, J, K, R, cg_iters, maxiter=None, tol=1e-6, mu0=0.0, use_gamma=True, jacobi=True, balance=True,
+        nthreads: int = 0):
+    """The dGN outer loop of Tensor Fox from w0 with the given per-iteration CG budgets.
+    Returns dict(w, iters, reason, f, hist[iters, 5] = [F, rel_err, mu, g, ||x||])."""
+    T = _np(T).reshape(-1)
+    w = _np(w0).reshape(-1).copy()
+    cgi = np.ascontiguousarray(np.asarray(cg_iters, dtype=np.int32))
+    m = int(maxiter if maxiter is not None else cgi.size)
+    assert cgi.size >= m
+    hist = np.zeros(5 * max(m, 1))
+    it, why = ctypes.c_int(), ctypes.c_int()
+    f = ctypes.c_double()
+    lib().oracle_dgn(I, J, K, R, _p(T), _p(w), m, float(tol), float(mu0), int(use_gamma), int(jacobi), int(balance),
+                     cgi.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), ctypes.byref(it), ctypes.byref(why),
+                     ctypes.byref(f), _p(hist), nthreads)
+    return {"w": w, "iters": it.value, "reason": why.value, "f": f.value, "hist": hist.reshape(-1, 5)[:it.value]}

@@ -464,3 +464,133 @@ int oracle_cg(int64_t I, int64_t J, int64_t K, int64_t R, const double *A, const
   free(x); free(r); free(p); free(z); free(tmp); free(minv);
   return status;
 }
+
+/*
+ * ---- NEXT #2: the damped Gauss-Newton outer loop of Tensor Fox, step by step.
+ * Per iteration k = 1..maxiter (the initial F, grad at w^(0) are evaluated first):
+ *   gamma_k from w^(k-1) if use_gamma, else D = I
+ *   x = CG-dGN on (J^T J + mu D) x = -grad F(w^(k-1)), cg_iters[k-1] iterations, tolerance tol,
+ *       Jacobi M = diag(J^T J) + mu diag(D) if jacobi
+ *   w^(k) = w^(k-1) + x
+ *   norm balancing: for each r, every mode's column gets norm (prod_l ||w_r^(l)||)^(1/3)
+ *   F(w^(k)); gain ratio g = (F(w^(k-1)) - F(w^(k))) / (F(w^(k-1)) - 1/2 ||f~||^2),
+ *       f~ = f(w^(k-1)) + J_f(w^(k-1)) x, evaluated entry by entry (reading R19)
+ *   damping: g < 0.25 -> mu = 3 mu; g > 0.75 -> mu = mu / 3
+ *   stopping conditions 1-7 in the paper's order (readings R20-R22)
+ * mu^(0) = mu0 if mu0 > 0 else tau * mean|T| with tau = 1.
+ * hist (nullable): per iteration [F, rel_err, mu used, g, ||x||]. Returns the stop reason (0 = maxiter,
+ * 1..7 = condition, 8 = non-finite) in *reason and the iterations done in *iters.
+ */
+static ld linearized_half_sq(int64_t I, int64_t J, int64_t K, int64_t R, const double *T, const double *A,
+                             const double *B, const double *C, const double *x) {
+  const double *xA = x, *xB = x + I * R, *xC = x + (I + J) * R;
+  ld s = 0.0L;
+  for (int64_t k = 0; k < K; ++k)
+    for (int64_t j = 0; j < J; ++j)
+      for (int64_t i = 0; i < I; ++i) {
+        ld rec = 0.0L, jx = 0.0L;
+        for (int64_t r = 0; r < R; ++r) {
+          const ld a = A[i + I * r], b = B[j + J * r], c = C[k + K * r];
+          rec += a * b * c;
+          jx -= (ld)xA[i + I * r] * b * c + a * (ld)xB[j + J * r] * c + a * b * (ld)xC[k + K * r];
+        }
+        const ld ft = ((ld)T[i + I * (j + J * k)] - rec) + jx;   /* f~ = f + J x (Lemma partialf) */
+        s += ft * ft;
+      }
+  return 0.5L * s;
+}
+
+int oracle_dgn(int64_t I, int64_t J, int64_t K, int64_t R, const double *T, double *w, int maxiter, double tol,
+               double mu0, int use_gamma, int jacobi, int balance, const int *cg_iters, int *iters, int *reason,
+               double *f_out, double *hist, int nthreads) {
+  const int64_t n = R * (I + J + K), N = I * J * K;
+  double *grad = (double *)malloc(sizeof(double) * n), *x = (double *)malloc(sizeof(double) * n);
+  double *gam = (double *)malloc(sizeof(double) * 3 * R), *wprev = (double *)malloc(sizeof(double) * n);
+  double *rel = (double *)malloc(sizeof(double) * (maxiter + 1));
+  ld nT2 = 0.0L, sabs = 0.0L;
+  for (int64_t q = 0; q < N; ++q) {
+    nT2 += (ld)T[q] * (ld)T[q];
+    sabs += fabsl((ld)T[q]);
+  }
+  const ld normT = sqrtl(nT2);
+  ld mu = mu0 > 0 ? (ld)mu0 : sabs / (ld)N;
+  double F;
+  double *gA = grad, *gB = grad + I * R, *gC = grad + (I + J) * R;
+  oracle_eval(I, J, K, R, T, w, w + I * R, w + (I + J) * R, &F, gA, gB, gC, nthreads);
+  rel[0] = (double)(sqrtl(2.0L * (ld)F) / normT);
+  const int c = 1 + (maxiter + 9) / 10;   /* c = 1 + ceil(maxiter / 10) */
+  int it = 0, why = 0;
+  for (int k = 1; k <= maxiter; ++k) {
+    const double *A = w, *B = w + I * R, *C = w + (I + J) * R;
+    if (use_gamma) oracle_reg_gamma(I, J, K, R, A, B, C, gam);
+    double *rhs = (double *)malloc(sizeof(double) * n);
+    for (int64_t q = 0; q < n; ++q) rhs[q] = -grad[q];
+    int cgit = 0;
+    int st = oracle_cg(I, J, K, R, A, B, C, rhs, (double)mu, use_gamma ? gam : NULL, cg_iters[k - 1], tol, jacobi, x,
+                       NULL, NULL, NULL, NULL, &cgit);
+    free(rhs);
+    if (st) { why = 8; break; }
+    const ld pred = (ld)F - linearized_half_sq(I, J, K, R, T, A, B, C, x);   /* predicted decrease */
+    ld step2 = 0.0L;
+    for (int64_t q = 0; q < n; ++q) {
+      wprev[q] = w[q];
+      w[q] = (double)((ld)w[q] + (ld)x[q]);
+      step2 += (ld)x[q] * (ld)x[q];
+    }
+    if (balance) {
+      const int64_t dims[3] = {I, J, K}, off[3] = {0, I * R, (I + J) * R};
+      for (int64_t r = 0; r < R; ++r) {
+        ld nr[3], prod = 1.0L;
+        for (int l = 0; l < 3; ++l) {
+          ld s = 0.0L;
+          for (int64_t a = 0; a < dims[l]; ++a) s += (ld)w[off[l] + a + dims[l] * r] * (ld)w[off[l] + a + dims[l] * r];
+          nr[l] = sqrtl(s);
+          prod *= nr[l];
+        }
+        if (prod == 0.0L) continue;
+        const ld alpha = cbrtl(prod);
+        for (int l = 0; l < 3; ++l) {
+          const ld sc = alpha / nr[l];
+          for (int64_t a = 0; a < dims[l]; ++a) w[off[l] + a + dims[l] * r] = (double)((ld)w[off[l] + a + dims[l] * r] * sc);
+        }
+      }
+    }
+    double Fn;
+    oracle_eval(I, J, K, R, T, w, w + I * R, w + (I + J) * R, &Fn, gA, gB, gC, nthreads);
+    const ld g = ((ld)F - (ld)Fn) / pred;
+    if (hist) {
+      hist[5 * (k - 1) + 0] = Fn;
+      hist[5 * (k - 1) + 1] = (double)(sqrtl(2.0L * (ld)Fn) / normT);
+      hist[5 * (k - 1) + 2] = (double)mu;
+      hist[5 * (k - 1) + 3] = (double)g;
+      hist[5 * (k - 1) + 4] = (double)sqrtl(step2);
+    }
+    if (g < 0.25L) mu *= 3.0L;
+    else if (g > 0.75L) mu /= 3.0L;
+    F = Fn;
+    it = k;
+    rel[k] = (double)(sqrtl(2.0L * (ld)F) / normT);
+    if (!isfinite(F)) { why = 8; break; }
+    ld ginf = 0.0L;
+    for (int64_t q = 0; q < n; ++q) if (fabsl((ld)grad[q]) > ginf) ginf = fabsl((ld)grad[q]);
+    /* stopping conditions in the paper's order */
+    if (rel[k] < tol) { why = 1; break; }
+    if (sqrtl(step2) < (ld)tol) { why = 2; break; }
+    if (fabs(rel[k - 1] - rel[k]) < tol) { why = 3; break; }
+    if (ginf < (ld)tol) { why = 4; break; }
+    if (k > 2 * c && k % c == 0) {
+      ld m1 = 0.0L, m2 = 0.0L, imp = 0.0L;
+      for (int t = k - 2 * c; t < k - c; ++t) m1 += rel[t];
+      for (int t = k - c; t < k; ++t) { m2 += rel[t]; imp += fabsl((ld)rel[t] - (ld)rel[t + 1]); }
+      m1 /= c; m2 /= c; imp /= c;
+      if (m1 - m2 < (ld)tol) { why = 5; break; }
+      if (imp < 1e-3L * m2) { why = 6; break; }
+    }
+    if ((ld)rel[k] > (nT2 > 1.0L ? nT2 : 1.0L) / (1e-16L + (ld)tol)) { why = 7; break; }
+  }
+  if (iters) *iters = it;
+  if (reason) *reason = why;
+  if (f_out) *f_out = F;
+  free(grad); free(x); free(gam); free(wprev); free(rel);
+  return 0;
+}

@@ -232,3 +232,14 @@ def shard_range(K: int, rank: int, world: int):
     base, extra = divmod(K, world)
     k0 = rank * base + min(rank, extra)
     return k0, k0 + base + (1 if rank < extra else 0)
+
+
+def cg_budget(maxiter: int, seed: int = 0):
+    """Tensor Fox's random CG budget: at dGN iteration k, cg_maxiter is a uniform random
+    integer in [1 + ceil(k^0.4), 2 + ceil(k^0.9)]. These are the random numbers the method draws; they are
+    drawn here (seeded) and passed to both the oracle and the CUDA path as an input."""
+    rng = np.random.default_rng(_seed(seed, "cg_budget"))
+    ks = np.arange(1, maxiter + 1)
+    lo = 1 + np.ceil(ks ** 0.4).astype(np.int64)
+    hi = 2 + np.ceil(ks ** 0.9).astype(np.int64)
+    return rng.integers(lo, hi + 1).astype(np.int32)

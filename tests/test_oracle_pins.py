@@ -468,3 +468,73 @@ def test_damped_cg_full_length_equals_dense_solve(jacobi):
     if jacobi:
         m = 1.0 / np.sqrt(np.diag(H))
         np.testing.assert_allclose((m[:, None] * H * m[None, :]).diagonal(), 1.0, rtol=1e-14)
+
+
+# --------------------------------------------------------------------------- dGN outer loop (NEXT #2)
+def test_cg_budget_interval():
+    """cg_maxiter at dGN iteration k is drawn from [1 + ceil(k^0.4), 2 + ceil(k^0.9)]."""
+    import synth
+    b = synth.cg_budget(200, seed=3)
+    ks = np.arange(1, 201)
+    assert np.all(b >= 1 + np.ceil(ks ** 0.4)) and np.all(b <= 2 + np.ceil(ks ** 0.9))
+    assert b[-1] <= 120 and b[0] in (2, 3)
+
+
+def test_linearized_model_matches_gradient_form():
+    """1/2||f + J x||^2 = F + <grad F, x> + 1/2 x^T J^T J x (gain-ratio denominator),
+    checked with the explicit Jacobian; the oracle's dGN evaluates the left side entry by entry."""
+    I, J, K, R = 4, 3, 2, 2
+    rng = np.random.default_rng(21)
+    T = rng.standard_normal(I * J * K)
+    w = rng.standard_normal(R * (I + J + K))
+    x = 0.3 * rng.standard_normal(R * (I + J + K))
+    Jm = jac.jacobian_entrywise(w, I, J, K, R)
+    r = jac.residual(T, w, I, J, K, R)
+    f, g = oracle.cpd_eval(T, w, I, J, K, R)
+    lhs = 0.5 * np.sum((r + Jm @ x) ** 2)
+    rhs_ = f + g @ x + 0.5 * x @ (Jm.T @ (Jm @ x))
+    assert abs(lhs - rhs_) <= 1e-12 * abs(lhs)
+
+
+def _exact_problem(I, J, K, R, seed):
+    rng = np.random.default_rng(seed)
+    A, B, C = (rng.standard_normal((n, R)) for n in (I, J, K))
+    t = build_T(A, B, C)
+    w0 = rng.standard_normal(R * (I + J + K))
+    return dense_T(t), w0
+
+
+def test_dgn_converges_on_exact_rank_tensor():
+    """From a random start the full dGN iteration (gamma damping, Jacobi CG, norm balancing, random CG budget)
+    drives the relative error of an exactly rank-3 tensor below tol (stopping condition 1)."""
+    import synth
+    I, J, K, R = 9, 8, 7, 3
+    T, w0 = _exact_problem(I, J, K, R, 5)
+    out = oracle.dgn(T, w0, I, J, K, R, synth.cg_budget(200, seed=1), tol=1e-6)
+    assert out["reason"] == 1, out
+    assert out["hist"][-1, 1] < 1e-6
+
+
+def test_dgn_damping_rule_and_balancing():
+    """mu^(0) = mean|T| (tau = 1, PAPER.md:2626); g < 0.25 -> 3 mu, g > 0.75 -> mu / 3 (PAPER.md:2744-2749);
+    norm balancing leaves the tensor (hence F) unchanged and equalises the column norms."""
+    import synth
+    I, J, K, R = 6, 5, 4, 3
+    T, w0 = _exact_problem(I, J, K, R, 9)
+    T = T + 0.05 * np.random.default_rng(1).standard_normal(T.size)
+    cgi = synth.cg_budget(12, seed=2)
+    out = oracle.dgn(T, w0, I, J, K, R, cgi, maxiter=12, tol=0.0)
+    h = out["hist"]
+    assert abs(h[0, 2] - np.mean(np.abs(T))) <= 1e-15 * h[0, 2]
+    for k in range(len(h) - 1):
+        g, mu, mun = h[k, 3], h[k, 2], h[k + 1, 2]
+        want = 3 * mu if g < 0.25 else (mu / 3 if g > 0.75 else mu)
+        assert abs(mun - want) <= 1e-14 * want
+    # balancing: same F trajectory for the first step with and without it; balanced norms are equal
+    nb = oracle.dgn(T, w0, I, J, K, R, cgi, maxiter=1, tol=0.0, balance=False)
+    bb = oracle.dgn(T, w0, I, J, K, R, cgi, maxiter=1, tol=0.0, balance=True)
+    assert abs(nb["hist"][0, 0] - bb["hist"][0, 0]) <= 1e-12 * nb["hist"][0, 0]
+    A, B, C = jac.factors_from_w(bb["w"], I, J, K, R)
+    na, nb_, nc = (np.linalg.norm(M, axis=0) for M in (A, B, C))
+    np.testing.assert_allclose(na, nb_, rtol=1e-13)
+    np.testing.assert_allclose(na, nc, rtol=1e-13)
