@@ -141,6 +141,38 @@ tf_status tf_cg_solve_damped(tf_ctx *ctx, tf_dims d, const double *grams, const 
                              double mu, const double *damp, int maxiter, double tol, int jacobi, double *x,
                              int *iters_done, double *res2);
 
+/* NEXT #2 -- the damped Gauss-Newton outer loop of Tensor Fox around the hot path,
+ * run by the library on the device (one host synchronisation per dGN iteration). Iteration k:
+ *   x = CG-dGN on (J^T J + mu D) x = -grad F(w) with cg_iters[k-1] iterations, CG tolerance tol
+ *       (D = Tensor Fox's gamma if use_gamma else I; Jacobi M = diag(J^T J) + mu diag(D) if jacobi);
+ *   w += x; norm balancing if balance; F, grad at the new w (fused evaluation);
+ *   gain ratio g = (F_old - F_new) / (-<grad_old, x> - 1/2 x^T J^T J x);
+ *   g < 0.25 -> mu *= 3, g > 0.75 -> mu /= 3; stopping conditions 1-7.
+ * mu^(0) = mu0 if > 0 else mean |T| (tau = 1). cg_iters (host) holds the random CG budgets
+ * drawn by the caller from [1 + ceil(k^0.4), 2 + ceil(k^0.9)]. */
+typedef struct {
+  int maxiter;          /* dGN iterations (paper default 200) */
+  double tol;           /* every stopping tolerance and the CG tolerance (paper default 1e-6) */
+  double mu0;           /* initial damping; <= 0 selects mean |T| */
+  int use_gamma;        /* 1: damping mu*D with Tensor Fox's gamma; 0: mu*I */
+  int jacobi;           /* 1: Jacobi-preconditioned CG */
+  int balance;          /* 1: norm-balance the factors after every step */
+  const int *cg_iters;  /* host, >= maxiter entries */
+} tf_dgn_params;
+
+typedef struct {
+  int iters;            /* dGN iterations done */
+  int reason;           /* 0 maxiter; 1..7 stopping condition of PAPER.md:2756-2773; 8 non-finite */
+  double f;             /* F at the returned w */
+  double rel_err;       /* ||T - [[A,B,C]]|| / ||T|| */
+  double mu;            /* damping after the last update */
+} tf_dgn_result;
+
+/* Runs the dGN loop from w (device, n doubles, overwritten with the result). Requires the whole tensor
+ * (K == K_total). hist (host, nullable): 5 doubles per iteration [F, rel_err, mu used, g, ||x||]. */
+tf_status tf_cpd_dgn(tf_ctx *ctx, tf_dims d, const double *T, double *w, const tf_dgn_params *prm,
+                     tf_dgn_result *res, double *hist);
+
 /* Instrumentation (bench.py): when enabled, the fused evaluation kernel is
  * bracketed by CUDA events on the ctx stream; tf_ctx_kernel_stats synchronizes
  * and returns the summed device time (ms) and count of the fused-kernel launches

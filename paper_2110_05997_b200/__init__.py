@@ -53,13 +53,27 @@ _lib.tf_reg_gamma.argtypes = [_vp, ctypes.c_int64, _vp, _vp]
 _lib.tf_gn_matvec_damped.argtypes = [_vp, TfDims, _vp, _vp, _vp, ctypes.c_double, _vp, _vp]
 _lib.tf_cg_solve_damped.argtypes = [_vp, TfDims, _vp, _vp, _vp, ctypes.c_double, _vp, ctypes.c_int, ctypes.c_double,
                                     ctypes.c_int, _vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double)]
+class TfDgnParams(ctypes.Structure):
+    _fields_ = [("maxiter", ctypes.c_int), ("tol", ctypes.c_double), ("mu0", ctypes.c_double),
+                ("use_gamma", ctypes.c_int), ("jacobi", ctypes.c_int), ("balance", ctypes.c_int),
+                ("cg_iters", ctypes.POINTER(ctypes.c_int))]
+
+
+class TfDgnResult(ctypes.Structure):
+    _fields_ = [("iters", ctypes.c_int), ("reason", ctypes.c_int), ("f", ctypes.c_double),
+                ("rel_err", ctypes.c_double), ("mu", ctypes.c_double)]
+
+
+_lib.tf_cpd_dgn.argtypes = [_vp, TfDims, _vp, _vp, ctypes.POINTER(TfDgnParams), ctypes.POINTER(TfDgnResult),
+                            ctypes.POINTER(ctypes.c_double)]
 _lib.tf_ctx_set_timing.argtypes = [_vp, ctypes.c_int]
 _lib.tf_ctx_kernel_stats.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64),
                                      ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
 
 EXPORTED = ["tf_ctx_create", "tf_ctx_destroy", "tf_ctx_set_stream", "tf_status_str", "tf_last_error", "tf_version",
             "tf_grams", "tf_hadamard", "tf_cpd_eval", "tf_cpd_eval_host", "tf_gn_matvec", "tf_cg_solve",
-            "tf_reg_gamma", "tf_gn_matvec_damped", "tf_cg_solve_damped", "tf_ctx_set_timing", "tf_ctx_kernel_stats"]
+            "tf_reg_gamma", "tf_gn_matvec_damped", "tf_cg_solve_damped", "tf_cpd_dgn", "tf_ctx_set_timing",
+            "tf_ctx_kernel_stats"]
 
 TF_OK, TF_ERR_ARG, TF_ERR_ALIGN, TF_ERR_UNSUPPORTED, TF_ERR_CUDA, TF_ERR_NONFINITE, TF_ERR_ALLOC = range(7)
 MAX_R = 128
@@ -258,6 +272,29 @@ class Context:
                                             int(maxiter), float(tol), int(bool(jacobi)), _ptr(x), ctypes.byref(it),
                                             ctypes.byref(r2)))
         return x, it.value, r2.value
+
+    def tf_cpd_dgn(self, d: Dims, T: torch.Tensor, w: torch.Tensor, cg_iters, maxiter: int | None = None,
+                   tol: float = 1e-6, mu0: float = 0.0, use_gamma: bool = True, jacobi: bool = True,
+                   balance: bool = True):
+        """Tensor Fox's dGN loop on the device; w (device) is updated in place.
+        cg_iters: the per-iteration random CG budgets (e.g. synth.cg_budget). Returns (result dict, history
+        array [iters, 5] = F, rel_err, mu, g, ||x||)."""
+        import numpy as np
+        ldT = d.ldT or d.I
+        _dev(T, "T", ldT * d.J * d.K - (ldT - d.I))
+        _dev(w, "w", d.n)
+        cgi = np.ascontiguousarray(np.asarray(cg_iters, dtype=np.int32))
+        m = int(maxiter if maxiter is not None else cgi.size)
+        if cgi.size < m:
+            raise ValueError("cg_iters shorter than maxiter")
+        prm = TfDgnParams(m, float(tol), float(mu0), int(bool(use_gamma)), int(bool(jacobi)), int(bool(balance)),
+                          cgi.ctypes.data_as(ctypes.POINTER(ctypes.c_int)))
+        res = TfDgnResult()
+        hist = np.zeros(5 * max(m, 1))
+        self._check(_lib.tf_cpd_dgn(self._h, d.c(), _ptr(T), _ptr(w), ctypes.byref(prm), ctypes.byref(res),
+                                    hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        out = {"iters": res.iters, "reason": res.reason, "f": res.f, "rel_err": res.rel_err, "mu": res.mu}
+        return out, hist.reshape(-1, 5)[:res.iters]
 
     def set_timing(self, enable: bool):
         self._check(_lib.tf_ctx_set_timing(self._h, int(bool(enable))))

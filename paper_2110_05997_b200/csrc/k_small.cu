@@ -203,3 +203,142 @@ cudaError_t launch_axpy1(int64_t n, const double* x, double* y, cudaStream_t st)
 }
 
 }  // namespace tfk
+
+namespace tfk {
+
+// ---------------------------------------------------------------------------------- dGN outer-loop helpers
+// Fixed-order reductions: per-block partials, then one block sums them in order (deterministic).
+constexpr int kRedBlocks = 296;
+
+// partial[b][0..3] = { sum g*x, sum x*y, sum x*x, max |g| } over this block's grid-stride share
+__global__ void k_dots_partial(int64_t n, const double* __restrict__ g, const double* __restrict__ x,
+                               const double* __restrict__ y, double* __restrict__ partial) {
+  __shared__ double red[4][8];
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, m = 0.0;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const double xv = x[q], gv = g[q];
+    s0 = fma(gv, xv, s0);
+    s1 = fma(xv, y[q], s1);
+    s2 = fma(xv, xv, s2);
+    m = fmax(m, fabs(gv));
+  }
+  s0 = warp_sum(s0);
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red[0][w] = s0;
+    red[1][w] = s1;
+    red[2][w] = s2;
+    red[3][w] = m;
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    double v = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i)
+      v = threadIdx.x == 3 ? fmax(v, red[3][i]) : v + red[threadIdx.x][i];
+    partial[blockIdx.x * 4 + threadIdx.x] = v;
+  }
+}
+
+// partial[b][0..1] = { sum |t|, sum t^2 } over the I x J x K tensor with leading dimension ldT
+__global__ void k_tsums_partial(int64_t I, int64_t JK, int64_t ldT, const double* __restrict__ T,
+                                double* __restrict__ partial) {
+  __shared__ double red[2][8];
+  double sa = 0.0, s2 = 0.0;
+  const int64_t N = I * JK;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < N; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = q % I, jk = q / I;
+    const double t = T[i + ldT * jk];
+    sa += fabs(t);
+    s2 = fma(t, t, s2);
+  }
+  sa = warp_sum(sa);
+  s2 = warp_sum(s2);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    red[0][w] = sa;
+    red[1][w] = s2;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    double v = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) v += red[threadIdx.x][i];
+    partial[blockIdx.x * 2 + threadIdx.x] = v;
+  }
+}
+
+// out[c] = ordered combination over blocks of partial[b][c] (c < ncomp; component 3 of the dots is a max)
+__global__ void k_partial_final(int nblk, int ncomp, int max_comp, const double* __restrict__ partial,
+                                double* __restrict__ out) {
+  if (threadIdx.x < ncomp) {
+    double v = 0.0;
+    for (int b = 0; b < nblk; ++b) {
+      const double p = partial[b * ncomp + threadIdx.x];
+      v = (int)threadIdx.x == max_comp ? fmax(v, p) : v + p;
+    }
+    out[threadIdx.x] = v;
+  }
+}
+
+__global__ void k_axpy_inplace(int64_t n, const double* __restrict__ x, double* __restrict__ w) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    w[q] += x[q];
+}
+
+// Norm balancing: column r of every mode gets the norm (prod_l ||w_r^(l)||)^(1/3); column
+// norms from the Grams' diagonals. Columns of a rank-one term with a zero factor are left unchanged.
+__global__ void k_balance(Modes m, const double* __restrict__ grams, double* __restrict__ w) {
+  const int64_t R = m.R, RR = R * R;
+  const int64_t n = R * (m.n[0] + m.n[1] + m.n[2]);
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const int l = q >= m.off[2] ? 2 : (q >= m.off[1] ? 1 : 0);
+    const int64_t r = (q - m.off[l]) / m.n[l];
+    const double n0 = sqrt(grams[r + R * r]), n1 = sqrt(grams[RR + r + R * r]), n2 = sqrt(grams[2 * RR + r + R * r]);
+    const double prod = n0 * n1 * n2;
+    if (prod == 0.0) continue;
+    const double nl = l == 0 ? n0 : (l == 1 ? n1 : n2);
+    w[q] *= cbrt(prod) / nl;
+  }
+}
+
+cudaError_t launch_dots(int64_t n, const double* g, const double* x, const double* y, double* partial, double* out,
+                        cudaStream_t st) {
+  k_dots_partial<<<kRedBlocks, 256, 0, st>>>(n, g, x, y, partial);
+  k_partial_final<<<1, 32, 0, st>>>(kRedBlocks, 4, 3, partial, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tsums(int64_t I, int64_t J, int64_t K, int64_t ldT, const double* T, double* partial, double* out,
+                         cudaStream_t st) {
+  k_tsums_partial<<<kRedBlocks, 256, 0, st>>>(I, J * K, ldT, T, partial);
+  k_partial_final<<<1, 32, 0, st>>>(kRedBlocks, 2, -1, partial, out);
+  return cudaGetLastError();
+}
+
+__global__ void k_scale_copy(int64_t n, double alpha, const double* __restrict__ x, double* __restrict__ y) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    y[q] = alpha * x[q];
+}
+
+cudaError_t launch_scale_copy(int64_t n, double alpha, const double* x, double* y, cudaStream_t st) {
+  k_scale_copy<<<vec_blocks(n), 256, 0, st>>>(n, alpha, x, y);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_axpy_inplace(int64_t n, const double* x, double* w, cudaStream_t st) {
+  k_axpy_inplace<<<vec_blocks(n), 256, 0, st>>>(n, x, w);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_balance(const Modes& m, const double* grams, double* w, cudaStream_t st) {
+  const int64_t n = m.R * (m.n[0] + m.n[1] + m.n[2]);
+  k_balance<<<vec_blocks(n), 256, 0, st>>>(m, grams, w);
+  return cudaGetLastError();
+}
+
+int red_blocks() { return kRedBlocks; }
+
+}  // namespace tfk

@@ -3,6 +3,7 @@
 // every step runs in the kernels of k_eval.cu, k_cg.cu and k_small.cu.
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -27,6 +28,8 @@ struct tf_ctx {
   DevBuf mvG, mvS, mvPi, mvD, mvPart;       // matvec / CG scratch
   DevBuf cgR, cgP, cgZ, cgState;            // CG vectors and state
   DevBuf hostW, hostGrad, hostGradTmp, hostF, hostStage[2];  // host-streamed eval
+  DevBuf dgnGrad, dgnX, dgnY, dgnGrams, dgnGamma, dgnScal, dgnPart;  // dGN outer loop
+  double* scal_host = nullptr;              // pinned, dGN scalars
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
   CgState* cg_host = nullptr;               // pinned
@@ -275,7 +278,8 @@ tf_status tf_ctx_create(tf_ctx** out, int device, void* cuda_stream) {
   c->device = device;
   c->stream = static_cast<cudaStream_t>(cuda_stream);
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device);
-  if (cudaMallocHost(&c->cg_host, sizeof(CgState)) != cudaSuccess) {
+  if (cudaMallocHost(&c->cg_host, sizeof(CgState)) != cudaSuccess ||
+      cudaMallocHost(&c->scal_host, 16 * sizeof(double)) != cudaSuccess) {
     delete c;
     return TF_ERR_ALLOC;
   }
@@ -289,7 +293,8 @@ tf_status tf_ctx_destroy(tf_ctx* c) {
   cudaStreamSynchronize(c->stream);
   DevBuf* bufs[] = {&c->gAp, &c->gBp, &c->gCp, &c->fp, &c->gram_part, &c->mvG, &c->mvS, &c->mvPi, &c->mvD,
                     &c->mvPart, &c->cgR, &c->cgP, &c->cgZ, &c->cgState, &c->hostW, &c->hostGrad,
-                    &c->hostGradTmp, &c->hostF, &c->hostStage[0], &c->hostStage[1]};
+                    &c->hostGradTmp, &c->hostF, &c->hostStage[0], &c->hostStage[1], &c->dgnGrad, &c->dgnX,
+                    &c->dgnY, &c->dgnGrams, &c->dgnGamma, &c->dgnScal, &c->dgnPart};
   for (DevBuf* b : bufs) free_buf(*b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (int i = 0; i < 2; ++i) {
@@ -298,6 +303,7 @@ tf_status tf_ctx_destroy(tf_ctx* c) {
   }
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->cg_host) cudaFreeHost(c->cg_host);
+  if (c->scal_host) cudaFreeHost(c->scal_host);
   delete c;
   return TF_OK;
 }
@@ -469,6 +475,29 @@ tf_status tf_gn_matvec(tf_ctx* c, tf_dims d, const double* grams, const double* 
   return tf_gn_matvec_damped(c, d, grams, w, v, lambda, nullptr, y);
 }
 
+// CG on (J^T J + lambda D) x = rhs; the state (iterations, ||r||^2, non-finite flag) lands in c->cgState.
+static tf_status cg_impl(tf_ctx* c, const tf_dims& d, const double* grams, const double* w, const double* rhs,
+                         double lambda, const double* damp, int maxiter, double tol, int jacobi, double* x) {
+  Modes m = make_modes(d, w);
+  const int64_t n = d.R * (d.I + d.J + d.K_total);
+  MatvecWs ws;
+  tf_status s;
+  if ((s = matvec_ws(c, d, m, ws))) return s;
+  if ((s = ensure(c, c->cgR, n * 8))) return s;
+  if ((s = ensure(c, c->cgP, n * 8))) return s;
+  if ((s = ensure(c, c->cgZ, n * 8))) return s;
+  if ((s = ensure(c, c->cgState, sizeof(CgState)))) return s;
+  CgState* st = (CgState*)c->cgState.p;
+  TF_CUDA(c, cudaMemsetAsync(st, 0, sizeof(CgState), c->stream));
+  TF_CUDA(c, launch_hadamard(d.R, grams, ws.pi, c->stream));
+  if (jacobi) TF_CUDA(c, launch_jacobi_scale(m, ws.pi, lambda, damp, ws.dscale, c->stream));
+  TF_CUDA(c, launch_cg_persistent(m, ws.pi, jacobi ? ws.dscale : nullptr, damp, lambda, tol, maxiter, rhs, nullptr, x,
+                                  (double*)c->cgR.p, (double*)c->cgP.p, (double*)c->cgZ.p, ws.G, ws.S, ws.partial, st,
+                                  0, c->nsm, c->stream));
+  c->total_launches += 2 + (jacobi ? 1 : 0);
+  return TF_OK;
+}
+
 tf_status tf_cg_solve_damped(tf_ctx* c, tf_dims d, const double* grams, const double* w, const double* rhs,
                              double lambda, const double* damp, int maxiter, double tol, int jacobi, double* x,
                              int* iters_done, double* res2) {
@@ -477,31 +506,142 @@ tf_status tf_cg_solve_damped(tf_ctx* c, tf_dims d, const double* grams, const do
   if (!grams || !w || !rhs || !x) return set_err(c, TF_ERR_ARG, "null pointer");
   if (maxiter < 0) return set_err(c, TF_ERR_ARG, "maxiter < 0");
   cudaSetDevice(c->device);
-  Modes m = make_modes(d, w);
-  const int64_t n = d.R * (d.I + d.J + d.K_total);
-  MatvecWs ws;
-  if ((s = matvec_ws(c, d, m, ws))) return s;
-  if ((s = ensure(c, c->cgR, n * 8))) return s;
-  if ((s = ensure(c, c->cgP, n * 8))) return s;
-  if ((s = ensure(c, c->cgZ, n * 8))) return s;
-  if ((s = ensure(c, c->cgState, sizeof(CgState)))) return s;
-  double* r = (double*)c->cgR.p;
-  double* p = (double*)c->cgP.p;
-  double* z = (double*)c->cgZ.p;
-  CgState* st = (CgState*)c->cgState.p;
-  TF_CUDA(c, cudaMemsetAsync(st, 0, sizeof(CgState), c->stream));
-  TF_CUDA(c, launch_hadamard(d.R, grams, ws.pi, c->stream));
-  if (jacobi) TF_CUDA(c, launch_jacobi_scale(m, ws.pi, lambda, damp, ws.dscale, c->stream));
-  TF_CUDA(c, launch_cg_persistent(m, ws.pi, jacobi ? ws.dscale : nullptr, damp, lambda, tol, maxiter, rhs, nullptr, x,
-                                  r, p, z, ws.G, ws.S, ws.partial, st, 0, c->nsm, c->stream));
-  c->total_launches += 2 + (jacobi ? 1 : 0);
-  TF_CUDA(c, cudaMemcpyAsync(c->cg_host, st, sizeof(CgState), cudaMemcpyDeviceToHost, c->stream));
+  if ((s = cg_impl(c, d, grams, w, rhs, lambda, damp, maxiter, tol, jacobi, x))) return s;
+  TF_CUDA(c, cudaMemcpyAsync(c->cg_host, c->cgState.p, sizeof(CgState), cudaMemcpyDeviceToHost, c->stream));
   TF_CUDA(c, cudaStreamSynchronize(c->stream));
   if (iters_done) *iters_done = c->cg_host->iters;
   if (res2) *res2 = c->cg_host->rr;
   if (c->cg_host->nonfinite)
     return set_err(c, TF_ERR_NONFINITE,
                    "CG: non-finite alpha/beta at iteration " + std::to_string(c->cg_host->nonfinite));
+  return TF_OK;
+}
+
+tf_status tf_cpd_dgn(tf_ctx* c, tf_dims d, const double* T, double* w, const tf_dgn_params* prm, tf_dgn_result* res,
+                     double* hist) {
+  tf_status s = check_dims(c, d);
+  if (s) return s;
+  if (!T || !w || !prm || !res || (prm->maxiter > 0 && !prm->cg_iters)) return set_err(c, TF_ERR_ARG, "null pointer");
+  if (d.K != d.K_total || d.k_begin != 0)
+    return set_err(c, TF_ERR_UNSUPPORTED, "tf_cpd_dgn needs the whole tensor on one device (K == K_total)");
+  if (prm->maxiter < 0) return set_err(c, TF_ERR_ARG, "maxiter < 0");
+  cudaSetDevice(c->device);
+  const int64_t n = d.R * (d.I + d.J + d.K_total), RR = d.R * d.R;
+  if ((s = ensure(c, c->dgnGrad, n * 8))) return s;
+  if ((s = ensure(c, c->dgnX, n * 8))) return s;
+  if ((s = ensure(c, c->dgnY, n * 8))) return s;
+  if ((s = ensure(c, c->dgnGrams, 3 * RR * 8))) return s;
+  if ((s = ensure(c, c->dgnGamma, 3 * d.R * 8))) return s;
+  if ((s = ensure(c, c->dgnScal, 16 * 8))) return s;
+  if ((s = ensure(c, c->dgnPart, (size_t)red_blocks() * 4 * 8))) return s;
+  double* grad = (double*)c->dgnGrad.p;
+  double* x = (double*)c->dgnX.p;
+  double* y = (double*)c->dgnY.p;
+  double* grams = (double*)c->dgnGrams.p;
+  double* gamma = (double*)c->dgnGamma.p;
+  double* scal = (double*)c->dgnScal.p;   // [0] F, [1..2] tensor sums, [4..7] dots
+  double* part = (double*)c->dgnPart.p;
+  double* hs = c->scal_host;
+  const Modes m = make_modes(d, w);
+  if ((s = ensure(c, c->cgState, sizeof(CgState)))) return s;
+  TF_CUDA(c, cudaMemsetAsync(c->cgState.p, 0, sizeof(CgState), c->stream));
+  auto sync_scalars = [&]() -> tf_status {
+    TF_CUDA(c, cudaMemcpyAsync(hs, scal, 12 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    TF_CUDA(c, cudaMemcpyAsync(c->cg_host, c->cgState.p, sizeof(CgState), cudaMemcpyDeviceToHost, c->stream));
+    TF_CUDA(c, cudaStreamSynchronize(c->stream));
+    return TF_OK;
+  };
+  // ||T||^2, mean |T|, F and grad at w0
+  TF_CUDA(c, launch_tsums(d.I, d.J, d.K, d.ldT, T, part, scal + 1, c->stream));
+  if ((s = eval_impl(c, d, T, w, scal, grad))) return s;
+  if ((s = grams_impl(c, d, w, grams))) return s;
+  c->total_launches += 2;
+  if ((s = sync_scalars())) return s;
+  const double normT2 = hs[2], normT = sqrt(normT2);
+  const double N = (double)d.I * d.J * d.K;
+  double mu = prm->mu0 > 0 ? prm->mu0 : hs[1] / N;
+  double F = hs[0];
+  std::vector<double> rel(prm->maxiter + 1);
+  rel[0] = normT > 0 ? sqrt(2.0 * F) / normT : 0.0;
+  const int cc = 1 + (prm->maxiter + 9) / 10;   // c = 1 + ceil(maxiter / 10)
+  const double tol = prm->tol;
+  int it = 0, why = 0;
+  for (int k = 1; k <= prm->maxiter; ++k) {
+    if (prm->use_gamma) {
+      TF_CUDA(c, launch_reg_gamma(d.R, grams, gamma, c->stream));
+      c->total_launches += 1;
+    }
+    TF_CUDA(c, launch_scale_copy(n, -1.0, grad, y, c->stream));   // rhs = -grad F(w^(k-1))
+    if ((s = cg_impl(c, d, grams, w, y, mu, prm->use_gamma ? gamma : nullptr, prm->cg_iters[k - 1], tol,
+                     prm->jacobi, x)))
+      return s;
+    // x^T J^T J x for the predicted decrease: one GN matvec with lambda = 0 (rhs in y is consumed by now)
+    {
+      MatvecWs ws;
+      if ((s = matvec_ws(c, d, m, ws))) return s;
+      TF_CUDA(c, launch_hadamard(d.R, grams, ws.pi, c->stream));
+      TF_CUDA(c, launch_cg_persistent(m, ws.pi, nullptr, nullptr, 0.0, 0.0, 0, nullptr, x, y, nullptr, nullptr,
+                                      nullptr, ws.G, ws.S, ws.partial, nullptr, 1, c->nsm, c->stream));
+    }
+    TF_CUDA(c, launch_dots(n, grad, x, y, part, scal + 4, c->stream));   // {g.x, x.JtJx, x.x, max|g_old|}
+    TF_CUDA(c, launch_axpy_inplace(n, x, w, c->stream));                 // w^(k) = w^(k-1) + x
+    if (prm->balance) {
+      if ((s = grams_impl(c, d, w, grams))) return s;
+      TF_CUDA(c, launch_balance(m, grams, w, c->stream));
+    }
+    if ((s = eval_impl(c, d, T, w, scal, grad))) return s;               // F, grad at w^(k)
+    if ((s = grams_impl(c, d, w, grams))) return s;
+    TF_CUDA(c, launch_dots(n, grad, grad, grad, part, scal + 8, c->stream));   // [11] = ||grad||_inf
+    c->total_launches += 12;
+    if ((s = sync_scalars())) return s;
+    if (c->cg_host->nonfinite) {
+      why = 8;
+      break;
+    }
+    const double Fn = hs[0], gx = hs[4], xjjx = hs[5], step = sqrt(hs[6]), ginf = hs[11];
+    const double pred = -gx - 0.5 * xjjx;          // F(w_old) - 1/2 ||f + J x||^2
+    const double g = (F - Fn) / pred;
+    if (hist) {
+      hist[5 * (k - 1) + 0] = Fn;
+      hist[5 * (k - 1) + 1] = normT > 0 ? sqrt(2.0 * Fn) / normT : 0.0;
+      hist[5 * (k - 1) + 2] = mu;
+      hist[5 * (k - 1) + 3] = g;
+      hist[5 * (k - 1) + 4] = step;
+    }
+    if (g < 0.25) mu *= 3.0;
+    else if (g > 0.75) mu /= 3.0;
+    F = Fn;
+    it = k;
+    rel[k] = normT > 0 ? sqrt(2.0 * F) / normT : 0.0;
+    if (!std::isfinite(F)) {
+      why = 8;
+      break;
+    }
+    // stopping conditions in the order of PAPER.md:2756-2773
+    if (rel[k] < tol) { why = 1; break; }
+    if (step < tol) { why = 2; break; }
+    if (fabs(rel[k - 1] - rel[k]) < tol) { why = 3; break; }
+    if (ginf < tol) { why = 4; break; }
+    if (k > 2 * cc && k % cc == 0) {
+      double m1 = 0.0, m2 = 0.0, imp = 0.0;
+      for (int t = k - 2 * cc; t < k - cc; ++t) m1 += rel[t];
+      for (int t = k - cc; t < k; ++t) {
+        m2 += rel[t];
+        imp += fabs(rel[t] - rel[t + 1]);
+      }
+      m1 /= cc;
+      m2 /= cc;
+      imp /= cc;
+      if (m1 - m2 < tol) { why = 5; break; }
+      if (imp < 1e-3 * m2) { why = 6; break; }
+    }
+    if (rel[k] > std::max(1.0, normT2) / (1e-16 + tol)) { why = 7; break; }
+  }
+  res->iters = it;
+  res->reason = why;
+  res->f = F;
+  res->rel_err = normT > 0 ? sqrt(2.0 * F) / normT : 0.0;
+  res->mu = mu;
   return TF_OK;
 }
 

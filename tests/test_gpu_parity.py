@@ -400,3 +400,46 @@ def test_cg_damped_per_iteration(ctx, jacobi):
         x, it, r2 = ctx.tf_cg_solve_damped(d, g, wt, torch.from_numpy(-grad).cuda(), mu, gt, i, 0.0, jacobi)
         assert it == i
         assert rel_err(to_np(x), ref["x_hist"][i - 1]) <= 1e-9, i
+
+
+# ------------------------------------------------------------------------- NEXT #2: the dGN outer loop
+def _exact_plus_noise(I, J, K, R, seed, sigma):
+    rng = np.random.default_rng(seed)
+    A, B, C = (rng.standard_normal((n, R)) for n in (I, J, K))
+    t = np.einsum("ir,jr,kr->ijk", A, B, C) + sigma * rng.standard_normal((I, J, K))
+    T = np.ascontiguousarray(t.transpose(2, 1, 0)).reshape(-1)
+    return T, rng.standard_normal(R * (I + J + K))
+
+
+@pytest.mark.parametrize("use_gamma,jacobi", [(True, True), (False, False)])
+def test_dgn_trajectory_matches_oracle(ctx, use_gamma, jacobi):
+    """The first dGN iterations (same random CG budgets) match the oracle's iterates: F, mu, g, ||x|| and w."""
+    I, J, K, R = 14, 11, 9, 3
+    T, w0 = _exact_plus_noise(I, J, K, R, 3, 1e-2)
+    cgi = synth.cg_budget(8, seed=4)
+    ref = oracle.dgn(T, w0, I, J, K, R, cgi, maxiter=8, tol=0.0, use_gamma=use_gamma, jacobi=jacobi)
+    wt = torch.from_numpy(w0.copy()).cuda()
+    out, hist = ctx.tf_cpd_dgn(tf.Dims(I, J, K, R), torch.from_numpy(T).cuda(), wt, cgi, maxiter=8, tol=0.0,
+                               use_gamma=use_gamma, jacobi=jacobi)
+    assert out["iters"] == ref["iters"] >= 5 and out["reason"] == ref["reason"]   # same stop (condition 5 here)
+    h, hr = hist, ref["hist"]
+    np.testing.assert_array_equal(np.sign(h[:, 3] - 0.25), np.sign(hr[:, 3] - 0.25))   # same damping decisions
+    assert rel_err(h[:, 2], hr[:, 2]) <= 1e-12                                      # mu history
+    assert rel_err(h[:, 0], hr[:, 0]) <= 1e-8                                       # F history
+    assert rel_err(h[:, 4], hr[:, 4]) <= 1e-8                                       # step norms
+    assert rel_err(to_np(wt), ref["w"]) <= 1e-8
+
+
+def test_dgn_converges_on_exact_rank_tensor(ctx):
+    """Full run to a stopping condition on an exactly rank-3 tensor: same stop as the oracle, converged fit."""
+    I, J, K, R = 9, 8, 7, 3
+    T, w0 = _exact_plus_noise(I, J, K, R, 5, 0.0)
+    cgi = synth.cg_budget(200, seed=1)
+    ref = oracle.dgn(T, w0, I, J, K, R, cgi, tol=1e-6)
+    wt = torch.from_numpy(w0.copy()).cuda()
+    out, hist = ctx.tf_cpd_dgn(tf.Dims(I, J, K, R), torch.from_numpy(T).cuda(), wt, cgi, tol=1e-6)
+    assert out["reason"] == ref["reason"] and out["iters"] == ref["iters"], (out, ref["reason"], ref["iters"])
+    assert out["rel_err"] < 1e-5
+    assert abs(out["rel_err"] - ref["hist"][-1, 1]) <= 1e-6 * ref["hist"][-1, 1] + 1e-12
+    f, _ = oracle.cpd_eval(T, to_np(wt), I, J, K, R)
+    assert abs(f - out["f"]) <= 1e-6 * f + 1e-24
