@@ -87,6 +87,16 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 #ifdef TF_EVAL_PROFILE
 // Development timeline: CTA 0, lane 0 of every warp records clock64 at 8 points of its first 16 slices.
 __device__ unsigned long long g_eval_tl[16 * 16 * 8];
+__device__ unsigned long long g_eval_cta[4096 * 4];   // per CTA: globaltimer at start, loop start, loop end, end
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TLC(pt)                                                                   \
+  do {                                                                            \
+    if (threadIdx.x == 0 && blockIdx.x < 4096) g_eval_cta[blockIdx.x * 4 + (pt)] = gtimer(); \
+  } while (0)
 #define TL(kk, pt)                                                                                          \
   do {                                                                                                      \
     if (blockIdx.x == 0 && lane == 0 && (kk) < 16) g_eval_tl[((kk) * 16 + warp) * 8 + (pt)] = clock64(); \
@@ -94,6 +104,9 @@ __device__ unsigned long long g_eval_tl[16 * 16 * 8];
 #else
 #define TL(kk, pt) \
   do {             \
+  } while (0)
+#define TLC(pt) \
+  do {          \
   } while (0)
 #endif
 
@@ -144,6 +157,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
   };
 
   // ---- prologue
+  TLC(0);
   if (tid == 0) {
     if (kTMA) prefetch_tmap(&tmapT);
     mbar_init(&full[0], 1);
@@ -160,22 +174,52 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
     }
   }
   if (!kTMA && nk > 0) load_tile_plain(kA, sTE);
-  for (int idx = tid; idx < kBJ * LDF; idx += kThreads) {
-    const int j = idx / LDF, r = idx % LDF;
-    const int64_t gj = j0 + j;
-    sB[idx] = (gj < p.J && r < p.R) ? p.B[gj + p.J * r] : 0.0;
+  // Factor tiles, coalesced along the contiguous (row) index of the column-major factors and batched so
+  // that 8 loads per thread are in flight: B -> sB (unscaled, kept), A -> sAc (unscaled, staging only).
+  {
+    constexpr int kLoadBatch = 8;
+    for (int base = tid; base < kBJ * LDF; base += kLoadBatch * kThreads) {
+      double v[kLoadBatch];
+#pragma unroll
+      for (int u = 0; u < kLoadBatch; ++u) {
+        const int idx = base + u * kThreads;
+        const int j = idx % kBJ, r = idx / kBJ;
+        const int64_t gj = j0 + j;
+        const bool ok = idx < kBJ * LDF && gj < p.J && r < p.R;
+        v[u] = ok ? p.B[gj + p.J * r] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kLoadBatch; ++u) {
+        const int idx = base + u * kThreads;
+        if (idx < kBJ * LDF) sB[(idx % kBJ) * LDF + idx / kBJ] = v[u];
+      }
+    }
+    for (int base = tid; base < kBI * LDF; base += kLoadBatch * kThreads) {
+      double v[kLoadBatch];
+#pragma unroll
+      for (int u = 0; u < kLoadBatch; ++u) {
+        const int idx = base + u * kThreads;
+        const int i = idx % kBI, r = idx / kBI;
+        const int64_t gi = i0 + i;
+        const bool ok = idx < kBI * LDF && gi < p.I && r < p.R;
+        v[u] = ok ? p.A[gi + p.I * r] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < kLoadBatch; ++u) {
+        const int idx = base + u * kThreads;
+        if (idx < kBI * LDF) sAc[(idx % kBI) * LDF + idx / kBI] = v[u];
+      }
+    }
   }
+  __syncthreads();
   // Unscaled A, distributed over the CTA: thread (warp, g, q) owns A[8*warp + 2q + e][8t + g] (its
   // phase-2 P^T fragment positions); used for dF/dC and to rebuild sAc = -A diag(c_k) each slice.
+  // Read from the staged tile; the first rebuild overwrites exactly these positions (same thread).
   double Areg[NT][2];
 #pragma unroll
   for (int t = 0; t < NT; ++t)
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int64_t gi = i0 + 8 * warp + 2 * q + e;
-      const int r = 8 * t + g;
-      Areg[t][e] = (gi < p.I && r < p.R) ? p.A[gi + p.I * r] : 0.0;
-    }
+    for (int e = 0; e < 2; ++e) Areg[t][e] = sAc[(8 * warp + 2 * q + e) * LDF + 8 * t + g];
   auto rebuild_sAc = [&](const double* c) {
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
@@ -198,6 +242,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
 
   const int wi = warp & 1, wj = warp >> 1;   // phase-1 warp tile: rows (BT/2)*wi.., cols 16*wj..
 
+  TLC(1);
   for (int kk = 0; kk < nk; ++kk) {
     const int b = kk & 1;
     const int64_t k = kA + kk;
@@ -337,6 +382,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
     }
   }
   __syncthreads();
+  TLC(2);
   if (nk > 0 && tid < RP) {
     const double* gsrc = sGC + ((nk - 1) & 1) * NW * RP;
     double v = 0.0;
@@ -368,6 +414,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
     for (int w = 0; w < NW; ++w) v += sRed[w];
     p.fp[bid] = v;
   }
+  TLC(3);
 }
 
 // Fixed-order reduction of all partials into the packed gradient and f (row a6). Threads run along r
@@ -492,6 +539,28 @@ size_t eval_smem_bytes(int NT, int BT) {
 }  // namespace tfk
 
 #ifdef TF_EVAL_PROFILE
+extern "C" void tf_eval_cta_dump(int ncta) {
+  static unsigned long long h[4096 * 4];
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(h, tfk::g_eval_cta, sizeof(h));
+  unsigned long long t0 = ~0ull, t1 = 0;
+  double pro = 0, loop = 0, epi = 0;
+  int n = ncta < 4096 ? ncta : 4096;
+  for (int b = 0; b < n; ++b) {
+    t0 = h[b * 4] < t0 ? h[b * 4] : t0;
+    t1 = h[b * 4 + 3] > t1 ? h[b * 4 + 3] : t1;
+    pro += (h[b * 4 + 1] - h[b * 4]) * 1e-3;
+    loop += (h[b * 4 + 2] - h[b * 4 + 1]) * 1e-3;
+    epi += (h[b * 4 + 3] - h[b * 4 + 2]) * 1e-3;
+  }
+  printf("CTAs %d: span %.1f us; per CTA avg prologue %.2f us, loop %.2f us, epilogue %.2f us\n", n, (t1 - t0) * 1e-3,
+         pro / n, loop / n, epi / n);
+  // per-SM style view: sum of CTA lifetimes vs span x concurrency
+  double life = 0;
+  for (int b = 0; b < n; ++b) life += (h[b * 4 + 3] - h[b * 4]) * 1e-3;
+  printf("sum of CTA lifetimes %.1f us = %.3f x (span x 148)\n", life, life / ((t1 - t0) * 1e-3 * 148));
+}
+
 extern "C" void tf_eval_timeline_dump(void) {
   unsigned long long h[16 * 16 * 8];
   cudaDeviceSynchronize();

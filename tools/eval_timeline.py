@@ -15,3 +15,5 @@ for _ in range(2):
     ctx.tf_cpd_eval(d, P.T, w)
 torch.cuda.synchronize()
 ctypes.CDLL(tf.LIB_PATH).tf_eval_timeline_dump()
+lib = ctypes.CDLL(tf.LIB_PATH)
+lib.tf_eval_cta_dump(4096)
