@@ -14,6 +14,9 @@ Contents
     different statements of the paper (Lemma partialf, entrywise; Lemma
     kronecker, Kronecker-product columns), plus explicit unfoldings and
     Khatri-Rao products (Alg. Unfolding; Kolda's unfolding formula).
+  * `mlsvd.py`: the MLSVD compression stage (NEXT #3): unfolding Grams, the
+    truncated MLSVD through them, Alg. Compression, the MLSVD-energy
+    initialisation and uncompression (numpy fp64, eigh as the SVD primitive).
 
 Pins (tests/test_oracle_pins.py, `-m "not gpu"`) tie every function to the
 paper or to mathematics; the list, and any function left "parity unpinned",
