@@ -173,6 +173,56 @@ typedef struct {
 tf_status tf_cpd_dgn(tf_ctx *ctx, tf_dims d, const double *T, double *w, const tf_dgn_params *prm,
                      tf_dgn_result *res, double *hist);
 
+/* ---------------------------------------------------------------------------------------------------
+ * NEXT #3 -- compression before the path (Tensor Fox section "Compression"): the
+ * truncated MLSVD of T (Alg. MLSVD; Thm MLSVD 1296-1301) with each mode's SVD taken
+ * through the unfolding Gram T_(l) T_(l)^T (Remark MLSVD-SVD 4446-4448, Lemma svd-transpose 4434-4436)
+ * and truncated to P_l = min(I_l, R) singular values, the rank choice of Alg. Compression
+ * (2566-2583), the MLSVD-energy initialisation (2600-2605) and the uncompression W~ = U W (2857-2868).
+ * All pointers are device memory unless stated; matrices are column-major with the leading dimension
+ * equal to their row count; these calls need the whole tensor (K == K_total, k_begin == 0).
+ * Readings: R23 singular-vector signs -- the largest-magnitude entry of every column of U_l
+ * is positive; R25 energy initialisation -- the R entries of largest |s| (ties: storage order), the
+ * coefficient on mode 1. */
+
+/* G_l = T_(l) T_(l)^T for l = 1, 2, 3 (I x I, J x J, K x K, symmetric, full storage); any output may be
+ * NULL to skip that mode. Entry (p, q) is the inner product of the mode-l hyperslices i_l = p and q
+ * (PAPER.md:1293). */
+tf_status tf_unfolding_grams(tf_ctx *ctx, tf_dims d, const double *T, double *G1, double *G2, double *G3);
+
+/* Top-P eigenpairs of a symmetric positive semidefinite n x n matrix G (the unfolding Gram) by subspace
+ * iteration from the n x P start block Omega (seeded N(0,1), drawn by the caller: the randomized range
+ * finder of PAPER.md:1424 / rand_svd) with Householder orthonormalisation and a Rayleigh-Ritz step
+ * (Jacobi) per iteration, until every Ritz residual ||G u_j - lam_j u_j|| <= max(tol, 16 sqrt(n) 2^-53)
+ * |lam_1| (or it stagnates at the fp64 floor, or maxiter). Outputs: U (n x P, orthonormal, R23 signs),
+ * lam (P, sorted by |lam| decreasing); iters (host, nullable) = iterations done. 1 <= P <= min(n, 128). */
+tf_status tf_sym_eig_top(tf_ctx *ctx, int64_t n, const double *G, int64_t P, const double *Omega, int maxiter,
+                         double tol, double *U, double *lam, int *iters);
+
+/* S = (U1^T, U2^T, U3^T) . T, the multilinear product of the MLSVD core, computed as
+ * three DMMA GEMMs over chunks of frontal slices (mode 1, then mode 2 per slice, then mode 3). U1 (I x P1),
+ * U2 (J x P2), U3 (K x P3); S (P1 x P2 x P3, first index fastest). P_l <= 128. */
+tf_status tf_multilinear_core(tf_ctx *ctx, tf_dims d, const double *T, const double *U1, int64_t P1,
+                              const double *U2, int64_t P2, const double *U3, int64_t P3, double *S);
+
+/* Alg. Compression with d.R as the target CPD rank. Omega: start blocks [I x P1 | J x P2 | K x P3]
+ * (P_l = min(I_l, R)). Outputs: U = [U1 | U2 | U3] in the same layout (all P_l columns; the first R~_l
+ * are U~_l), sigma = [sigma^(1) | sigma^(2) | sigma^(3)] (P_l each, decreasing), S = the truncated core
+ * S~ (R~1 x R~2 x R~3, first index fastest; capacity P1*P2*P3), ranks (host, 3) = (R~1, R~2, R~3):
+ * for each mode the first i with sum_{r>i} sigma_r^2 / sum_{r<=P_l} sigma_r^2 < mlsvd_tol / 3.
+ * eig_iters (host, nullable, 3). Synchronizes the stream (the ranks size the core). */
+tf_status tf_compress(tf_ctx *ctx, tf_dims d, const double *T, const double *Omega, double mlsvd_tol,
+                      int eig_maxiter, double eig_tol, double *U, double *sigma, double *S, int64_t *ranks,
+                      int *eig_iters);
+
+/* MLSVD-energy initialisation on the core S (R1 x R2 x R3): w = [vec W1; vec W2; vec W3] (R*(R1+R2+R3))
+ * with W1[:, r] = s_j e_{j1}, W2[:, r] = e_{j2}, W3[:, r] = e_{j3} for the R entries j of largest |s|. */
+tf_status tf_energy_init(tf_ctx *ctx, int64_t R1, int64_t R2, int64_t R3, const double *S, int64_t R, double *w);
+
+/* Uncompression of one mode: out (n x R) = U (n x Rl) . W (Rl x R). */
+tf_status tf_uncompress(tf_ctx *ctx, int64_t n, int64_t Rl, const double *U, const double *W, int64_t R,
+                        double *out);
+
 /* Instrumentation (bench.py): when enabled, the fused evaluation kernel is
  * bracketed by CUDA events on the ctx stream; tf_ctx_kernel_stats synchronizes
  * and returns the summed device time (ms) and count of the fused-kernel launches

@@ -67,13 +67,23 @@ class TfDgnResult(ctypes.Structure):
 _lib.tf_cpd_dgn.argtypes = [_vp, TfDims, _vp, _vp, ctypes.POINTER(TfDgnParams), ctypes.POINTER(TfDgnResult),
                             ctypes.POINTER(ctypes.c_double)]
 _lib.tf_ctx_set_timing.argtypes = [_vp, ctypes.c_int]
+_i64 = ctypes.c_int64
+_lib.tf_unfolding_grams.argtypes = [_vp, TfDims, _vp, _vp, _vp, _vp]
+_lib.tf_sym_eig_top.argtypes = [_vp, _i64, _vp, _i64, _vp, ctypes.c_int, ctypes.c_double, _vp, _vp,
+                                ctypes.POINTER(ctypes.c_int)]
+_lib.tf_multilinear_core.argtypes = [_vp, TfDims, _vp, _vp, _i64, _vp, _i64, _vp, _i64, _vp]
+_lib.tf_compress.argtypes = [_vp, TfDims, _vp, _vp, ctypes.c_double, ctypes.c_int, ctypes.c_double, _vp, _vp, _vp,
+                             ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_int)]
+_lib.tf_energy_init.argtypes = [_vp, _i64, _i64, _i64, _vp, _i64, _vp]
+_lib.tf_uncompress.argtypes = [_vp, _i64, _i64, _vp, _vp, _i64, _vp]
 _lib.tf_ctx_kernel_stats.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64),
                                      ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
 
 EXPORTED = ["tf_ctx_create", "tf_ctx_destroy", "tf_ctx_set_stream", "tf_status_str", "tf_last_error", "tf_version",
             "tf_grams", "tf_hadamard", "tf_cpd_eval", "tf_cpd_eval_host", "tf_gn_matvec", "tf_cg_solve",
             "tf_reg_gamma", "tf_gn_matvec_damped", "tf_cg_solve_damped", "tf_cpd_dgn", "tf_ctx_set_timing",
-            "tf_ctx_kernel_stats"]
+            "tf_ctx_kernel_stats", "tf_unfolding_grams", "tf_sym_eig_top", "tf_multilinear_core", "tf_compress",
+            "tf_energy_init", "tf_uncompress"]
 
 TF_OK, TF_ERR_ARG, TF_ERR_ALIGN, TF_ERR_UNSUPPORTED, TF_ERR_CUDA, TF_ERR_NONFINITE, TF_ERR_ALLOC = range(7)
 MAX_R = 128
@@ -272,6 +282,80 @@ class Context:
                                             int(maxiter), float(tol), int(bool(jacobi)), _ptr(x), ctypes.byref(it),
                                             ctypes.byref(r2)))
         return x, it.value, r2.value
+
+    # ------------------------------------------------------------------ compression stage (NEXT #3)
+    def tf_unfolding_grams(self, d: Dims, T: torch.Tensor, modes=(1, 2, 3)):
+        """[G1, G2, G3] = T_(l) T_(l)^T (None for modes not requested); each (I_l, I_l), column-major
+        storage, symmetric."""
+        ldT = d.ldT or d.I
+        _dev(T, "T", ldT * d.J * d.K - (ldT - d.I))
+        dims = (d.I, d.J, d.K)
+        out = [torch.empty(dims[l] * dims[l], dtype=torch.float64, device=T.device) if (l + 1) in modes else None
+               for l in range(3)]
+        self._check(_lib.tf_unfolding_grams(self._h, d.c(), _ptr(T), _ptr(out[0]), _ptr(out[1]), _ptr(out[2])))
+        return out
+
+    def tf_sym_eig_top(self, n: int, G: torch.Tensor, P: int, Omega: torch.Tensor, maxiter: int = 100,
+                       tol: float = 0.0):
+        """(U (n*P, column-major), lam (P,), iterations) — top-P eigenpairs of the symmetric PSD G."""
+        _dev(G, "G", n * n)
+        _dev(Omega, "Omega", n * P)
+        U = torch.empty(n * P, dtype=torch.float64, device=G.device)
+        lam = torch.empty(P, dtype=torch.float64, device=G.device)
+        it = ctypes.c_int()
+        self._check(_lib.tf_sym_eig_top(self._h, n, _ptr(G), P, _ptr(Omega), int(maxiter), float(tol), _ptr(U),
+                                        _ptr(lam), ctypes.byref(it)))
+        return U, lam, it.value
+
+    def tf_multilinear_core(self, d: Dims, T: torch.Tensor, U1, P1: int, U2, P2: int, U3, P3: int):
+        """S = (U1^T, U2^T, U3^T)·T as a flat (P1*P2*P3,) first-index-fastest tensor."""
+        ldT = d.ldT or d.I
+        _dev(T, "T", ldT * d.J * d.K - (ldT - d.I))
+        for name, U, n, P in (("U1", U1, d.I, P1), ("U2", U2, d.J, P2), ("U3", U3, d.K, P3)):
+            _dev(U, name, n * P)
+        S = torch.empty(P1 * P2 * P3, dtype=torch.float64, device=T.device)
+        self._check(_lib.tf_multilinear_core(self._h, d.c(), _ptr(T), _ptr(U1), P1, _ptr(U2), P2, _ptr(U3), P3,
+                                             _ptr(S)))
+        return S
+
+    def tf_compress(self, d: Dims, T: torch.Tensor, Omega: torch.Tensor, mlsvd_tol: float = 1e-6,
+                    eig_maxiter: int = 100, eig_tol: float = 0.0):
+        """Alg. Compression. Returns dict(U=[U1, U2, U3] (I_l x P_l, column-major flat), sigma=[...],
+        S=core (R~1*R~2*R~3,), ranks=(R~1, R~2, R~3), P=(P1, P2, P3), eig_iters=[...])."""
+        ldT = d.ldT or d.I
+        _dev(T, "T", ldT * d.J * d.K - (ldT - d.I))
+        dims = (d.I, d.J, d.K)
+        P = tuple(min(n, d.R) for n in dims)
+        nU = sum(n * p for n, p in zip(dims, P))
+        _dev(Omega, "Omega", nU)
+        U = torch.empty(nU, dtype=torch.float64, device=T.device)
+        sigma = torch.empty(sum(P), dtype=torch.float64, device=T.device)
+        S = torch.empty(P[0] * P[1] * P[2], dtype=torch.float64, device=T.device)
+        ranks = (ctypes.c_int64 * 3)()
+        iters = (ctypes.c_int * 3)()
+        self._check(_lib.tf_compress(self._h, d.c(), _ptr(T), _ptr(Omega), float(mlsvd_tol), int(eig_maxiter),
+                                     float(eig_tol), _ptr(U), _ptr(sigma), _ptr(S), ranks, iters))
+        rk = tuple(int(r) for r in ranks)
+        offs = [0, dims[0] * P[0], dims[0] * P[0] + dims[1] * P[1]]
+        soffs = [0, P[0], P[0] + P[1]]
+        return {"U": [U[offs[l]:offs[l] + dims[l] * P[l]] for l in range(3)],
+                "sigma": [sigma[soffs[l]:soffs[l] + P[l]] for l in range(3)],
+                "S": S[:rk[0] * rk[1] * rk[2]], "ranks": rk, "P": P, "eig_iters": [int(i) for i in iters]}
+
+    def tf_energy_init(self, R1: int, R2: int, R3: int, S: torch.Tensor, R: int) -> torch.Tensor:
+        """Packed w = [vec W1; vec W2; vec W3] of the MLSVD-energy initialisation on the core S."""
+        _dev(S, "S", R1 * R2 * R3)
+        w = torch.empty(R * (R1 + R2 + R3), dtype=torch.float64, device=S.device)
+        self._check(_lib.tf_energy_init(self._h, R1, R2, R3, _ptr(S), R, _ptr(w)))
+        return w
+
+    def tf_uncompress(self, n: int, Rl: int, U: torch.Tensor, W: torch.Tensor, R: int) -> torch.Tensor:
+        """out (n x R, column-major flat) = U (n x Rl) W (Rl x R)."""
+        _dev(U, "U", n * Rl)
+        _dev(W, "W", Rl * R)
+        out = torch.empty(n * R, dtype=torch.float64, device=U.device)
+        self._check(_lib.tf_uncompress(self._h, n, Rl, _ptr(U), _ptr(W), R, _ptr(out)))
+        return out
 
     def tf_cpd_dgn(self, d: Dims, T: torch.Tensor, w: torch.Tensor, cg_iters, maxiter: int | None = None,
                    tol: float = 1e-6, mu0: float = 0.0, use_gamma: bool = True, jacobi: bool = True,

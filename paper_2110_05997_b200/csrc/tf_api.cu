@@ -8,43 +8,11 @@
 #include <string>
 #include <vector>
 
-#include "../../include/tf.h"
-#include "tf_internal.h"
+#include "tf_ctx.h"
 
 using namespace tfk;
 
-struct DevBuf {
-  void* p = nullptr;
-  size_t cap = 0;
-};
-
-struct tf_ctx {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  int nsm = 148;
-  std::string err;
-  DevBuf gAp, gBp, gCp, fp;                 // eval partials
-  DevBuf gram_part;                         // Gram split-K partials
-  DevBuf mvG, mvS, mvPi, mvD, mvPart;       // matvec / CG scratch
-  DevBuf cgR, cgP, cgZ, cgState;            // CG vectors and state
-  DevBuf hostW, hostGrad, hostGradTmp, hostF, hostStage[2];  // host-streamed eval
-  DevBuf dgnGrad, dgnX, dgnY, dgnGrams, dgnGamma, dgnScal, dgnPart;  // dGN outer loop
-  double* scal_host = nullptr;              // pinned, dGN scalars
-  cudaStream_t copy_stream = nullptr;
-  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
-  CgState* cg_host = nullptr;               // pinned
-  bool timing = false;
-  std::vector<cudaEvent_t> ev_pool;
-  size_t ev_used_pairs = 0;
-  int64_t eval_launches = 0;
-  int64_t total_launches = 0;
-};
-
-namespace {
-
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+namespace tfh {
 
 EncodeTiledFn get_encode_fn() {
   static EncodeTiledFn fn = nullptr;
@@ -68,12 +36,6 @@ tf_status set_err(tf_ctx* c, tf_status s, const std::string& msg) {
 tf_status cuda_err(tf_ctx* c, cudaError_t e, const char* where) {
   return set_err(c, TF_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
-
-#define TF_CUDA(c, expr)                                      \
-  do {                                                        \
-    cudaError_t e_ = (expr);                                  \
-    if (e_ != cudaSuccess) return cuda_err((c), e_, #expr);   \
-  } while (0)
 
 tf_status ensure(tf_ctx* c, DevBuf& b, size_t bytes) {
   if (bytes == 0) bytes = 8;
@@ -99,6 +61,12 @@ void free_buf(DevBuf& b) {
   b.p = nullptr;
   b.cap = 0;
 }
+
+}  // namespace tfh
+
+using namespace tfh;
+
+namespace {
 
 tf_status check_dims(tf_ctx* c, tf_dims& d) {
   if (!c) return TF_ERR_ARG;
@@ -294,7 +262,9 @@ tf_status tf_ctx_destroy(tf_ctx* c) {
   DevBuf* bufs[] = {&c->gAp, &c->gBp, &c->gCp, &c->fp, &c->gram_part, &c->mvG, &c->mvS, &c->mvPi, &c->mvD,
                     &c->mvPart, &c->cgR, &c->cgP, &c->cgZ, &c->cgState, &c->hostW, &c->hostGrad,
                     &c->hostGradTmp, &c->hostF, &c->hostStage[0], &c->hostStage[1], &c->dgnGrad, &c->dgnX,
-                    &c->dgnY, &c->dgnGrams, &c->dgnGamma, &c->dgnScal, &c->dgnPart};
+                    &c->dgnY, &c->dgnGrams, &c->dgnGamma, &c->dgnScal, &c->dgnPart, &c->gemmPart,
+                    &c->eigQ, &c->eigZ, &c->eigH, &c->eigV, &c->eigU, &c->eigRes, &c->eigScal, &c->mlG,
+                    &c->mlU, &c->mlLam, &c->mlX, &c->mlY, &c->mlRanks};
   for (DevBuf* b : bufs) free_buf(*b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (int i = 0; i < 2; ++i) {

@@ -1,0 +1,57 @@
+// Host-side context of the C ABI (include/tf.h) and the helpers every host translation unit uses.
+#pragma once
+#include <string>
+#include <vector>
+
+#include "../../include/tf.h"
+#include "tf_internal.h"
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+struct tf_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int nsm = 148;
+  std::string err;
+  DevBuf gAp, gBp, gCp, fp;                 // eval partials
+  DevBuf gram_part;                         // Gram split-K partials
+  DevBuf mvG, mvS, mvPi, mvD, mvPart;       // matvec / CG scratch
+  DevBuf cgR, cgP, cgZ, cgState;            // CG vectors and state
+  DevBuf hostW, hostGrad, hostGradTmp, hostF, hostStage[2];  // host-streamed eval
+  DevBuf dgnGrad, dgnX, dgnY, dgnGrams, dgnGamma, dgnScal, dgnPart;  // dGN outer loop
+  DevBuf gemmPart;                          // compression: GEMM split-K partials
+  DevBuf eigQ, eigZ, eigH, eigV, eigU, eigRes, eigScal;  // compression: subspace iteration
+  DevBuf mlG, mlU, mlLam, mlX, mlY, mlRanks;              // compression: Grams, U, core intermediates
+  double* scal_host = nullptr;              // pinned, dGN scalars
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
+  tfk::CgState* cg_host = nullptr;          // pinned
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used_pairs = 0;
+  int64_t eval_launches = 0;
+  int64_t total_launches = 0;
+};
+
+namespace tfh {
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn();
+tf_status set_err(tf_ctx* c, tf_status s, const std::string& msg);
+tf_status cuda_err(tf_ctx* c, cudaError_t e, const char* where);
+tf_status ensure(tf_ctx* c, DevBuf& b, size_t bytes);
+void free_buf(DevBuf& b);
+
+}  // namespace tfh
+
+#define TF_CUDA(c, expr)                                          \
+  do {                                                            \
+    cudaError_t e_ = (expr);                                      \
+    if (e_ != cudaSuccess) return tfh::cuda_err((c), e_, #expr);  \
+  } while (0)

@@ -85,4 +85,51 @@ int red_blocks();
 // y += x (n doubles), used by the host-streamed evaluation
 cudaError_t launch_axpy1(int64_t n, const double* x, double* y, cudaStream_t st);
 
+// ---- compression stage (NEXT #3): generic DMMA GEMM (k_gemm.cu) and eigen/QR kernels (k_eig.cu)
+struct GemmOperand {
+  const double* ptr;
+  int64_t ld;       // X[p, k] = ptr[k + ld*p] (kc) or ptr[p + ld*k] (!kc)
+  int64_t bstride;  // batch stride (0: the same operand for every batch)
+  bool kc;
+};
+// C[m, n] = alpha * sum_b sum_k A_b[m, k] B_b[n, k] + beta * C
+struct GemmArgs {
+  GemmOperand a, b;
+  int64_t M, N, Kd, batch;
+  bool sum_batch;      // batches summed into one C, else one C per batch (cstride apart)
+  bool sym;            // A == B: only tiles tn >= tm, mirrored
+  int64_t out_batches; // sum_batch ? 1 : batch
+  double* C;
+  int64_t ldc, cstride;
+  double alpha, beta;
+  int BM, BN;
+  int64_t ntm, ntn;
+  int ksplit;
+  int64_t steps_per_split;
+  double* part;        // [items][ksplit][BM*BN] when ksplit > 1
+};
+cudaError_t launch_gemm(const CUtensorMap* ma, const CUtensorMap* mb, const GemmArgs& g, int64_t items, bool tma,
+                        cudaStream_t st);
+size_t gemm_smem_bytes(int BM, int BN, bool akc, bool bkc);
+constexpr int kGemmBK = 32;
+
+// Householder QR of Z (n x P, ld) -> Q with orthonormal columns spanning Z (Z is overwritten)
+cudaError_t launch_house_qr(int64_t n, int P, double* Z, int64_t ldz, double* Q, int64_t ldq, cudaStream_t st);
+// symmetric eigen-decomposition of (H + H^T)/2 (P x P) by parallel cyclic Jacobi in one CTA:
+// theta sorted by |theta| decreasing, V (P x P, ld P) the matching eigenvectors; Vtmp: P*P scratch
+cudaError_t launch_jacobi_eig(int P, const double* H, int64_t ldh, double* Vtmp, double* V, double* theta,
+                              cudaStream_t st);
+// res[j] = || ZV[:, j] - theta_j U[:, j] ||_2
+cudaError_t launch_eig_residual(int64_t n, int P, const double* ZV, const double* U, int64_t ld, const double* theta,
+                                double* res, cudaStream_t st);
+// reading R23: make the largest-magnitude entry of every column positive (first on ties)
+cudaError_t launch_sign_fix(int64_t n, int P, double* U, int64_t ld, cudaStream_t st);
+// sigma = sqrt(|lam|)
+cudaError_t launch_sqrt_abs(int64_t n, const double* lam, double* sigma, cudaStream_t st);
+// Alg. Compression rank choice for one mode: first i with sum_{r>i} s_r^2 / sum s_r^2 < tol3 (s = sigma)
+cudaError_t launch_trunc_rank(int P, const double* sigma, double tol3, int64_t* rank, cudaStream_t st);
+// MLSVD-energy initialisation: the R entries of largest |s| of S (P1 x P2 x P3) -> packed w (core dims)
+cudaError_t launch_energy_init(int64_t P1, int64_t P2, int64_t P3, const double* S, int64_t R, double* w,
+                               cudaStream_t st);
+
 }  // namespace tfk

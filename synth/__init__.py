@@ -243,3 +243,16 @@ def cg_budget(maxiter: int, seed: int = 0):
     lo = 1 + np.ceil(ks ** 0.4).astype(np.int64)
     hi = 2 + np.ceil(ks ** 0.9).astype(np.int64)
     return rng.integers(lo, hi + 1).astype(np.int32)
+
+
+def omega_blocks(dims, R: int, device="cpu", seed: int = 0, tag: str = "omega") -> torch.Tensor:
+    """Start blocks of the randomized truncated SVD (rand_svd): for each mode l an
+    I_l × P_l block of i.i.d. N(0,1) entries (column-major), P_l = min(I_l, R), concatenated
+    [Ω1 | Ω2 | Ω3]. These are the random numbers the compression stage draws; they are drawn here
+    (seeded) and passed to the CUDA path as an input."""
+    dev = torch.device(device)
+    parts = []
+    for l, n in enumerate(dims):
+        P = min(n, R)
+        parts.append(randn((P, n), dev, seed, tag, l).reshape(-1))   # (P, n) row-major = n x P column-major
+    return torch.cat(parts)
