@@ -29,13 +29,34 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile every translation unit to a relocatable object in parallel, then link the shared library."""
     if not force and not needs_build():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", tmp, *[os.path.join(CSRC, s) for s in SOURCES]]
+    from concurrent.futures import ThreadPoolExecutor
+
+    tag = f".tmp{os.getpid()}"
+    objdir = os.path.join(HERE, "build_obj")
+    os.makedirs(objdir, exist_ok=True)
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"] + ["-c"]
+    jobs = []
+    for src in SOURCES:
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        jobs.append(([_nvcc(), *compile_flags, "-o", obj, os.path.join(CSRC, src)], obj))
     if verbose:
-        print(" ".join(cmd))
-    subprocess.check_call(cmd)
+        for cmd, _ in jobs:
+            print(" ".join(cmd))
+
+    def run(job):
+        subprocess.check_call(job[0])
+        return job[1]
+
+    with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(run, jobs))
+    tmp = LIB + tag
+    link = [_nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs]
+    if verbose:
+        print(" ".join(link))
+    subprocess.check_call(link)
     os.replace(tmp, LIB)
     return LIB
 

@@ -118,12 +118,14 @@ __global__ void __launch_bounds__(kQrThreads) k_house_qr(int64_t n, int P, doubl
 // |theta| decreasing (the ordering of Lemma svd-transpose) with ties kept in index order.
 __global__ void __launch_bounds__(1024) k_jacobi_eig(int P, const double* __restrict__ H, int64_t ldh,
                                                      double* __restrict__ Vt, double* __restrict__ V,
-                                                     double* __restrict__ theta) {
+                                                     double* __restrict__ theta, int vsm) {
   extern __shared__ double hs[];
   const int Pp = P + (P & 1);
   const int half = Pp / 2;
   double* cs = hs + (size_t)Pp * Pp;        // [half][2]
   int* pr = reinterpret_cast<int*>(cs + 2 * half);   // [half][2]
+  // the rotation accumulator lives in shared memory when it fits (P <= 112), else in global memory
+  double* Vw = vsm ? reinterpret_cast<double*>(pr + 2 * half + 2) : Vt;
   __shared__ int rotated;
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int e = tid; e < Pp * Pp; e += nt) {
@@ -132,7 +134,7 @@ __global__ void __launch_bounds__(1024) k_jacobi_eig(int P, const double* __rest
     if (r < P && c < P) v = 0.5 * (H[r + (int64_t)c * ldh] + H[c + (int64_t)r * ldh]);
     hs[r + Pp * c] = v;
   }
-  for (int e = tid; e < P * P; e += nt) Vt[e] = (e % P == e / P) ? 1.0 : 0.0;
+  for (int e = tid; e < P * P; e += nt) Vw[e] = (e % P == e / P) ? 1.0 : 0.0;
   __syncthreads();
   for (int sweep = 0; sweep < 60; ++sweep) {
     if (tid == 0) rotated = 0;
@@ -187,9 +189,9 @@ __global__ void __launch_bounds__(1024) k_jacobi_eig(int P, const double* __rest
         hs[row + Pp * p] = c * hp - s * hq;
         hs[row + Pp * q] = s * hp + c * hq;
         if (row < P) {
-          const double vp = Vt[row + (int64_t)P * p], vq = Vt[row + (int64_t)P * q];
-          Vt[row + (int64_t)P * p] = c * vp - s * vq;
-          Vt[row + (int64_t)P * q] = s * vp + c * vq;
+          const double vp = Vw[row + (int64_t)P * p], vq = Vw[row + (int64_t)P * q];
+          Vw[row + (int64_t)P * p] = c * vp - s * vq;
+          Vw[row + (int64_t)P * q] = s * vp + c * vq;
         }
       }
       __syncthreads();
@@ -215,7 +217,7 @@ __global__ void __launch_bounds__(1024) k_jacobi_eig(int P, const double* __rest
       rank += (tj > ti) || (tj == ti && j < i);
     }
     theta[rank] = hs[i + Pp * i];
-    for (int r = 0; r < P; ++r) V[r + (int64_t)P * rank] = Vt[r + (int64_t)P * i];
+    for (int r = 0; r < P; ++r) V[r + (int64_t)P * rank] = Vw[r + (int64_t)P * i];
   }
 }
 
@@ -368,6 +370,85 @@ __global__ void __launch_bounds__(1024) k_energy_init(int64_t P1, int64_t P2, in
   }
 }
 
+// Column normalisation W[:, j] = Z[:, j] / ||Z[:, j]|| (one block per column); flags a zero column.
+__global__ void k_col_normalize(int64_t n, const double* __restrict__ Z, int64_t ldz, double* __restrict__ W,
+                                int64_t ldw, int* __restrict__ fail) {
+  __shared__ double red[33];
+  const int j = blockIdx.x;
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const double z = Z[i + ldz * j];
+    s += z * z;
+  }
+  s = block_sum(s, red);
+  if (!(s > 0.0) || !isfinite(s)) {
+    if (threadIdx.x == 0) atomicExch(fail, 1);
+    return;
+  }
+  const double inv = 1.0 / sqrt(s);
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) W[i + ldw * j] = Z[i + ldz * j] * inv;
+}
+
+// Cholesky B = L L^T of the symmetric part of B (P x P, one CTA, right-looking, B in shared memory) and
+// Linv = L^{-1} by forward substitution (one column per thread). A pivot below 1e-8 (B comes from
+// column-normalised vectors, so its diagonal is ~1) flags the block as numerically dependent.
+__global__ void __launch_bounds__(1024) k_chol_inv(int P, const double* __restrict__ B, double* __restrict__ Linv,
+                                                   int* __restrict__ fail) {
+  extern __shared__ double bs[];   // P x P, column-major; the lower triangle becomes L
+  __shared__ int bad;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < P * P; e += nt) {
+    const int r = e % P, c = e / P;
+    bs[e] = 0.5 * (B[r + (int64_t)P * c] + B[c + (int64_t)P * r]);
+  }
+  if (tid == 0) bad = 0;
+  __syncthreads();
+  for (int j = 0; j < P; ++j) {
+    if (tid == 0) {
+      const double d = bs[j + P * j];
+      if (!(d > 1e-8)) bad = 1;
+      bs[j + P * j] = d > 0.0 ? sqrt(d) : 1.0;
+    }
+    __syncthreads();
+    const double ljj = bs[j + P * j];
+    for (int i = j + 1 + tid; i < P; i += nt) bs[i + P * j] /= ljj;
+    __syncthreads();
+    const int m = P - j - 1;
+    for (int e = tid; e < m * m; e += nt) {
+      const int i = j + 1 + e % m, k = j + 1 + e / m;
+      if (i >= k) bs[i + P * k] -= bs[i + P * j] * bs[k + P * j];
+    }
+    __syncthreads();
+  }
+  if (bad) {
+    if (tid == 0) atomicExch(fail, 1);
+    return;
+  }
+  for (int c = tid; c < P; c += nt) {
+    for (int i = 0; i < c; ++i) Linv[i + (int64_t)P * c] = 0.0;
+    Linv[c + (int64_t)P * c] = 1.0 / bs[c + P * c];
+    for (int i = c + 1; i < P; ++i) {
+      double acc = 0.0;
+      for (int k = c; k < i; ++k) acc += bs[i + P * k] * Linv[k + (int64_t)P * c];
+      Linv[i + (int64_t)P * c] = -acc / bs[i + P * i];
+    }
+  }
+}
+
+cudaError_t launch_col_normalize(int64_t n, int P, const double* Z, int64_t ldz, double* W, int64_t ldw, int* fail,
+                                 cudaStream_t st) {
+  k_col_normalize<<<P, 256, 0, st>>>(n, Z, ldz, W, ldw, fail);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_chol_inv(int P, const double* B, double* Linv, int* fail, cudaStream_t st) {
+  const size_t smem = (size_t)P * P * 8;
+  cudaError_t e = cudaFuncSetAttribute(k_chol_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_chol_inv<<<1, 1024, smem, st>>>(P, B, Linv, fail);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_house_qr(int64_t n, int P, double* Z, int64_t ldz, double* Q, int64_t ldq, cudaStream_t st) {
   k_house_qr<<<1, kQrThreads, 0, st>>>(n, P, Z, ldz, Q, ldq);
   return cudaGetLastError();
@@ -376,10 +457,12 @@ cudaError_t launch_house_qr(int64_t n, int P, double* Z, int64_t ldz, double* Q,
 cudaError_t launch_jacobi_eig(int P, const double* H, int64_t ldh, double* Vtmp, double* V, double* theta,
                               cudaStream_t st) {
   const int Pp = P + (P & 1);
-  const size_t smem = (size_t)Pp * Pp * 8 + (size_t)Pp * 8 + (size_t)Pp * 4 + 64;
+  size_t smem = (size_t)Pp * Pp * 8 + (size_t)Pp * 8 + (size_t)Pp * 4 + 16;
+  const int vsm = smem + (size_t)P * P * 8 <= 220 * 1024;
+  if (vsm) smem += (size_t)P * P * 8;
   cudaError_t e = cudaFuncSetAttribute(k_jacobi_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_jacobi_eig<<<1, 1024, smem, st>>>(P, H, ldh, Vtmp, V, theta);
+  k_jacobi_eig<<<1, 1024, smem, st>>>(P, H, ldh, Vtmp, V, theta, vsm);
   return cudaGetLastError();
 }
 

@@ -263,7 +263,7 @@ tf_status tf_ctx_destroy(tf_ctx* c) {
                     &c->mvPart, &c->cgR, &c->cgP, &c->cgZ, &c->cgState, &c->hostW, &c->hostGrad,
                     &c->hostGradTmp, &c->hostF, &c->hostStage[0], &c->hostStage[1], &c->dgnGrad, &c->dgnX,
                     &c->dgnY, &c->dgnGrams, &c->dgnGamma, &c->dgnScal, &c->dgnPart, &c->gemmPart,
-                    &c->eigQ, &c->eigZ, &c->eigH, &c->eigV, &c->eigU, &c->eigRes, &c->eigScal, &c->mlG,
+                    &c->eigQ, &c->eigZ, &c->eigH, &c->eigV, &c->eigU, &c->eigRes, &c->eigScal, &c->eigB, &c->mlG,
                     &c->mlU, &c->mlLam, &c->mlX, &c->mlY, &c->mlRanks};
   for (DevBuf* b : bufs) free_buf(*b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);

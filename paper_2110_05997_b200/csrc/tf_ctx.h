@@ -23,7 +23,7 @@ struct tf_ctx {
   DevBuf hostW, hostGrad, hostGradTmp, hostF, hostStage[2];  // host-streamed eval
   DevBuf dgnGrad, dgnX, dgnY, dgnGrams, dgnGamma, dgnScal, dgnPart;  // dGN outer loop
   DevBuf gemmPart;                          // compression: GEMM split-K partials
-  DevBuf eigQ, eigZ, eigH, eigV, eigU, eigRes, eigScal;  // compression: subspace iteration
+  DevBuf eigQ, eigZ, eigH, eigV, eigU, eigRes, eigScal, eigB;  // compression: subspace iteration
   DevBuf mlG, mlU, mlLam, mlX, mlY, mlRanks;              // compression: Grams, U, core intermediates
   double* scal_host = nullptr;              // pinned, dGN scalars
   cudaStream_t copy_stream = nullptr;

@@ -115,6 +115,11 @@ constexpr int kGemmBK = 32;
 
 // Householder QR of Z (n x P, ld) -> Q with orthonormal columns spanning Z (Z is overwritten)
 cudaError_t launch_house_qr(int64_t n, int P, double* Z, int64_t ldz, double* Q, int64_t ldq, cudaStream_t st);
+// W[:, j] = Z[:, j] / ||Z[:, j]||; *fail = 1 on a zero column
+cudaError_t launch_col_normalize(int64_t n, int P, const double* Z, int64_t ldz, double* W, int64_t ldw, int* fail,
+                                 cudaStream_t st);
+// B = L L^T (P x P) and Linv = L^{-1}; *fail = 1 when a pivot is below 1e-8
+cudaError_t launch_chol_inv(int P, const double* B, double* Linv, int* fail, cudaStream_t st);
 // symmetric eigen-decomposition of (H + H^T)/2 (P x P) by parallel cyclic Jacobi in one CTA:
 // theta sorted by |theta| decreasing, V (P x P, ld P) the matching eigenvectors; Vtmp: P*P scratch
 cudaError_t launch_jacobi_eig(int P, const double* H, int64_t ldh, double* Vtmp, double* V, double* theta,

@@ -176,6 +176,7 @@ tf_status eig_top_impl(tf_ctx* c, int64_t n, const double* G, int P, const doubl
   if ((s = ensure(c, c->eigH, (size_t)P * P * 8))) return s;
   if ((s = ensure(c, c->eigV, (size_t)2 * P * P * 8))) return s;
   if ((s = ensure(c, c->eigScal, (size_t)2 * P * 8 + 64))) return s;
+  if ((s = ensure(c, c->eigB, (size_t)2 * P * P * 8))) return s;
   double* Q = (double*)c->eigQ.p;
   double* Z = (double*)c->eigZ.p;
   double* Uw = (double*)c->eigU.p;
@@ -185,8 +186,36 @@ tf_status eig_top_impl(tf_ctx* c, int64_t n, const double* G, int P, const doubl
   double* Vt = V + (size_t)P * P;
   double* theta = (double*)c->eigScal.p;
   double* res = theta + P;
+  int* fail = reinterpret_cast<int*>(res + P);
+  double* Bm = (double*)c->eigB.p;
+  double* Linv = Bm + (size_t)P * P;
+  // Q = orth(X): column-scaled CholeskyQR2 (X's columns are nearly orthogonal after the Ritz rotation, so
+  // its Gram is ~I; a few GEMMs and one small Cholesky per pass), Householder QR when Cholesky reports a
+  // numerically dependent block (exact low rank). X is preserved by CholeskyQR2; W, tmp are scratch.
+  auto orth = [&](double* X, double* W, double* tmp) -> tf_status {
+    int hfail = 0;
+    tf_status st;
+    TF_CUDA(c, cudaMemsetAsync(fail, 0, sizeof(int), c->stream));
+    TF_CUDA(c, launch_col_normalize(n, P, X, ldw, W, ldw, fail, c->stream));
+    double* src = W;
+    for (int pass = 0; pass < 2; ++pass) {
+      if ((st = gemm_run(c, gemm_args(opnd(src, ldw, true), opnd(src, ldw, true), P, P, n, Bm, P)))) return st;
+      TF_CUDA(c, launch_chol_inv(P, Bm, Linv, fail, c->stream));
+      if ((st = gemm_run(c, gemm_args(opnd(src, ldw, false), opnd(Linv, P, false), n, P, P, pass ? Q : tmp, ldw))))
+        return st;
+      src = tmp;
+    }
+    c->total_launches += 4;
+    TF_CUDA(c, cudaMemcpyAsync(&hfail, fail, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    TF_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (hfail) {
+      TF_CUDA(c, launch_house_qr(n, P, X, ldw, Q, ldw, c->stream));
+      c->total_launches += 1;
+    }
+    return TF_OK;
+  };
   TF_CUDA(c, cudaMemcpy2DAsync(Z, ldw * 8, Omega, n * 8, n * 8, P, cudaMemcpyDeviceToDevice, c->stream));
-  TF_CUDA(c, launch_house_qr(n, P, Z, ldw, Q, ldw, c->stream));
+  if ((s = orth(Z, ZV, Uw))) return s;
   const double u = std::ldexp(1.0, -53);
   const double tol_eff = std::max(tol, 16.0 * std::sqrt((double)n) * u);
   double host[2 * TF_MAX_R + 2];
@@ -212,8 +241,8 @@ tf_status eig_top_impl(tf_ctx* c, int64_t n, const double* G, int P, const doubl
     const bool stall = it >= 3 && maxres > 0.5 * prev && maxres <= 1e3 * tol_eff * scale;
     if (conv || stall || it == maxiter) break;
     prev = maxres;
-    TF_CUDA(c, launch_house_qr(n, P, ZV, ldw, Q, ldw, c->stream));
-    c->total_launches += 1;
+    // orthonormalise the Ritz-rotated block ZV ~ U Theta for the next iteration
+    if ((s = orth(ZV, Z, Uw))) return s;
   }
   if (it > maxiter) it = maxiter;
   TF_CUDA(c, launch_sign_fix(n, P, Uw, ldw, c->stream));
