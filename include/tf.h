@@ -223,6 +223,32 @@ tf_status tf_energy_init(tf_ctx *ctx, int64_t R1, int64_t R2, int64_t R3, const 
 tf_status tf_uncompress(tf_ctx *ctx, int64_t n, int64_t Rl, const double *U, const double *W, int64_t R,
                         double *out);
 
+/* The whole Tensor Fox flow (flow chart "Compression -> Initialization -> dGN ->
+ * Uncompression"): tf_compress of T to the R~1 x R~2 x R~3 core; the starting point on the core from the
+ * MLSVD-energy initialisation (init = 1) or from w0_core (init = 0: rows 0..R~_l-1 of each block of
+ * [W1 (P1 x R) | W2 (P2 x R) | W3 (P3 x R)], e.g. N(0,1) entries drawn by the caller);
+ * tf_cpd_dgn on the core; uncompression W~_l = U~_l W_l; and the output form with unit columns and
+ * lambda_r = prod_l ||W~_l[:, r]||. W (device, R*(I+J+K), w layout) gets the unit
+ * factors, lambda (device, R) the weights. res->rel_err is ||T - sum_r lambda_r w_r^(1) (x) w_r^(2) (x)
+ * w_r^(3)|| / ||T|| on the ORIGINAL tensor, from one fused evaluation. hist (host, nullable): the dGN
+ * history on the core (5 doubles per iteration, as tf_cpd_dgn). Synchronizes the stream. */
+typedef struct {
+  double mlsvd_tol;       /* Alg. Compression tolerance */
+  int eig_maxiter;        /* subspace-iteration cap per mode */
+  int init;               /* 1: MLSVD-energy initialisation; 0: w0_core */
+  tf_dgn_params dgn;      /* the dGN loop on the core */
+} tf_cpd_params;
+
+typedef struct {
+  int64_t ranks[3];       /* R~1, R~2, R~3 */
+  int eig_iters[3];
+  tf_dgn_result dgn;      /* on the core */
+  double rel_err;         /* on the original tensor */
+} tf_cpd_result;
+
+tf_status tf_cpd(tf_ctx *ctx, tf_dims d, const double *T, const double *Omega, const double *w0_core,
+                 const tf_cpd_params *prm, double *W, double *lambda, tf_cpd_result *res, double *hist);
+
 /* Instrumentation (bench.py): when enabled, the fused evaluation kernel is
  * bracketed by CUDA events on the ctx stream; tf_ctx_kernel_stats synchronizes
  * and returns the summed device time (ms) and count of the fused-kernel launches

@@ -195,3 +195,16 @@ def energy_init(S: np.ndarray, R: int):
 def uncompress(Us, Ws):
     """W~_l = U_l W_l for each mode."""
     return [U @ W for U, W in zip(Us, Ws)]
+
+
+def normalize_cpd(Ws):
+    """Tensor Fox's output form (flow chart): factors with unit columns and the
+    diagonal Lambda, T ≈ sum_r lambda_r w_r^(1) ⊗ w_r^(2) ⊗ w_r^(3), lambda_r = prod_l ||W~_l[:, r]||.
+    A zero column keeps lambda_r = 0 and is left as it is."""
+    lam = np.ones(Ws[0].shape[1])
+    out = []
+    for W in Ws:
+        nrm = np.sqrt(np.sum(W * W, axis=0))
+        lam = lam * nrm
+        out.append(np.where(nrm > 0, W / np.where(nrm > 0, nrm, 1.0), W))
+    return out, lam

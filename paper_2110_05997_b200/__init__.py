@@ -76,6 +76,20 @@ _lib.tf_compress.argtypes = [_vp, TfDims, _vp, _vp, ctypes.c_double, ctypes.c_in
                              ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_int)]
 _lib.tf_energy_init.argtypes = [_vp, _i64, _i64, _i64, _vp, _i64, _vp]
 _lib.tf_uncompress.argtypes = [_vp, _i64, _i64, _vp, _vp, _i64, _vp]
+
+
+class TfCpdParams(ctypes.Structure):
+    _fields_ = [("mlsvd_tol", ctypes.c_double), ("eig_maxiter", ctypes.c_int), ("init", ctypes.c_int),
+                ("dgn", TfDgnParams)]
+
+
+class TfCpdResult(ctypes.Structure):
+    _fields_ = [("ranks", _i64 * 3), ("eig_iters", ctypes.c_int * 3), ("dgn", TfDgnResult),
+                ("rel_err", ctypes.c_double)]
+
+
+_lib.tf_cpd.argtypes = [_vp, TfDims, _vp, _vp, _vp, ctypes.POINTER(TfCpdParams), _vp, _vp, ctypes.POINTER(TfCpdResult),
+                        ctypes.POINTER(ctypes.c_double)]
 _lib.tf_ctx_kernel_stats.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64),
                                      ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
 
@@ -83,7 +97,7 @@ EXPORTED = ["tf_ctx_create", "tf_ctx_destroy", "tf_ctx_set_stream", "tf_status_s
             "tf_grams", "tf_hadamard", "tf_cpd_eval", "tf_cpd_eval_host", "tf_gn_matvec", "tf_cg_solve",
             "tf_reg_gamma", "tf_gn_matvec_damped", "tf_cg_solve_damped", "tf_cpd_dgn", "tf_ctx_set_timing",
             "tf_ctx_kernel_stats", "tf_unfolding_grams", "tf_sym_eig_top", "tf_multilinear_core", "tf_compress",
-            "tf_energy_init", "tf_uncompress"]
+            "tf_energy_init", "tf_uncompress", "tf_cpd"]
 
 TF_OK, TF_ERR_ARG, TF_ERR_ALIGN, TF_ERR_UNSUPPORTED, TF_ERR_CUDA, TF_ERR_NONFINITE, TF_ERR_ALLOC = range(7)
 MAX_R = 128
@@ -379,6 +393,38 @@ class Context:
                                     hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
         out = {"iters": res.iters, "reason": res.reason, "f": res.f, "rel_err": res.rel_err, "mu": res.mu}
         return out, hist.reshape(-1, 5)[:res.iters]
+
+    def tf_cpd(self, d: Dims, T: torch.Tensor, Omega: torch.Tensor, cg_iters, w0_core: torch.Tensor | None = None,
+               mlsvd_tol: float = 1e-6, eig_maxiter: int = 100, maxiter: int | None = None, tol: float = 1e-6,
+               mu0: float = 0.0, use_gamma: bool = True, jacobi: bool = True, balance: bool = True):
+        """The whole Tensor Fox flow: compression, initialisation (MLSVD energy when w0_core is None, else
+        the given [W1 | W2 | W3] random start on the P_l-row blocks), dGN on the core, uncompression and the
+        unit-column output. Returns (W (n,), lambda (R,), result dict, dGN history on the core)."""
+        import numpy as np
+        ldT = d.ldT or d.I
+        _dev(T, "T", ldT * d.J * d.K - (ldT - d.I))
+        dims = (d.I, d.J, d.K)
+        P = [min(x, d.R) for x in dims]
+        _dev(Omega, "Omega", sum(x * p for x, p in zip(dims, P)))
+        if w0_core is not None:
+            _dev(w0_core, "w0_core", d.R * sum(P))
+        cgi = np.ascontiguousarray(np.asarray(cg_iters, dtype=np.int32))
+        m = int(maxiter if maxiter is not None else cgi.size)
+        if cgi.size < m:
+            raise ValueError("cg_iters shorter than maxiter")
+        dp = TfDgnParams(m, float(tol), float(mu0), int(bool(use_gamma)), int(bool(jacobi)), int(bool(balance)),
+                         cgi.ctypes.data_as(ctypes.POINTER(ctypes.c_int)))
+        prm = TfCpdParams(float(mlsvd_tol), int(eig_maxiter), 0 if w0_core is not None else 1, dp)
+        res = TfCpdResult()
+        W = torch.empty(d.R * sum(dims), dtype=torch.float64, device=T.device)
+        lam = torch.empty(d.R, dtype=torch.float64, device=T.device)
+        hist = np.zeros(5 * max(m, 1))
+        self._check(_lib.tf_cpd(self._h, d.c(), _ptr(T), _ptr(Omega), _ptr(w0_core), ctypes.byref(prm), _ptr(W),
+                                _ptr(lam), ctypes.byref(res), hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+        out = {"ranks": tuple(int(x) for x in res.ranks), "eig_iters": [int(x) for x in res.eig_iters],
+               "dgn": {"iters": res.dgn.iters, "reason": res.dgn.reason, "f": res.dgn.f, "rel_err": res.dgn.rel_err,
+                       "mu": res.dgn.mu}, "rel_err": res.rel_err}
+        return W, lam, out, hist.reshape(-1, 5)[:res.dgn.iters]
 
     def set_timing(self, enable: bool):
         self._check(_lib.tf_ctx_set_timing(self._h, int(bool(enable))))

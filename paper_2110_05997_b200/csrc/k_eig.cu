@@ -449,6 +449,58 @@ cudaError_t launch_chol_inv(int P, const double* B, double* Linv, int* fail, cud
   return cudaGetLastError();
 }
 
+__global__ void k_truncate_rows(int64_t P1, int64_t P2, int64_t P3, int64_t R1, int64_t R2, int64_t R3, int64_t R,
+                                const double* __restrict__ w0, double* __restrict__ w) {
+  const int64_t n = R * (R1 + R2 + R3);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t src;
+    if (e < R * R1) {
+      src = (e % R1) + P1 * (e / R1);
+    } else if (e < R * (R1 + R2)) {
+      const int64_t x = e - R * R1;
+      src = R * P1 + (x % R2) + P2 * (x / R2);
+    } else {
+      const int64_t x = e - R * (R1 + R2);
+      src = R * (P1 + P2) + (x % R3) + P3 * (x / R3);
+    }
+    w[e] = w0[src];
+  }
+}
+
+__global__ void k_normalize_cpd(int64_t n1, int64_t n2, int64_t n3, int64_t R, double* __restrict__ w,
+                                double* __restrict__ lambda) {
+  __shared__ double red[33];
+  const int64_t r = blockIdx.x;
+  const int64_t ns[3] = {n1, n2, n3};
+  const int64_t off[3] = {0, R * n1, R * (n1 + n2)};
+  double lam = 1.0;
+  for (int l = 0; l < 3; ++l) {
+    double* col = w + off[l] + ns[l] * r;
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < ns[l]; i += blockDim.x) s += col[i] * col[i];
+    s = block_sum(s, red);
+    const double nrm = sqrt(s);
+    lam *= nrm;
+    if (nrm > 0.0) {
+      const double inv = 1.0 / nrm;
+      for (int64_t i = threadIdx.x; i < ns[l]; i += blockDim.x) col[i] *= inv;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) lambda[r] = lam;
+}
+
+cudaError_t launch_truncate_rows(const int64_t* P, const int64_t* Rt, int64_t R, const double* w0, double* w,
+                                 cudaStream_t st) {
+  k_truncate_rows<<<64, 256, 0, st>>>(P[0], P[1], P[2], Rt[0], Rt[1], Rt[2], R, w0, w);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_normalize_cpd(const int64_t* n, int64_t R, double* w, double* lambda, cudaStream_t st) {
+  k_normalize_cpd<<<(unsigned)R, 256, 0, st>>>(n[0], n[1], n[2], R, w, lambda);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_house_qr(int64_t n, int P, double* Z, int64_t ldz, double* Q, int64_t ldq, cudaStream_t st) {
   k_house_qr<<<1, kQrThreads, 0, st>>>(n, P, Z, ldz, Q, ldq);
   return cudaGetLastError();

@@ -24,7 +24,8 @@ struct tf_ctx {
   DevBuf dgnGrad, dgnX, dgnY, dgnGrams, dgnGamma, dgnScal, dgnPart;  // dGN outer loop
   DevBuf gemmPart;                          // compression: GEMM split-K partials
   DevBuf eigQ, eigZ, eigH, eigV, eigU, eigRes, eigScal, eigB;  // compression: subspace iteration
-  DevBuf mlG, mlU, mlLam, mlX, mlY, mlRanks;              // compression: Grams, U, core intermediates
+  DevBuf mlG, mlU, mlLam, mlX, mlY, mlRanks;
+  DevBuf cpdU, cpdSig, cpdS, cpdW, cpdGrad, cpdScal;   // tf_cpd pipeline              // compression: Grams, U, core intermediates
   double* scal_host = nullptr;              // pinned, dGN scalars
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};

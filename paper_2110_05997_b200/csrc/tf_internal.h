@@ -133,6 +133,11 @@ cudaError_t launch_sign_fix(int64_t n, int P, double* U, int64_t ld, cudaStream_
 cudaError_t launch_sqrt_abs(int64_t n, const double* lam, double* sigma, cudaStream_t st);
 // Alg. Compression rank choice for one mode: first i with sum_{r>i} s_r^2 / sum s_r^2 < tol3 (s = sigma)
 cudaError_t launch_trunc_rank(int P, const double* sigma, double tol3, int64_t* rank, cudaStream_t st);
+// copy rows 0..Rt_l-1 of each P_l x R block of w0 = [W1 | W2 | W3] into the packed core point w
+cudaError_t launch_truncate_rows(const int64_t* P, const int64_t* Rt, int64_t R, const double* w0, double* w,
+                                 cudaStream_t st);
+// unit columns and lambda_r = prod_l ||W_l[:, r]|| (one block per r); zero columns are left as they are
+cudaError_t launch_normalize_cpd(const int64_t* n, int64_t R, double* w, double* lambda, cudaStream_t st);
 // MLSVD-energy initialisation: the R entries of largest |s| of S (P1 x P2 x P3) -> packed w (core dims)
 cudaError_t launch_energy_init(int64_t P1, int64_t P2, int64_t P3, const double* S, int64_t R, double* w,
                                cudaStream_t st);

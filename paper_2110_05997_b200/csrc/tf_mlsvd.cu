@@ -383,4 +383,77 @@ tf_status tf_uncompress(tf_ctx* c, int64_t n, int64_t Rl, const double* U, const
   return gemm_run(c, gemm_args(opnd(U, n, false), opnd(W, Rl, true), n, R, Rl, out, n));
 }
 
+tf_status tf_cpd(tf_ctx* c, tf_dims d, const double* T, const double* Omega, const double* w0_core,
+                 const tf_cpd_params* prm, double* W, double* lambda, tf_cpd_result* res, double* hist) {
+  tf_status s = check_whole(c, d);
+  if (s) return s;
+  if (!T || !Omega || !prm || !W || !lambda || !res) return set_err(c, TF_ERR_ARG, "null pointer");
+  if (!prm->init && !w0_core) return set_err(c, TF_ERR_ARG, "init = 0 needs w0_core");
+  if (d.R < 1 || d.R > TF_MAX_R) return set_err(c, d.R < 1 ? TF_ERR_ARG : TF_ERR_UNSUPPORTED, "bad R");
+  cudaSetDevice(c->device);
+  const int64_t R = d.R;
+  const int64_t dims[3] = {d.I, d.J, d.K};
+  int64_t P[3];
+  int64_t nU = 0;
+  for (int l = 0; l < 3; ++l) {
+    P[l] = std::min<int64_t>(dims[l], R);
+    nU += dims[l] * P[l];
+  }
+  const int64_t n = R * (d.I + d.J + d.K);
+  if ((s = ensure(c, c->cpdU, (size_t)nU * 8))) return s;
+  if ((s = ensure(c, c->cpdSig, (size_t)(P[0] + P[1] + P[2]) * 8))) return s;
+  if ((s = ensure(c, c->cpdS, (size_t)P[0] * P[1] * P[2] * 8))) return s;
+  if ((s = ensure(c, c->cpdW, (size_t)R * (P[0] + P[1] + P[2]) * 8))) return s;
+  if ((s = ensure(c, c->cpdGrad, (size_t)n * 8))) return s;
+  if ((s = ensure(c, c->cpdScal, (size_t)red_blocks() * 2 * 8 + 64))) return s;
+  double* U = (double*)c->cpdU.p;
+  double* S = (double*)c->cpdS.p;
+  double* wc = (double*)c->cpdW.p;
+  // 1. compression
+  int64_t rk[3];
+  if ((s = tf_compress(c, d, T, Omega, prm->mlsvd_tol, prm->eig_maxiter, 0.0, U, (double*)c->cpdSig.p, S, rk,
+                       res->eig_iters)))
+    return s;
+  for (int l = 0; l < 3; ++l) res->ranks[l] = rk[l];
+  // 2. initialisation on the core
+  if (prm->init) {
+    if (R > rk[0] * rk[1] * rk[2]) return set_err(c, TF_ERR_ARG, "R exceeds the entries of the truncated core");
+    TF_CUDA(c, launch_energy_init(rk[0], rk[1], rk[2], S, R, wc, c->stream));
+  } else {
+    TF_CUDA(c, launch_truncate_rows(P, rk, R, w0_core, wc, c->stream));
+  }
+  c->total_launches += 1;
+  // 3. dGN on the core
+  tf_dims dc;
+  memset(&dc, 0, sizeof(dc));
+  dc.I = rk[0];
+  dc.J = rk[1];
+  dc.K = rk[2];
+  dc.R = R;
+  if ((s = tf_cpd_dgn(c, dc, S, wc, &prm->dgn, &res->dgn, hist))) return s;
+  // 4. uncompression W~_l = U~_l W_l (U~_l = the first R~_l columns of U_l)
+  int64_t uoff = 0, woff = 0, ooff = 0;
+  for (int l = 0; l < 3; ++l) {
+    if ((s = gemm_run(c, gemm_args(opnd(U + uoff, dims[l], false), opnd(wc + woff, rk[l], true), dims[l], R, rk[l],
+                                   W + ooff, dims[l]))))
+      return s;
+    uoff += dims[l] * P[l];
+    woff += rk[l] * R;
+    ooff += dims[l] * R;
+  }
+  // 5. relative error on the original tensor (one fused evaluation), then the unit-column form
+  double* scal = (double*)c->cpdScal.p;
+  double* part = scal + 8;
+  TF_CUDA(c, launch_tsums(d.I, d.J, d.K, d.ldT, T, part, scal, c->stream));
+  c->total_launches += 1;
+  if ((s = tf_cpd_eval(c, d, T, W, scal + 2, (double*)c->cpdGrad.p, nullptr))) return s;
+  TF_CUDA(c, launch_normalize_cpd(dims, R, W, lambda, c->stream));
+  c->total_launches += 1;
+  double h[3];
+  TF_CUDA(c, cudaMemcpyAsync(h, scal, 3 * 8, cudaMemcpyDeviceToHost, c->stream));
+  TF_CUDA(c, cudaStreamSynchronize(c->stream));
+  res->rel_err = h[1] > 0.0 ? std::sqrt(2.0 * std::max(h[2], 0.0) / h[1]) : 0.0;
+  return TF_OK;
+}
+
 }  // extern "C"

@@ -259,3 +259,73 @@ def test_c5_full_size_compression_sampled(ctx):
         for k in range(K):
             acc += U3[cc, k] * float(U2[b] @ (T3[k] @ U1[a]))
         assert abs(S[cc, b, a].item() - acc) <= 1e-11 * math.sqrt(nT2), (a, b, cc)
+
+
+# ------------------------------------------------------------------------- the whole Tensor Fox flow
+def _oracle_pipeline(T, I, J, K, R, tol, cgi, maxiter, w0_blocks=None, dgn_tol=1e-6):
+    import oracle
+    c = M.compress(T, I, J, K, R, tol)
+    r1, r2, r3 = c["ranks"]
+    if w0_blocks is None:
+        W1, W2, W3, _ = M.energy_init(c["S"], R)
+    else:
+        W1, W2, W3 = (blk[:r] for blk, r in zip(w0_blocks, c["ranks"]))
+    w0 = np.concatenate([W1.T.reshape(-1), W2.T.reshape(-1), W3.T.reshape(-1)])
+    Sflat = jac.storage_from_tensor(c["S"])
+    ref = oracle.dgn(Sflat, w0, r1, r2, r3, R, cgi, maxiter=maxiter, tol=dgn_tol)
+    w = ref["w"]
+    Ws = [w[:R * r1].reshape(R, r1).T, w[R * r1:R * (r1 + r2)].reshape(R, r2).T, w[R * (r1 + r2):].reshape(R, r3).T]
+    full = M.uncompress(c["U"], Ws)
+    unit, lam = M.normalize_cpd(full)
+    return c, ref, unit, lam
+
+
+def test_tf_cpd_warmup(ctx, golden_dir):
+    """Compression -> energy initialisation -> dGN -> uncompression on the warming-up tensor:
+    the GPU flow follows the oracle's flow (same ranks, same first dGN iterates) and, with tol = 1e-12, fits T to
+    the order of the paper's printed final CPD (relative error 5.6e-7): below 1e-6. Long dGN runs
+    are chaotic in the last bits (different fp64 summation orders), so only the first iterations are compared
+    entry by entry and the end point by its quality."""
+    T = warmup_T(golden_dir)
+    cgi = synth.cg_budget(200, seed=9)
+    Om = synth.omega_blocks((6, 5, 4), 3, "cpu")
+    W, lam, out, hist = ctx.tf_cpd(tf.Dims(6, 5, 4, 3), torch.from_numpy(T).cuda(), Om.cuda(), cgi, tol=1e-12)
+    c, ref, unit, lam_ref = _oracle_pipeline(T, 6, 5, 4, 3, 1e-6, cgi, None, dgn_tol=1e-12)
+    assert out["ranks"] == c["ranks"] == (3, 3, 3)
+    n0 = min(10, len(hist), len(ref["hist"]))
+    assert np.allclose(hist[:n0, 0], ref["hist"][:n0, 0], rtol=1e-8, atol=0)
+    assert np.array_equal(hist[:n0, 2], ref["hist"][:n0, 2]) or np.allclose(hist[:n0, 2], ref["hist"][:n0, 2],
+                                                                           rtol=1e-12)
+    assert out["rel_err"] < 1e-6 and ref["hist"][-1, 1] < 1e-6, (out, ref["hist"][-1])
+    Wn = to_np(W)
+    t = jac.tensor_from_storage(T, 6, 5, 4)
+    a, b, cc = (Wn[:18].reshape(3, 6).T, Wn[18:33].reshape(3, 5).T, Wn[33:].reshape(3, 4).T)
+    for X in (a, b, cc):
+        assert np.allclose(np.linalg.norm(X, axis=0), 1.0, atol=1e-14)
+    rec = np.einsum("r,ir,jr,kr->ijk", to_np(lam), a, b, cc)
+    assert abs(np.linalg.norm(t - rec) / np.linalg.norm(t) - out["rel_err"]) <= 1e-2 * out["rel_err"] + 1e-14
+
+
+def test_tf_cpd_random_init_recipe(ctx):
+    """The flow with a random N(0,1) start on the core on a reduced c3 recipe (collinear
+    factors, noise), a fixed number of dGN iterations: the trajectory and the uncompressed factors match the
+    oracle's flow."""
+    Pb = synth.make_problem("c3", "cpu", dims=(60, 50, 40, 5))
+    c = Pb.cfg
+    I, J, K, R = c.I, c.J, c.K, c.R
+    T = to_np(Pb.T).reshape(-1)
+    cgi = synth.cg_budget(12, seed=2)
+    Ps = [min(n, R) for n in (I, J, K)]
+    blocks = [synth.randn((R, p), torch.device("cpu"), "core-init", l).numpy().T for l, p in enumerate(Ps)]
+    w0 = torch.from_numpy(np.concatenate([b.T.reshape(-1) for b in blocks]))
+    Om = synth.omega_blocks((I, J, K), R, "cpu")
+    W, lam, out, hist = ctx.tf_cpd(tf.Dims(I, J, K, R), Pb.T.cuda(), Om.cuda(), cgi, w0_core=w0.cuda(), maxiter=12,
+                                   tol=0.0)
+    cref, ref, unit, lam_ref = _oracle_pipeline(T, I, J, K, R, 1e-6, cgi, 12, w0_blocks=blocks, dgn_tol=0.0)
+    assert out["ranks"] == cref["ranks"]
+    assert out["dgn"]["iters"] == ref["iters"] == 12
+    assert np.allclose(hist[:, 0], ref["hist"][:, 0], rtol=1e-7)
+    assert np.allclose(hist[:, 2], ref["hist"][:, 2], rtol=1e-12)
+    Wr = np.concatenate([u.T.reshape(-1) for u in unit])
+    assert np.linalg.norm(to_np(W) - Wr) <= 1e-6 * np.linalg.norm(Wr)
+    assert np.allclose(to_np(lam), lam_ref, rtol=1e-6)

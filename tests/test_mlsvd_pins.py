@@ -200,3 +200,19 @@ def test_energy_bound_of_truncation():
         assert lhs <= rhs * (1 + 1e-12) + 1e-20
         # and the orthogonal projection identity ||T - T~|| = ||S - S~|| (PAPER.md:2553 footnote)
         assert abs(math.sqrt(lhs) / np.linalg.norm(t) - M.truncation_error(m["S"], shape)) < 1e-12
+
+
+def test_normalize_cpd_output_form():
+    """The unit-column output form: sum_r lambda_r w_r^(1)⊗w_r^(2)⊗w_r^(3) is the same
+    tensor, every column has unit norm, lambda_r = prod of the column norms; a zero column gives lambda 0."""
+    A, B, C = (RNG.standard_normal((n, 4)) for n in (5, 6, 7))
+    C[:, 2] = 0.0
+    (a, b, c), lam = M.normalize_cpd([A, B, C])
+    t0 = np.einsum("ir,jr,kr->ijk", A, B, C)
+    t1 = np.einsum("r,ir,jr,kr->ijk", lam, a, b, c)
+    assert np.allclose(t0, t1, atol=1e-13)
+    for X in (a, b):
+        assert np.allclose(np.linalg.norm(X, axis=0), 1.0)
+    assert lam[2] == 0.0 and np.allclose(np.linalg.norm(c[:, [0, 1, 3]], axis=0), 1.0)
+    assert np.allclose(lam[[0, 1, 3]], [np.linalg.norm(A[:, r]) * np.linalg.norm(B[:, r]) * np.linalg.norm(C[:, r])
+                                       for r in (0, 1, 3)])
