@@ -329,6 +329,35 @@ def run_ours(args):
         v, sample, _ = oracle_sample(cfg, Ts, wn, k_sl, 1 if cfg.cg_iters else 0, threads)
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample}
 
+    # compression stage (NEXT #3), measured once beside the step on the resident T (not part of `value`)
+    stages = None
+    if rank == 0 and world == 1 and not args.no_stages:
+        Om = synth.omega_blocks((I, J, K), R, dev)
+        ctx.tf_compress(dglob, P.T, Om)
+        ctx.tf_unfolding_grams(dglob, P.T)
+        torch.cuda.synchronize(dev)
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        ctx.tf_unfolding_grams(dglob, P.T)
+        s1.record(stream)
+        torch.cuda.synchronize(dev)
+        gram_ms = s0.elapsed_time(s1)
+        reps = 3
+        s0.record(stream)
+        for _ in range(reps):
+            comp = ctx.tf_compress(dglob, P.T, Om)
+        s1.record(stream)
+        torch.cuda.synchronize(dev)
+        comp_ms = s0.elapsed_time(s1) / reps
+        gram_flops = sum((nl + 1) for nl in (I, J, K)) * float(I) * J * K   # symmetric T_(l) T_(l)^T, algorithmic
+        stages = {"compress": {"ms": comp_ms, "ranks": list(comp["ranks"]), "eig_iters": comp["eig_iters"],
+                               "unfolding_grams_ms": gram_ms,
+                               "unfolding_grams_tflops": gram_flops / (gram_ms * 1e-3) / 1e12,
+                               "unfolding_grams_frac": gram_flops / (gram_ms * 1e-3) / 1e12 / peak_tf,
+                               "what": "tf_compress: 3 unfolding Grams (k_gemm_dmma, symmetric tiles) + top-P "
+                                       "eigenpairs (subspace iteration) + multilinear core; mlsvd_tol 1e-6"}}
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -340,7 +369,7 @@ def run_ours(args):
                        "l2": f"inputs larger than L2 (T = {cfg.t_bytes / 1e9:.2f} GB > 126 MB), no flush",
                        "step": "tf_cpd_eval + tf_grams + tf_cg_solve(cg_iters)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
-            "gpu_launches": int(launches),
+            "gpu_launches": int(launches), "stages": stages,
         }
         print(json.dumps(line), flush=True)
     ctx.close()
@@ -359,6 +388,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-stages", action="store_true", help="skip the compression-stage measurement")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
