@@ -249,6 +249,22 @@ typedef struct {
 tf_status tf_cpd(tf_ctx *ctx, tf_dims d, const double *T, const double *Omega, const double *w0_core,
                  const tf_cpd_params *prm, double *W, double *lambda, tf_cpd_result *res, double *hist);
 
+/* ---------------------------------------------------------------------------------------------------
+ * NEXT #4 -- CP-ALS (Alg. ALS), the second workload on the slice-streaming MTTKRP. */
+
+/* M = T_(mode) (W^(L) ⊙ ... ⊙ W^(mode+1) ⊙ W^(mode-1) ⊙ ... ⊙ W^(1)) (Thm unfolding-formula2's order,
+ * PAPER.md:1282-1285): I_mode x R, column-major. Runs as DMMA GEMMs over chunks of the materialised
+ * Khatri-Rao product (<= 512 MB each). K-sharded calls: modes 1 and 2 give the partial sum over the local
+ * slices, mode 3 the local rows k_begin .. k_begin+K-1 (M is K x R). */
+tf_status tf_mttkrp(tf_ctx *ctx, tf_dims d, const double *T, const double *w, int mode, double *M);
+
+/* `sweeps` sweeps of Alg. ALS from w (device, updated in place): for l = 1, 2, 3 in turn,
+ * W^(l) = T_(l) (⊙ others) ((* others' Grams))^dagger (Thm special-products 11-12), the
+ * pseudo-inverse taken from the Jacobi eigen-decomposition with numpy's cut-off (eigenvalues below
+ * 1e-15 x the largest are dropped; reading R30). f_hist (host, nullable, 3*sweeps): F after every update,
+ * from one fused evaluation each (extra passes over T). Needs the whole tensor (K == K_total). */
+tf_status tf_als(tf_ctx *ctx, tf_dims d, const double *T, double *w, int sweeps, double *f_hist);
+
 /* Instrumentation (bench.py): when enabled, the fused evaluation kernel is
  * bracketed by CUDA events on the ctx stream; tf_ctx_kernel_stats synchronizes
  * and returns the summed device time (ms) and count of the fused-kernel launches

@@ -78,6 +78,10 @@ _lib.tf_energy_init.argtypes = [_vp, _i64, _i64, _i64, _vp, _i64, _vp]
 _lib.tf_uncompress.argtypes = [_vp, _i64, _i64, _vp, _vp, _i64, _vp]
 
 
+_lib.tf_mttkrp.argtypes = [_vp, TfDims, _vp, _vp, ctypes.c_int, _vp]
+_lib.tf_als.argtypes = [_vp, TfDims, _vp, _vp, ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+
+
 class TfCpdParams(ctypes.Structure):
     _fields_ = [("mlsvd_tol", ctypes.c_double), ("eig_maxiter", ctypes.c_int), ("init", ctypes.c_int),
                 ("dgn", TfDgnParams)]
@@ -97,7 +101,7 @@ EXPORTED = ["tf_ctx_create", "tf_ctx_destroy", "tf_ctx_set_stream", "tf_status_s
             "tf_grams", "tf_hadamard", "tf_cpd_eval", "tf_cpd_eval_host", "tf_gn_matvec", "tf_cg_solve",
             "tf_reg_gamma", "tf_gn_matvec_damped", "tf_cg_solve_damped", "tf_cpd_dgn", "tf_ctx_set_timing",
             "tf_ctx_kernel_stats", "tf_unfolding_grams", "tf_sym_eig_top", "tf_multilinear_core", "tf_compress",
-            "tf_energy_init", "tf_uncompress", "tf_cpd"]
+            "tf_energy_init", "tf_uncompress", "tf_cpd", "tf_mttkrp", "tf_als"]
 
 TF_OK, TF_ERR_ARG, TF_ERR_ALIGN, TF_ERR_UNSUPPORTED, TF_ERR_CUDA, TF_ERR_NONFINITE, TF_ERR_ALLOC = range(7)
 MAX_R = 128
@@ -425,6 +429,30 @@ class Context:
                "dgn": {"iters": res.dgn.iters, "reason": res.dgn.reason, "f": res.dgn.f, "rel_err": res.dgn.rel_err,
                        "mu": res.dgn.mu}, "rel_err": res.rel_err}
         return W, lam, out, hist.reshape(-1, 5)[:res.dgn.iters]
+
+    # ------------------------------------------------------------------ CP-ALS (NEXT #4)
+    def tf_mttkrp(self, d: Dims, T: torch.Tensor, w: torch.Tensor, mode: int, M: torch.Tensor | None = None):
+        """M = T_(mode) (⊙ of the other factors), (I_mode x R) column-major flat."""
+        ldT = d.ldT or d.I
+        _dev(T, "T", ldT * d.J * d.K - (ldT - d.I))
+        _dev(w, "w", d.n)
+        rows = (d.I, d.J, d.K)[mode - 1]
+        if M is None:
+            M = torch.empty(rows * d.R, dtype=torch.float64, device=T.device)
+        _dev(M, "M", rows * d.R)
+        self._check(_lib.tf_mttkrp(self._h, d.c(), _ptr(T), _ptr(w), int(mode), _ptr(M)))
+        return M
+
+    def tf_als(self, d: Dims, T: torch.Tensor, w: torch.Tensor, sweeps: int, track_f: bool = False):
+        """Alg. ALS sweeps on w (device, in place). Returns F after every update (3*sweeps) if track_f."""
+        import numpy as np
+        ldT = d.ldT or d.I
+        _dev(T, "T", ldT * d.J * d.K - (ldT - d.I))
+        _dev(w, "w", d.n)
+        fh = np.zeros(max(3 * sweeps, 1)) if track_f else None
+        self._check(_lib.tf_als(self._h, d.c(), _ptr(T), _ptr(w), int(sweeps),
+                                fh.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if track_f else None))
+        return fh[:3 * sweeps] if track_f else None
 
     def set_timing(self, enable: bool):
         self._check(_lib.tf_ctx_set_timing(self._h, int(bool(enable))))

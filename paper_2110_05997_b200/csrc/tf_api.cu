@@ -265,7 +265,7 @@ tf_status tf_ctx_destroy(tf_ctx* c) {
                     &c->dgnY, &c->dgnGrams, &c->dgnGamma, &c->dgnScal, &c->dgnPart, &c->gemmPart,
                     &c->eigQ, &c->eigZ, &c->eigH, &c->eigV, &c->eigU, &c->eigRes, &c->eigScal, &c->eigB, &c->mlG,
                     &c->mlU, &c->mlLam, &c->mlX, &c->mlY, &c->mlRanks, &c->cpdU, &c->cpdSig, &c->cpdS,
-                    &c->cpdW, &c->cpdGrad, &c->cpdScal};
+                    &c->cpdW, &c->cpdGrad, &c->cpdScal, &c->alsKR, &c->alsM, &c->alsSmall, &c->alsF};
   for (DevBuf* b : bufs) free_buf(*b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (int i = 0; i < 2; ++i) {

@@ -25,7 +25,8 @@ struct tf_ctx {
   DevBuf gemmPart;                          // compression: GEMM split-K partials
   DevBuf eigQ, eigZ, eigH, eigV, eigU, eigRes, eigScal, eigB;  // compression: subspace iteration
   DevBuf mlG, mlU, mlLam, mlX, mlY, mlRanks;
-  DevBuf cpdU, cpdSig, cpdS, cpdW, cpdGrad, cpdScal;   // tf_cpd pipeline              // compression: Grams, U, core intermediates
+  DevBuf cpdU, cpdSig, cpdS, cpdW, cpdGrad, cpdScal;   // tf_cpd pipeline
+  DevBuf alsKR, alsM, alsSmall, alsF;                 // CP-ALS              // compression: Grams, U, core intermediates
   double* scal_host = nullptr;              // pinned, dGN scalars
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
@@ -48,6 +49,12 @@ tf_status set_err(tf_ctx* c, tf_status s, const std::string& msg);
 tf_status cuda_err(tf_ctx* c, cudaError_t e, const char* where);
 tf_status ensure(tf_ctx* c, DevBuf& b, size_t bytes);
 void free_buf(DevBuf& b);
+
+// generic DMMA GEMM (k_gemm.cu) planning and launch, tf_mlsvd.cu
+tfk::GemmOperand opnd(const double* p, int64_t ld, bool kc, int64_t bstride = 0);
+tfk::GemmArgs gemm_args(tfk::GemmOperand a, tfk::GemmOperand b, int64_t M, int64_t N, int64_t Kd, double* C,
+                        int64_t ldc);
+tf_status gemm_run(tf_ctx* c, tfk::GemmArgs g);
 
 }  // namespace tfh
 

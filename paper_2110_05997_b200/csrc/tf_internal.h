@@ -142,4 +142,9 @@ cudaError_t launch_normalize_cpd(const int64_t* n, int64_t R, double* w, double*
 cudaError_t launch_energy_init(int64_t P1, int64_t P2, int64_t P3, const double* S, int64_t R, double* w,
                                cudaStream_t st);
 
+// ---- CP-ALS (NEXT #4, k_als.cu)
+cudaError_t launch_khatri_rao(int64_t nx, const double* X, int64_t x0, int64_t xn, int64_t ny, const double* Y,
+                              int64_t R, double* KR, cudaStream_t st);
+cudaError_t launch_pinv_from_eig(int R, const double* Q, const double* theta, double* out, cudaStream_t st);
+
 }  // namespace tfk

@@ -10,7 +10,7 @@
 using namespace tfk;
 using namespace tfh;
 
-namespace {
+namespace tfh {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
@@ -48,7 +48,7 @@ bool make_map(CUtensorMap* map, const GemmOperand& x, int64_t np, int64_t nk, in
   return r == CUDA_SUCCESS;
 }
 
-GemmOperand opnd(const double* p, int64_t ld, bool kc, int64_t bstride = 0) {
+GemmOperand opnd(const double* p, int64_t ld, bool kc, int64_t bstride) {
   GemmOperand o;
   o.ptr = p;
   o.ld = ld;
@@ -61,8 +61,11 @@ GemmOperand opnd(const double* p, int64_t ld, bool kc, int64_t bstride = 0) {
 // waves * (k-steps per split + overhead) over the SMs, bounded by the partial-buffer size.
 tf_status gemm_run(tf_ctx* c, GemmArgs g) {
   if (g.M <= 0 || g.N <= 0) return TF_OK;
+  // tile: 128 or 64 rows; 128, 112, 96 or 64 columns (the narrower widths cut the padding of N = R
+  // around 100 on the 128-row tile)
   g.BM = g.M > 64 ? 128 : 64;
-  g.BN = g.N > 64 ? 128 : 64;
+  g.BN = g.N > 112 ? 128 : g.N > 96 ? 112 : g.N > 64 ? 96 : 64;
+  if (g.BM == 64 && (g.BN == 112 || g.BN == 96)) g.BN = 128;
   if (g.sym) g.BN = g.BM;
   g.ntm = (g.M + g.BM - 1) / g.BM;
   g.ntn = (g.N + g.BN - 1) / g.BN;
@@ -125,6 +128,10 @@ GemmArgs gemm_args(GemmOperand a, GemmOperand b, int64_t M, int64_t N, int64_t K
   g.beta = 0.0;
   return g;
 }
+
+}  // namespace tfh
+
+namespace {
 
 tf_status check_whole(tf_ctx* c, tf_dims& d) {
   if (!c) return TF_ERR_ARG;
