@@ -357,6 +357,29 @@ def run_ours(args):
                                "unfolding_grams_frac": gram_flops / (gram_ms * 1e-3) / 1e12 / peak_tf,
                                "what": "tf_compress: 3 unfolding Grams (k_gemm_dmma, symmetric tiles) + top-P "
                                        "eigenpairs (subspace iteration) + multilinear core; mlsvd_tol 1e-6"}}
+        # CP-ALS (NEXT #4): the three single-mode MTTKRPs and one sweep from the same point
+        wa = w.clone()
+        mt = []
+        for mode in (1, 2, 3):
+            M = ctx.tf_mttkrp(dglob, P.T, wa, mode)
+            s0.record(stream)
+            ctx.tf_mttkrp(dglob, P.T, wa, mode, M)
+            s1.record(stream)
+            torch.cuda.synchronize(dev)
+            mt.append(s0.elapsed_time(s1))
+        ctx.tf_als(dglob, P.T, wa, 1)
+        torch.cuda.synchronize(dev)
+        s0.record(stream)
+        ctx.tf_als(dglob, P.T, wa, 1)
+        s1.record(stream)
+        torch.cuda.synchronize(dev)
+        sweep_ms = s0.elapsed_time(s1)
+        mt_flops = 2.0 * I * J * K * R
+        stages["als"] = {"sweep_ms": sweep_ms, "mttkrp_ms": mt,
+                         "mttkrp_tflops": [mt_flops / (x * 1e-3) / 1e12 for x in mt],
+                         "mttkrp_frac": [mt_flops / (x * 1e-3) / 1e12 / peak_tf for x in mt],
+                         "what": "tf_als: per mode one MTTKRP (chunked Khatri-Rao + k_gemm_dmma) + Grams + Jacobi "
+                                 "pseudo-inverse + W = M V^+; tf_mttkrp alone timed per mode"}
 
     if rank == 0:
         line = {
