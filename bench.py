@@ -4,6 +4,9 @@
 One step = one full pass of the hot path over the workload:
   tf_cpd_eval (residual, F, three fused MTTKRPs, Grams)  [+ one SUM all-reduce of [grad|f] when N>1]
   + tf_cg_solve (Hadamard chains, Jacobi-free CG on (J^T J + lambda I) x = -grad, fixed iterations)
+The evaluation uses the library's default guarded Pi form (reading R31 of DESIGN.md): the three MTTKRPs of T
+in one pass (4IJKR flops) with F by the Gram expansion, rerun in the residual form (6IJKR) on the device when
+cancellation makes the expansion unsafe; the JSON line reports which one the timed steps used.
 Default workload: c5 (1200^3, R=100, 13.8 GB fp64 T, 20 CG iterations) — the largest BASELINE
 config, the one the north star's scaling target is quoted on, and it fits one GPU.
 
@@ -259,17 +262,25 @@ def run_ours(args):
     ms_per_step = ms_total / args.steps
     value = 1000.0 / ms_per_step          # whole-job evaluations of the full problem per second
 
-    # roofline of the dominant kernel (the fused evaluation kernel), on this rank
+    # roofline of the dominant kernel (the fused evaluation kernel), on this rank. The evaluation runs in the
+    # guarded Pi form (two DMMA slice contractions: 4*I*J*K*R flops) unless its cancellation guard fell back to
+    # the residual form (three contractions: 6*I*J*K*R) — ask the library which one the timed steps used.
     kernel_ms = eval_ms / max(1, eval_n)
-    flops = 6.0 * I * J * (k1 - k0) * R
+    fell_back = ctx.eval_fell_back()
+    form = "residual" if fell_back != 0 else "pi"
+    nctr = 6.0 if form == "residual" else 4.0
+    flops = nctr * I * J * (k1 - k0) * R
     peak_tf, peak_bw = fp64_peak()
     achieved_tf = flops / (kernel_ms * 1e-3) / 1e12
     prof = load_json(os.path.join(ROOT, "profiles", f"ncu_eval_{cfg.name}_r01.json"), {}) or {}
     traffic = prof.get("dram_bytes_per_launch") if world == 1 else None
     roofline = {"bound": "tensor", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": achieved_tf / peak_tf, "traffic": traffic,
-                "kernel": "k_eval_fused", "kernel_ms": kernel_ms,
-                "algorithmic": f"6*I*J*K_local*R = {flops:.4e} flop per launch (3 DMMA contractions per slice)",
+                "kernel": "k_eval_fused", "kernel_ms": kernel_ms, "eval_form": form,
+                "algorithmic": (f"{int(nctr)}*I*J*K_local*R = {flops:.4e} flop per evaluation "
+                                + ("(Pi form: T_k B and T_k^T A diag(c_k) per slice, PAPER.md:2641; kernel_ms spans "
+                                   "the MTTKRP pass through the guard)" if form == "pi" else
+                                   "(residual form: 3 DMMA contractions per slice)")),
                 "peak_source": "measured FP64 DMMA (mma.sync.m8n8k4.f64) peak, tools/peaks.cu, profiles/peaks_r01.json",
                 "hbm": {"bytes": 8.0 * I * J * (k1 - k0), "achieved_gbs": 8.0 * I * J * (k1 - k0) / (kernel_ms * 1e-3) / 1e9,
                         "peak_gbs": peak_bw}}

@@ -265,6 +265,22 @@ tf_status tf_mttkrp(tf_ctx *ctx, tf_dims d, const double *T, const double *w, in
  * from one fused evaluation each (extra passes over T). Needs the whole tensor (K == K_total). */
 tf_status tf_als(tf_ctx *ctx, tf_dims d, const double *T, double *w, int sweeps, double *f_hist);
 
+/* How tf_cpd_eval forms F and grad F (both give the same values to fp64 accuracy; reading R31):
+ *   0 (default, auto): form 2 when the evaluation is large enough to amortise its extra launches
+ *     (6*I*J*K*R >= 5e9 flops), else form 1;
+ *   2 guarded Pi form at any size: one pass over T computes the three MTTKRPs T_(l)(.W) (two DMMA slice
+ *     contractions, 4*I*J*K*R flops; PAPER.md:2641 grad = W Pi - T_(l)(.W)) and F = 1/2||T||^2 - <A, M1> +
+ *     1/2 sum(piA * piB * piC); when cancellation makes that unsafe (2F < 1e-3 ||T||^2 or
+ *     ||grad|| < 1e-3 ||W Pi||, i.e. near an exact fit or a stationary point) the residual form is rerun
+ *     on the device automatically;
+ *   1 residual form always: E_k = T_k - A diag(c_k) B^T in registers, F = 1/2 sum E^2, grad = J^T f
+ *     (three contractions, 6*I*J*K*R flops). The environment variable TF_EVAL_FORM=residual selects 1
+ *     for new contexts. */
+tf_status tf_ctx_set_eval_form(tf_ctx *ctx, int form);
+/* Synchronizes and reports whether the last guarded Pi-form evaluation on this ctx fell back to the
+ * residual form (1), did not (0), or no Pi-form evaluation has run (-1). */
+tf_status tf_ctx_eval_fallback(tf_ctx *ctx, int *fell_back);
+
 /* Instrumentation (bench.py): when enabled, the fused evaluation kernel is
  * bracketed by CUDA events on the ctx stream; tf_ctx_kernel_stats synchronizes
  * and returns the summed device time (ms) and count of the fused-kernel launches

@@ -67,6 +67,8 @@ class TfDgnResult(ctypes.Structure):
 _lib.tf_cpd_dgn.argtypes = [_vp, TfDims, _vp, _vp, ctypes.POINTER(TfDgnParams), ctypes.POINTER(TfDgnResult),
                             ctypes.POINTER(ctypes.c_double)]
 _lib.tf_ctx_set_timing.argtypes = [_vp, ctypes.c_int]
+_lib.tf_ctx_set_eval_form.argtypes = [_vp, ctypes.c_int]
+_lib.tf_ctx_eval_fallback.argtypes = [_vp, ctypes.POINTER(ctypes.c_int)]
 _i64 = ctypes.c_int64
 _lib.tf_unfolding_grams.argtypes = [_vp, TfDims, _vp, _vp, _vp, _vp]
 _lib.tf_sym_eig_top.argtypes = [_vp, _i64, _vp, _i64, _vp, ctypes.c_int, ctypes.c_double, _vp, _vp,
@@ -101,7 +103,8 @@ EXPORTED = ["tf_ctx_create", "tf_ctx_destroy", "tf_ctx_set_stream", "tf_status_s
             "tf_grams", "tf_hadamard", "tf_cpd_eval", "tf_cpd_eval_host", "tf_gn_matvec", "tf_cg_solve",
             "tf_reg_gamma", "tf_gn_matvec_damped", "tf_cg_solve_damped", "tf_cpd_dgn", "tf_ctx_set_timing",
             "tf_ctx_kernel_stats", "tf_unfolding_grams", "tf_sym_eig_top", "tf_multilinear_core", "tf_compress",
-            "tf_energy_init", "tf_uncompress", "tf_cpd", "tf_mttkrp", "tf_als"]
+            "tf_energy_init", "tf_uncompress", "tf_cpd", "tf_mttkrp", "tf_als", "tf_ctx_set_eval_form",
+            "tf_ctx_eval_fallback"]
 
 TF_OK, TF_ERR_ARG, TF_ERR_ALIGN, TF_ERR_UNSUPPORTED, TF_ERR_CUDA, TF_ERR_NONFINITE, TF_ERR_ALLOC = range(7)
 MAX_R = 128
@@ -453,6 +456,17 @@ class Context:
         self._check(_lib.tf_als(self._h, d.c(), _ptr(T), _ptr(w), int(sweeps),
                                 fh.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if track_f else None))
         return fh[:3 * sweeps] if track_f else None
+
+    def set_eval_form(self, form: str):
+        """'auto' (default: the guarded Pi form, 4IJKR flops, when large enough), 'pi' (guarded Pi form at any
+        size) or 'residual' (6IJKR flops) for tf_cpd_eval."""
+        self._check(_lib.tf_ctx_set_eval_form(self._h, {"auto": 0, "residual": 1, "pi": 2}[form]))
+
+    def eval_fell_back(self) -> int:
+        """1 if the last guarded Pi-form evaluation reran the residual form, 0 if not, -1 if none ran."""
+        v = ctypes.c_int()
+        self._check(_lib.tf_ctx_eval_fallback(self._h, ctypes.byref(v)))
+        return v.value
 
     def set_timing(self, enable: bool):
         self._check(_lib.tf_ctx_set_timing(self._h, int(bool(enable))))

@@ -110,9 +110,12 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 #endif
 
-template <int NT, bool kTMA, int BT>
+// RECON = false is the Pi-form pass (the three MTTKRPs of T itself): phase 1 is skipped,
+// phases 2-3 run on T_k, and the per-CTA scalar is sum t^2 (for the Gram expansion of f).
+template <int NT, bool kTMA, int BT, bool RECON>
 __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
     k_eval_fused(const __grid_constant__ CUtensorMap tmapT, const double* __restrict__ T, EvalArgs p) {
+  if (p.run_if && *p.run_if == 0) return;   // guarded fallback not needed (uniform across the grid)
   using S = EvalSmem<NT, BT>;
   using Gm = EvalTile<BT>;
   constexpr int kBI = Gm::BI, kBJ = Gm::BJ, kLDE = Gm::LDE, NW = Gm::NW, kThreads = Gm::THREADS;
@@ -254,7 +257,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
     TL(kk, 1);
 
     // ---- phase 1: E = T + (-A diag(c)) B^T on a (BT/2) x 16 warp tile (MF x 2 fragments)
-    {
+    if (RECON) {
       double E[MF][NF][2];
 #pragma unroll
       for (int m = 0; m < MF; ++m)
@@ -333,6 +336,13 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
       double ea[kBJ / 4];
 #pragma unroll
       for (int s = 0; s < kBJ / 4; ++s) ea[s] = sT[(4 * s + q) * kLDE + 8 * warp + g];
+      if (!RECON) {   // sum t^2 of this slice tile: warp w's fragments cover rows 8w.., all 64 columns
+#pragma unroll
+        for (int s = 0; s < kBJ / 4; s += 2) {
+          fsum0 = fma(ea[s], ea[s], fsum0);
+          fsum1 = fma(ea[s + 1], ea[s + 1], fsum1);
+        }
+      }
       double gcv[NV];
 #pragma unroll
       for (int j = NT; j < NV; ++j) gcv[j] = 0.0;
@@ -435,6 +445,7 @@ __device__ __forceinline__ double ordered_sum8(const double* __restrict__ x, int
 }
 
 __global__ void k_eval_finalize(EvalArgs p, int RP, double* __restrict__ f, double* __restrict__ grad) {
+  if (p.run_if && *p.run_if == 0) return;
   const int64_t R = p.R;
   const int64_t nA = p.I * R, nB = p.J * R, nC = p.Ktot * R;
   const int64_t total = nA + nB + nC;
@@ -470,18 +481,120 @@ __global__ void k_eval_finalize(EvalArgs p, int RP, double* __restrict__ f, doub
   }
 }
 
-template <int NT, int BT>
-static cudaError_t launch_eval_nt(const CUtensorMap* map, const double* T, const EvalArgs& p, bool tma,
-                                  cudaStream_t st) {
+// Pi-form reduction: the MTTKRP partials of the RECON = false pass (accA = +M1, accB = -M2, gC = +M3) become
+// grad = W Pi - M (Kolda's theorem). On entry grad already holds W Pi (three small DMMA
+// GEMMs with Pi^(l) = Hadamard product of the other Grams, the C Gram over the local slices); rows of dF/dC
+// outside the local slices are written 0. part[blk] = {<A, M1>, ||grad||^2, ||W Pi||^2} per block.
+constexpr int kPiThreads = 256;
+__global__ void __launch_bounds__(kPiThreads) k_eval_finalize_pi(EvalArgs p, int RP, double* __restrict__ grad,
+                                                                 double* __restrict__ part) {
+  const int64_t R = p.R;
+  const int64_t nA = p.I * R, nB = p.J * R, nC = p.Ktot * R;
+  const int64_t total = nA + nB + nC;
+  const int64_t nPA = (int64_t)p.nTj * p.kSplit, nPB = (int64_t)p.nTi * p.kSplit, nPC = (int64_t)p.nTi * p.nTj;
+  double ip = 0.0, g2 = 0.0, w2 = 0.0;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    double m = 0.0;
+    int64_t out;
+    bool live = true;
+    if (idx < nA) {
+      const int64_t i = idx / R, r = idx % R;
+      m = ordered_sum8(p.gAp + i * RP + r, nPA, p.Ipad * RP);
+      out = i + p.I * r;
+      ip = fma(p.A[out], m, ip);
+    } else if (idx < nA + nB) {
+      const int64_t qq = idx - nA, j = qq / R, r = qq % R;
+      m = -ordered_sum8(p.gBp + j * RP + r, nPB, p.Jpad * RP);
+      out = nA + j + p.J * r;
+    } else {
+      const int64_t qq = idx - nA - nB, kg = qq / R, r = qq % R;
+      const int64_t k = kg - p.kbeg;
+      out = nA + nB + kg + p.Ktot * r;
+      if (k >= 0 && k < p.K) m = ordered_sum8(p.gCp + k * RP + r, nPC, p.K * RP);
+      else live = false;
+    }
+    const double wp = live ? grad[out] : 0.0;
+    const double gval = wp - m;
+    grad[out] = gval;
+    g2 = fma(gval, gval, g2);
+    w2 = fma(wp, wp, w2);
+  }
+  __shared__ double red[3][kPiThreads / 32];
+  ip = warp_sum(ip);
+  g2 = warp_sum(g2);
+  w2 = warp_sum(w2);
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = ip;
+    red[1][threadIdx.x >> 5] = g2;
+    red[2][threadIdx.x >> 5] = w2;
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) {
+    double v = 0.0;
+    for (int w = 0; w < kPiThreads / 32; ++w) v += red[threadIdx.x][w];
+    part[blockIdx.x * 3 + threadIdx.x] = v;
+  }
+}
+
+// f = 1/2 ||T||^2 - <A, M1> + 1/2 1^T (piA * piB * piC) 1 and the cancellation guard (one block; every sum in
+// a fixed order: strided per-thread partials, then warps, then thread 0 over the warps).
+__global__ void __launch_bounds__(256) k_eval_pi_guard(EvalArgs p, const double* __restrict__ grams,
+                                                       const double* __restrict__ part, int nblk,
+                                                       double* __restrict__ f, int* __restrict__ flag) {
+  __shared__ double red[5][8];
+  const int64_t R = p.R, RR = R * R;
+  double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};   // t2, x2, ip, g2, w2
+  for (int64_t s = threadIdx.x; s < p.nCta; s += blockDim.x) v[0] += p.fp[s];
+  for (int64_t e = threadIdx.x; e < RR; e += blockDim.x) v[1] += grams[e] * grams[RR + e] * grams[2 * RR + e];
+  for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
+    v[2] += part[3 * b];
+    v[3] += part[3 * b + 1];
+    v[4] += part[3 * b + 2];
+  }
+#pragma unroll
+  for (int u = 0; u < 5; ++u) {
+    const double x = warp_sum(v[u]);
+    if ((threadIdx.x & 31) == 0) red[u][threadIdx.x >> 5] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (int u = 0; u < 5; ++u)
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t[u] += red[u][w];
+    const double fv = (0.5 * t[0] - t[2]) + 0.5 * t[1];
+    *f = fv;
+    const bool safe = (2.0 * fv >= 1e-3 * t[0]) && (t[3] >= 1e-6 * t[4]) && isfinite(fv);
+    *flag = safe ? 0 : 1;
+  }
+}
+
+int eval_pi_blocks(int nsm) { return 2 * nsm; }
+
+cudaError_t launch_eval_finalize_pi(const EvalArgs& p, int RP, double* grad, double* part, int nblk,
+                                    cudaStream_t st) {
+  k_eval_finalize_pi<<<nblk, kPiThreads, 0, st>>>(p, RP, grad, part);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_eval_pi_guard(const EvalArgs& p, const double* grams, const double* part, int nblk, double* f,
+                                 int* flag, cudaStream_t st) {
+  k_eval_pi_guard<<<1, 256, 0, st>>>(p, grams, part, nblk, f, flag);
+  return cudaGetLastError();
+}
+
+template <int NT, int BT, bool RECON>
+static cudaError_t launch_eval_ntr(const CUtensorMap* map, const double* T, const EvalArgs& p, bool tma,
+                                   cudaStream_t st) {
   const size_t smem = EvalSmem<NT, BT>::bytes;
   constexpr int threads = EvalTile<BT>::THREADS;
   if (tma) {
-    auto kern = k_eval_fused<NT, true, BT>;
+    auto kern = k_eval_fused<NT, true, BT, RECON>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<p.nCta, threads, smem, st>>>(*map, T, p);
   } else {
-    auto kern = k_eval_fused<NT, false, BT>;
+    auto kern = k_eval_fused<NT, false, BT, RECON>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     kern<<<p.nCta, threads, smem, st>>>(*map, T, p);
@@ -489,13 +602,21 @@ static cudaError_t launch_eval_nt(const CUtensorMap* map, const double* T, const
   return cudaGetLastError();
 }
 
+template <int NT, int BT>
+static cudaError_t launch_eval_nt(const CUtensorMap* map, const double* T, const EvalArgs& p, bool tma,
+                                  cudaStream_t st, bool recon) {
+  if (BT == 64 && !recon) return launch_eval_ntr<NT, 64, false>(map, T, p, tma, st);
+  return launch_eval_ntr<NT, BT, true>(map, T, p, tma, st);
+}
+
 cudaError_t launch_eval(const CUtensorMap* map, const double* T, const EvalArgs& p, int NT, bool tma, int BT,
-                        cudaStream_t st) {
+                        cudaStream_t st, bool recon) {
   if (BT == 32) {
+    if (!recon) return cudaErrorInvalidValue;   // the Pi-form pass exists for the 64-wide tile only
     switch (NT) {
 #define TF_CASE(n) \
   case n:          \
-    return launch_eval_nt<n, 32>(map, T, p, tma, st);
+    return launch_eval_nt<n, 32>(map, T, p, tma, st, true);
       TF_CASE(1) TF_CASE(2) TF_CASE(3) TF_CASE(4) TF_CASE(5) TF_CASE(6) TF_CASE(7) TF_CASE(8)
       TF_CASE(9) TF_CASE(10) TF_CASE(11) TF_CASE(12) TF_CASE(13) TF_CASE(14) TF_CASE(15) TF_CASE(16)
 #undef TF_CASE
@@ -506,7 +627,7 @@ cudaError_t launch_eval(const CUtensorMap* map, const double* T, const EvalArgs&
   switch (NT) {
 #define TF_CASE(n) \
   case n:          \
-    return launch_eval_nt<n, 64>(map, T, p, tma, st);
+    return launch_eval_nt<n, 64>(map, T, p, tma, st, recon);
     TF_CASE(1) TF_CASE(2) TF_CASE(3) TF_CASE(4) TF_CASE(5) TF_CASE(6) TF_CASE(7) TF_CASE(8)
     TF_CASE(9) TF_CASE(10) TF_CASE(11) TF_CASE(12) TF_CASE(13) TF_CASE(14) TF_CASE(15) TF_CASE(16)
 #undef TF_CASE

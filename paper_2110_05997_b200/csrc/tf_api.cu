@@ -144,6 +144,8 @@ tf_status eval_impl(tf_ctx* c, const tf_dims& d, const double* T, const double* 
   const int BT = eval_tile();
   const int ctas_per_sm = BT == 32 ? 2 : 1;
   EvalArgs p;
+  memset(&p, 0, sizeof(p));
+  p.run_if = nullptr;
   p.A = w;
   p.B = w + d.I * d.R;
   p.C = w + (d.I + d.J) * d.R;
@@ -204,11 +206,64 @@ tf_status eval_impl(tf_ctx* c, const tf_dims& d, const double* T, const double* 
     c->ev_used_pairs++;
     TF_CUDA(c, cudaEventRecord(e0, c->stream));
   }
-  TF_CUDA(c, launch_eval(&map, T, p, NT, tma, BT, c->stream));
+  // small problems are launch-bound: the Pi form's extra launches (Grams, guard, conditional fallback) would
+  // cost more than the reconstruction flops it saves
+  const bool pi_form = BT == 64 && (c->eval_form == 2 || (c->eval_form == 0 && 6.0 * d.I * d.J * d.K * d.R >= 5e9));
+  if (!pi_form) {
+    TF_CUDA(c, launch_eval(&map, T, p, NT, tma, BT, c->stream));
+    if (c->timing) TF_CUDA(c, cudaEventRecord(e1, c->stream));
+    TF_CUDA(c, launch_eval_finalize(p, RP, f, grad, c->nsm, c->stream));
+    c->eval_launches += 1;
+    c->total_launches += 2;
+    return TF_OK;
+  }
+  // Pi form: one pass computes the three MTTKRPs of T (2 contractions per slice), then
+  // grad = W Pi - M and f by the Gram expansion; if cancellation makes that unsafe the residual form runs
+  // (the same kernel with the reconstruction phase; reading R31).
+  const int nblk = eval_pi_blocks(c->nsm);
+  if ((s = ensure(c, c->evGrams, (size_t)9 * d.R * d.R * 8))) return s;
+  if ((s = ensure(c, c->evPart, (size_t)3 * nblk * 8 + 64))) return s;
+  double* grams = (double*)c->evGrams.p;
+  double* part = (double*)c->evPart.p;
+  int* flag = reinterpret_cast<int*>(part + 3 * nblk);
+  TF_CUDA(c, launch_eval(&map, T, p, NT, tma, BT, c->stream, false));
+  if (d.K == d.K_total) {
+    if ((s = grams_impl(c, d, w, grams))) return s;
+  } else {   // C Gram over the local slices only (the partial f and grad of a K-shard)
+    const int64_t R = d.R;
+    GemmArgs ga = gemm_args(opnd(p.A, d.I, true), opnd(p.A, d.I, true), R, R, d.I, grams, R);
+    ga.sym = true;
+    if ((s = gemm_run(c, ga))) return s;
+    GemmArgs gb = gemm_args(opnd(p.B, d.J, true), opnd(p.B, d.J, true), R, R, d.J, grams + R * R, R);
+    gb.sym = true;
+    if ((s = gemm_run(c, gb))) return s;
+    GemmArgs gc = gemm_args(opnd(p.C + d.k_begin, d.K_total, true), opnd(p.C + d.k_begin, d.K_total, true), R, R,
+                            d.K, grams + 2 * R * R, R);
+    gc.sym = true;
+    if ((s = gemm_run(c, gc))) return s;
+  }
+  // W Pi into grad: Pi = [Pi1 | Pi2 | Pi3 | ...] from the (local) Grams, then one small GEMM per mode
+  double* pi = grams + 3 * d.R * d.R;
+  TF_CUDA(c, launch_hadamard(d.R, grams, pi, c->stream));
+  {
+    const int64_t R = d.R, RR = R * R;
+    if ((s = gemm_run(c, gemm_args(opnd(p.A, d.I, false), opnd(pi, R, true), d.I, R, R, grad, d.I)))) return s;
+    if ((s = gemm_run(c, gemm_args(opnd(p.B, d.J, false), opnd(pi + RR, R, true), d.J, R, R, grad + d.I * R,
+                                   d.J))))
+      return s;
+    if ((s = gemm_run(c, gemm_args(opnd(p.C + d.k_begin, d.K_total, false), opnd(pi + 2 * RR, R, true), d.K, R, R,
+                                   grad + (d.I + d.J) * R + d.k_begin, d.K_total))))
+      return s;
+  }
+  TF_CUDA(c, launch_eval_finalize_pi(p, RP, grad, part, nblk, c->stream));
+  TF_CUDA(c, launch_eval_pi_guard(p, grams, part, nblk, f, flag, c->stream));
+  EvalArgs pr = p;
+  pr.run_if = flag;
+  TF_CUDA(c, launch_eval(&map, T, pr, NT, tma, BT, c->stream, true));
   if (c->timing) TF_CUDA(c, cudaEventRecord(e1, c->stream));
-  TF_CUDA(c, launch_eval_finalize(p, RP, f, grad, c->nsm, c->stream));
+  TF_CUDA(c, launch_eval_finalize(pr, RP, f, grad, c->nsm, c->stream));
   c->eval_launches += 1;
-  c->total_launches += 2;
+  c->total_launches += 5;
   return TF_OK;
 }
 
@@ -246,6 +301,10 @@ tf_status tf_ctx_create(tf_ctx** out, int device, void* cuda_stream) {
   c->device = device;
   c->stream = static_cast<cudaStream_t>(cuda_stream);
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device);
+  {
+    const char* e = getenv("TF_EVAL_FORM");
+    c->eval_form = (e && std::string(e) == "residual") ? 1 : 0;
+  }
   if (cudaMallocHost(&c->cg_host, sizeof(CgState)) != cudaSuccess ||
       cudaMallocHost(&c->scal_host, 16 * sizeof(double)) != cudaSuccess) {
     delete c;
@@ -265,7 +324,7 @@ tf_status tf_ctx_destroy(tf_ctx* c) {
                     &c->dgnY, &c->dgnGrams, &c->dgnGamma, &c->dgnScal, &c->dgnPart, &c->gemmPart,
                     &c->eigQ, &c->eigZ, &c->eigH, &c->eigV, &c->eigU, &c->eigRes, &c->eigScal, &c->eigB, &c->mlG,
                     &c->mlU, &c->mlLam, &c->mlX, &c->mlY, &c->mlRanks, &c->cpdU, &c->cpdSig, &c->cpdS,
-                    &c->cpdW, &c->cpdGrad, &c->cpdScal, &c->alsKR, &c->alsM, &c->alsSmall, &c->alsF};
+                    &c->cpdW, &c->cpdGrad, &c->cpdScal, &c->alsKR, &c->alsM, &c->alsSmall, &c->alsF, &c->evGrams, &c->evPart};
   for (DevBuf* b : bufs) free_buf(*b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   for (int i = 0; i < 2; ++i) {
@@ -282,6 +341,28 @@ tf_status tf_ctx_destroy(tf_ctx* c) {
 tf_status tf_ctx_set_stream(tf_ctx* c, void* s) {
   if (!c) return TF_ERR_ARG;
   c->stream = static_cast<cudaStream_t>(s);
+  return TF_OK;
+}
+
+tf_status tf_ctx_set_eval_form(tf_ctx* c, int form) {
+  if (!c) return TF_ERR_ARG;
+  if (form < 0 || form > 2)
+    return set_err(c, TF_ERR_ARG, "eval form must be 0 (auto), 1 (residual) or 2 (guarded Pi form at any size)");
+  c->eval_form = form;
+  return TF_OK;
+}
+
+tf_status tf_ctx_eval_fallback(tf_ctx* c, int* fell_back) {
+  if (!c || !fell_back) return TF_ERR_ARG;
+  *fell_back = -1;
+  if (!c->evPart.p) return TF_OK;
+  cudaSetDevice(c->device);
+  const int nblk = eval_pi_blocks(c->nsm);
+  int v = -1;
+  TF_CUDA(c, cudaMemcpyAsync(&v, reinterpret_cast<int*>((double*)c->evPart.p + 3 * nblk), sizeof(int),
+                             cudaMemcpyDeviceToHost, c->stream));
+  TF_CUDA(c, cudaStreamSynchronize(c->stream));
+  *fell_back = v;
   return TF_OK;
 }
 

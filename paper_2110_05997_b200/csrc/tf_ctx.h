@@ -26,7 +26,9 @@ struct tf_ctx {
   DevBuf eigQ, eigZ, eigH, eigV, eigU, eigRes, eigScal, eigB;  // compression: subspace iteration
   DevBuf mlG, mlU, mlLam, mlX, mlY, mlRanks;
   DevBuf cpdU, cpdSig, cpdS, cpdW, cpdGrad, cpdScal;   // tf_cpd pipeline
-  DevBuf alsKR, alsM, alsSmall, alsF;                 // CP-ALS              // compression: Grams, U, core intermediates
+  DevBuf alsKR, alsM, alsSmall, alsF;                 // CP-ALS
+  DevBuf evGrams, evPart;                             // Pi-form evaluation: local Grams, guard partials
+  int eval_form = 0;                                  // 0 guarded Pi form, 1 residual form              // compression: Grams, U, core intermediates
   double* scal_host = nullptr;              // pinned, dGN scalars
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};

@@ -18,10 +18,22 @@ struct EvalArgs {
   double* gBp;  // [nTi*kSplit][Jpad][RP]
   double* gCp;  // [nTi*nTj][K][RP]
   double* fp;   // [nCta]
+  const int* run_if;   // nullable: the kernel runs only if *run_if != 0 (guarded fallback)
 };
 
+// Pi-form evaluation (PAPER.md:2641 grad = W Pi - T_(l)(.W); f by the Gram expansion), guarded:
+//   launch_eval(..., recon = false) writes the three MTTKRPs of T and sum t^2 into the partials;
+//   launch_eval_finalize_pi forms grad = W Pi - M and per-block partials of <A, M1>, ||grad||^2, ||W Pi||^2;
+//   launch_eval_pi_guard sums them, writes f and *flag = 1 when cancellation makes the expansion unsafe
+//   (2f < 1e-3 ||T||^2 or ||grad|| < 1e-3 ||W Pi||), in which case the residual form is rerun (run_if = flag).
+cudaError_t launch_eval_finalize_pi(const EvalArgs& p, int RP, double* grad, double* part, int nblk,
+                                    cudaStream_t st);
+cudaError_t launch_eval_pi_guard(const EvalArgs& p, const double* grams, const double* part, int nblk, double* f,
+                                 int* flag, cudaStream_t st);
+int eval_pi_blocks(int nsm);
+
 cudaError_t launch_eval(const CUtensorMap* map, const double* T, const EvalArgs& p, int NT, bool tma, int BT,
-                        cudaStream_t st);
+                        cudaStream_t st, bool recon = true);
 cudaError_t launch_eval_finalize(const EvalArgs& p, int RP, double* f, double* grad, int nsm, cudaStream_t st);
 size_t eval_smem_bytes(int NT, int BT);
 

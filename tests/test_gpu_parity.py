@@ -443,3 +443,67 @@ def test_dgn_converges_on_exact_rank_tensor(ctx):
     assert abs(out["rel_err"] - ref["hist"][-1, 1]) <= 1e-6 * ref["hist"][-1, 1] + 1e-12
     f, _ = oracle.cpd_eval(T, to_np(wt), I, J, K, R)
     assert abs(f - out["f"]) <= 1e-6 * f + 1e-24
+
+
+# ------------------------------------------------------------------------- guarded Pi-form evaluation (R31)
+@pytest.mark.parametrize("case", ["c1-true", "c1-perturbed", "c2", "c3-true", "c3-random", "c4", "c5", "sharded",
+                                  "warmup"])
+def test_pi_form_and_residual_form_both_match_oracle(ctx, case, golden_dir):
+    """tf_cpd_eval in the guarded Pi form (default) and the residual form give the oracle's F and grad within the
+    bar; the guard falls back to the residual form exactly where the Gram expansion cancels (near exact fits)
+    and keeps the Pi form elsewhere."""
+    kw = {}
+    if case.startswith("c1"):
+        P = synth.make_problem("c1", "cpu")
+        point = case.split("-")[1]
+    elif case == "c2":
+        P, point = synth.make_problem("c2", "cpu"), "random"
+    elif case.startswith("c3"):
+        P = synth.make_problem("c3", "cpu", dims=(70, 66, 33, 20))
+        point = case.split("-")[1]
+    elif case == "c4":
+        P, point = synth.make_problem("c4", "cpu", dims=(150, 80, 40, 50)), "random_uniform"
+    elif case == "c5":
+        P, point = synth.make_problem("c5", "cpu", dims=(100, 77, 21, 100)), "random"
+    elif case == "sharded":
+        P, point = synth.make_problem("c2", "cpu", dims=(64, 70, 50, 10)), "random"
+    if case == "warmup":
+        g = json.load(open(os.path.join(golden_dir, "warmup.json")))
+        x, y = np.array(g["x"]), np.array(g["y"])
+        z = np.array(g["z_num"], dtype=np.float64) / g["z_den"]
+        X, Y, Z = np.meshgrid(x, y, z, indexing="ij")
+        t = (np.cos(1 - X) * np.sin(1 + Y ** 2) - np.sin(1 + X ** 2) * np.exp(X ** 2 + Y ** 2 + Z ** 2)
+             - np.cos(X) * np.log(1 + Z))
+        T_np = np.ascontiguousarray(t.transpose(2, 1, 0)).reshape(-1)
+        A = np.stack([np.cos(1 - x), -np.sin(1 + x ** 2) * np.exp(x ** 2), -np.cos(x)], axis=1)
+        B = np.stack([np.sin(1 + y ** 2), np.exp(y ** 2), np.ones_like(y)], axis=1)
+        C = np.stack([np.ones_like(z), np.exp(z ** 2), np.log(1 + z)], axis=1)
+        w_np = np.concatenate([A.T.reshape(-1), B.T.reshape(-1), C.T.reshape(-1)])
+        I, J, K, R = 6, 5, 4, 3
+        expect_fallback = 1
+    else:
+        c = P.cfg
+        I, J, K, R = c.I, c.J, c.K, c.R
+        T_np, w_np = to_np(P.T).reshape(-1), to_np(P.w(point))
+        expect_fallback = 1 if point == "true" else 0
+    fr, gr = oracle.cpd_eval(T_np, w_np, I, J, K, R)
+    T_t = torch.from_numpy(T_np).cuda()
+    w_t = torch.from_numpy(w_np).cuda()
+    for form in ("pi", "residual"):
+        ctx.set_eval_form(form)
+        if case == "sharded":
+            f, g = 0.0, np.zeros_like(gr)
+            for k0, k1 in ((0, 17), (17, 40), (40, K)):
+                d = tf.Dims(I, J, k1 - k0, R, K_total=K, k_begin=k0)
+                fp, gp = ctx.tf_cpd_eval(d, T_t.reshape(K, J, I)[k0:k1].contiguous(), w_t)
+                f += fp.item()
+                g += to_np(gp)
+        else:
+            fd, gd = ctx.tf_cpd_eval(tf.Dims(I, J, K, R), T_t, w_t)
+            f, g = fd.item(), to_np(gd)
+        if form == "pi" and case != "sharded":
+            assert ctx.eval_fell_back() == expect_fallback, (case, form)
+        okf, ef, bf = within([f], [fr], f_floor(T_np, fr))
+        okg, eg, bg = within(g, gr, grad_floor(w_np, I, J, K, R))
+        assert okf and okg, (case, form, ef, bf, eg, bg)
+    ctx.set_eval_form("auto")

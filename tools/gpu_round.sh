@@ -21,7 +21,7 @@ for s in $STAGES; do
     full)
       CFG=${NCU_CFG:-c5}
       timeout 600 python tools/quick_time.py $CFG 2 > gpurun_out/qt_$TAG.log 2>&1 && \
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_eval_fused -s 1 -c 1 \
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_eval_fused -s 2 -c 1 \
         -o gpurun_out/prof_${CFG}_$TAG python tools/quick_time.py $CFG 2 > gpurun_out/ncufull_$TAG.log 2>&1
       echo "ncu full rc=$?"; tail -3 gpurun_out/ncufull_$TAG.log ;;
     fullgemm)

@@ -30,6 +30,8 @@ e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / iters
 kms, n, tot = ctx.kernel_stats()
-flops = 6.0 * c.I * c.J * c.K * c.R
-print(f"{name}: eval {ms:.3f} ms/eval, fused kernel {kms/n:.3f} ms, {flops/(kms/n*1e-3)/1e12:.2f} TFLOP/s "
-      f"(6IJKR), {8*c.I*c.J*c.K/(kms/n*1e-3)/1e9:.0f} GB/s of T", flush=True)
+fb = ctx.eval_fell_back()
+form = "residual" if fb != 0 else "pi"
+flops = (6.0 if form == "residual" else 4.0) * c.I * c.J * c.K * c.R
+print(f"{name}: eval {ms:.3f} ms/eval ({form} form), fused kernel {kms/n:.3f} ms, {flops/(kms/n*1e-3)/1e12:.2f} "
+      f"TFLOP/s ({'6' if form == 'residual' else '4'}IJKR), {8*c.I*c.J*c.K/(kms/n*1e-3)/1e9:.0f} GB/s of T", flush=True)
