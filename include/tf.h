@@ -281,6 +281,17 @@ tf_status tf_ctx_set_eval_form(tf_ctx *ctx, int form);
  * residual form (1), did not (0), or no Pi-form evaluation has run (-1). */
 tf_status tf_ctx_eval_fallback(tf_ctx *ctx, int *fell_back);
 
+/* K-sharded dGN loop: every rank holds slices k_begin .. k_begin+K-1 of T (d.K local,
+ * d.K_total global) and the full w; each evaluation's partial [grad | F] and the tensor sums are summed over
+ * the ranks through the caller's all-reduce hook, everything else (Grams, gamma, CG, balancing, damping,
+ * stopping) runs replicated, so every rank returns the same w. The hook is called from the host thread
+ * after the library synchronized its stream, with `buf` = xbuf (device, caller-owned, >= n + 1 doubles,
+ * n = R(I+J+K_total)) holding `count` doubles; it must replace them with their elementwise SUM over the
+ * ranks (e.g. an NCCL all-reduce of the tensor that owns xbuf) before returning 0 (nonzero -> TF_ERR_CUDA). */
+typedef int (*tf_allreduce_fn)(double *buf, int64_t count, void *user);
+tf_status tf_cpd_dgn_sharded(tf_ctx *ctx, tf_dims d, const double *T_local, double *w, const tf_dgn_params *prm,
+                             tf_dgn_result *res, double *hist, tf_allreduce_fn allreduce, void *user, double *xbuf);
+
 /* Instrumentation (bench.py): when enabled, the fused evaluation kernel is
  * bracketed by CUDA events on the ctx stream; tf_ctx_kernel_stats synchronizes
  * and returns the summed device time (ms) and count of the fused-kernel launches

@@ -67,7 +67,10 @@ class TfDgnResult(ctypes.Structure):
 _lib.tf_cpd_dgn.argtypes = [_vp, TfDims, _vp, _vp, ctypes.POINTER(TfDgnParams), ctypes.POINTER(TfDgnResult),
                             ctypes.POINTER(ctypes.c_double)]
 _lib.tf_ctx_set_timing.argtypes = [_vp, ctypes.c_int]
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_int64, ctypes.c_void_p)
 _lib.tf_ctx_set_eval_form.argtypes = [_vp, ctypes.c_int]
+_lib.tf_cpd_dgn_sharded.argtypes = [_vp, TfDims, _vp, _vp, ctypes.POINTER(TfDgnParams), ctypes.POINTER(TfDgnResult),
+                                    ctypes.POINTER(ctypes.c_double), ALLREDUCE_FN, ctypes.c_void_p, _vp]
 _lib.tf_ctx_eval_fallback.argtypes = [_vp, ctypes.POINTER(ctypes.c_int)]
 _i64 = ctypes.c_int64
 _lib.tf_unfolding_grams.argtypes = [_vp, TfDims, _vp, _vp, _vp, _vp]
@@ -104,7 +107,7 @@ EXPORTED = ["tf_ctx_create", "tf_ctx_destroy", "tf_ctx_set_stream", "tf_status_s
             "tf_reg_gamma", "tf_gn_matvec_damped", "tf_cg_solve_damped", "tf_cpd_dgn", "tf_ctx_set_timing",
             "tf_ctx_kernel_stats", "tf_unfolding_grams", "tf_sym_eig_top", "tf_multilinear_core", "tf_compress",
             "tf_energy_init", "tf_uncompress", "tf_cpd", "tf_mttkrp", "tf_als", "tf_ctx_set_eval_form",
-            "tf_ctx_eval_fallback"]
+            "tf_ctx_eval_fallback", "tf_cpd_dgn_sharded"]
 
 TF_OK, TF_ERR_ARG, TF_ERR_ALIGN, TF_ERR_UNSUPPORTED, TF_ERR_CUDA, TF_ERR_NONFINITE, TF_ERR_ALLOC = range(7)
 MAX_R = 128
@@ -456,6 +459,47 @@ class Context:
         self._check(_lib.tf_als(self._h, d.c(), _ptr(T), _ptr(w), int(sweeps),
                                 fh.ctypes.data_as(ctypes.POINTER(ctypes.c_double)) if track_f else None))
         return fh[:3 * sweeps] if track_f else None
+
+    def tf_cpd_dgn_sharded(self, d: Dims, T_local: torch.Tensor, w: torch.Tensor, cg_iters, allreduce,
+                           maxiter: int | None = None, tol: float = 1e-6, mu0: float = 0.0, use_gamma: bool = True,
+                           jacobi: bool = True, balance: bool = True):
+        """The dGN loop on this rank's K-shard (d.K local slices starting at d.k_begin of d.K_total).
+        allreduce(buf) must replace the float64 CUDA tensor `buf` by its elementwise SUM over the ranks, in
+        place (e.g. torch.distributed.all_reduce); it is called with the library's stream synchronized.
+        Returns (result dict, history) like tf_cpd_dgn; w (full, replicated) is updated in place."""
+        import numpy as np
+        ldT = d.ldT or d.I
+        _dev(T_local, "T_local", ldT * d.J * d.K - (ldT - d.I))
+        _dev(w, "w", d.n)
+        cgi = np.ascontiguousarray(np.asarray(cg_iters, dtype=np.int32))
+        m = int(maxiter if maxiter is not None else cgi.size)
+        if cgi.size < m:
+            raise ValueError("cg_iters shorter than maxiter")
+        prm = TfDgnParams(m, float(tol), float(mu0), int(bool(use_gamma)), int(bool(jacobi)), int(bool(balance)),
+                          cgi.ctypes.data_as(ctypes.POINTER(ctypes.c_int)))
+        res = TfDgnResult()
+        hist = np.zeros(5 * max(m, 1))
+        xbuf = torch.empty(d.n + 1, dtype=torch.float64, device=w.device)
+        errors = []
+
+        def hook(buf, count, user):
+            try:
+                view = xbuf[:count]
+                allreduce(view)
+                torch.cuda.current_stream(w.device).synchronize()
+                return 0
+            except Exception as e:   # never raise across the C ABI
+                errors.append(e)
+                return 1
+
+        cb = ALLREDUCE_FN(hook)
+        st = _lib.tf_cpd_dgn_sharded(self._h, d.c(), _ptr(T_local), _ptr(w), ctypes.byref(prm), ctypes.byref(res),
+                                     hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), cb, None, _ptr(xbuf))
+        if errors:
+            raise errors[0]
+        self._check(st)
+        out = {"iters": res.iters, "reason": res.reason, "f": res.f, "rel_err": res.rel_err, "mu": res.mu}
+        return out, hist.reshape(-1, 5)[:res.iters]
 
     def set_eval_form(self, form: str):
         """'auto' (default: the guarded Pi form, 4IJKR flops, when large enough), 'pi' (guarded Pi form at any

@@ -208,7 +208,9 @@ tf_status eval_impl(tf_ctx* c, const tf_dims& d, const double* T, const double* 
   }
   // small problems are launch-bound: the Pi form's extra launches (Grams, guard, conditional fallback) would
   // cost more than the reconstruction flops it saves
-  const bool pi_form = BT == 64 && (c->eval_form == 2 || (c->eval_form == 0 && 6.0 * d.I * d.J * d.K * d.R >= 5e9));
+  const bool pi_form = BT == 64 && !c->force_residual &&
+                       (c->eval_form == 2 || (c->eval_form == 0 && 6.0 * d.I * d.J * d.K * d.R >= 5e9));
+  c->last_eval_pi = pi_form;
   if (!pi_form) {
     TF_CUDA(c, launch_eval(&map, T, p, NT, tma, BT, c->stream));
     if (c->timing) TF_CUDA(c, cudaEventRecord(e1, c->stream));
@@ -569,17 +571,18 @@ tf_status tf_cg_solve_damped(tf_ctx* c, tf_dims d, const double* grams, const do
   return TF_OK;
 }
 
-tf_status tf_cpd_dgn(tf_ctx* c, tf_dims d, const double* T, double* w, const tf_dgn_params* prm, tf_dgn_result* res,
-                     double* hist) {
-  tf_status s = check_dims(c, d);
-  if (s) return s;
-  if (!T || !w || !prm || !res || (prm->maxiter > 0 && !prm->cg_iters)) return set_err(c, TF_ERR_ARG, "null pointer");
-  if (d.K != d.K_total || d.k_begin != 0)
-    return set_err(c, TF_ERR_UNSUPPORTED, "tf_cpd_dgn needs the whole tensor on one device (K == K_total)");
-  if (prm->maxiter < 0) return set_err(c, TF_ERR_ARG, "maxiter < 0");
-  cudaSetDevice(c->device);
+}  // extern "C"
+
+namespace {
+
+// The dGN loop; with an exchange hook (K-sharded ranks) the partial [grad | F] of every evaluation and the
+// tensor sums are summed over the ranks through xbuf, everything else runs replicated (identical inputs,
+// deterministic kernels -> identical trajectories on every rank).
+tf_status dgn_impl(tf_ctx* c, tf_dims d, const double* T, double* w, const tf_dgn_params* prm, tf_dgn_result* res,
+                   double* hist, tf_allreduce_fn xfn, void* xuser, double* xbuf) {
+  tf_status s;
   const int64_t n = d.R * (d.I + d.J + d.K_total), RR = d.R * d.R;
-  if ((s = ensure(c, c->dgnGrad, n * 8))) return s;
+  if ((s = ensure(c, c->dgnGrad, (n + 1) * 8))) return s;
   if ((s = ensure(c, c->dgnX, n * 8))) return s;
   if ((s = ensure(c, c->dgnY, n * 8))) return s;
   if ((s = ensure(c, c->dgnGrams, 3 * RR * 8))) return s;
@@ -597,20 +600,51 @@ tf_status tf_cpd_dgn(tf_ctx* c, tf_dims d, const double* T, double* w, const tf_
   const Modes m = make_modes(d, w);
   if ((s = ensure(c, c->cgState, sizeof(CgState)))) return s;
   TF_CUDA(c, cudaMemsetAsync(c->cgState.p, 0, sizeof(CgState), c->stream));
+  // Once the guarded Pi-form evaluation falls back (the fit has become too close for the Gram expansion),
+  // the remaining iterations evaluate in the residual form directly instead of paying for both passes.
+  int* hflag = reinterpret_cast<int*>(hs + 14);
   auto sync_scalars = [&]() -> tf_status {
     TF_CUDA(c, cudaMemcpyAsync(hs, scal, 12 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     TF_CUDA(c, cudaMemcpyAsync(c->cg_host, c->cgState.p, sizeof(CgState), cudaMemcpyDeviceToHost, c->stream));
+    const bool pi = c->last_eval_pi;
+    if (pi)
+      TF_CUDA(c, cudaMemcpyAsync(hflag, reinterpret_cast<int*>((double*)c->evPart.p + 3 * eval_pi_blocks(c->nsm)),
+                                 sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     TF_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (pi && *hflag == 1) c->force_residual = true;
+    return TF_OK;
+  };
+  struct ResetForce {
+    tf_ctx* c;
+    ~ResetForce() { c->force_residual = false; }
+  } reset_force{c};
+  // exchange: xbuf <- src (cnt doubles), SUM over ranks by the hook, src <- xbuf
+  auto exchange = [&](double* src, int64_t cnt) -> tf_status {
+    if (!xfn) return TF_OK;
+    TF_CUDA(c, cudaMemcpyAsync(xbuf, src, cnt * 8, cudaMemcpyDeviceToDevice, c->stream));
+    TF_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (xfn(xbuf, cnt, xuser) != 0) return set_err(c, TF_ERR_CUDA, "the all-reduce hook reported a failure");
+    TF_CUDA(c, cudaMemcpyAsync(src, xbuf, cnt * 8, cudaMemcpyDeviceToDevice, c->stream));
+    return TF_OK;
+  };
+  // [grad | F] of the local slices -> global (grad is allocated with one spare slot for F)
+  auto eval_global = [&]() -> tf_status {
+    tf_status st;
+    if (!xfn) return eval_impl(c, d, T, w, scal, grad);
+    if ((st = eval_impl(c, d, T, w, grad + n, grad))) return st;
+    if ((st = exchange(grad, n + 1))) return st;
+    TF_CUDA(c, cudaMemcpyAsync(scal, grad + n, 8, cudaMemcpyDeviceToDevice, c->stream));
     return TF_OK;
   };
   // ||T||^2, mean |T|, F and grad at w0
   TF_CUDA(c, launch_tsums(d.I, d.J, d.K, d.ldT, T, part, scal + 1, c->stream));
-  if ((s = eval_impl(c, d, T, w, scal, grad))) return s;
+  if ((s = exchange(scal + 1, 2))) return s;
+  if ((s = eval_global())) return s;
   if ((s = grams_impl(c, d, w, grams))) return s;
   c->total_launches += 2;
   if ((s = sync_scalars())) return s;
   const double normT2 = hs[2], normT = sqrt(normT2);
-  const double N = (double)d.I * d.J * d.K;
+  const double N = (double)d.I * d.J * d.K_total;
   double mu = prm->mu0 > 0 ? prm->mu0 : hs[1] / N;
   double F = hs[0];
   std::vector<double> rel(prm->maxiter + 1);
@@ -641,7 +675,7 @@ tf_status tf_cpd_dgn(tf_ctx* c, tf_dims d, const double* T, double* w, const tf_
       if ((s = grams_impl(c, d, w, grams))) return s;
       TF_CUDA(c, launch_balance(m, grams, w, c->stream));
     }
-    if ((s = eval_impl(c, d, T, w, scal, grad))) return s;               // F, grad at w^(k)
+    if ((s = eval_global())) return s;                                   // F, grad at w^(k)
     if ((s = grams_impl(c, d, w, grams))) return s;
     TF_CUDA(c, launch_dots(n, grad, grad, grad, part, scal + 8, c->stream));   // [11] = ||grad||_inf
     c->total_launches += 12;
@@ -695,6 +729,33 @@ tf_status tf_cpd_dgn(tf_ctx* c, tf_dims d, const double* T, double* w, const tf_
   res->rel_err = normT > 0 ? sqrt(2.0 * F) / normT : 0.0;
   res->mu = mu;
   return TF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+tf_status tf_cpd_dgn(tf_ctx* c, tf_dims d, const double* T, double* w, const tf_dgn_params* prm, tf_dgn_result* res,
+                     double* hist) {
+  tf_status s = check_dims(c, d);
+  if (s) return s;
+  if (!T || !w || !prm || !res || (prm->maxiter > 0 && !prm->cg_iters)) return set_err(c, TF_ERR_ARG, "null pointer");
+  if (d.K != d.K_total || d.k_begin != 0)
+    return set_err(c, TF_ERR_UNSUPPORTED, "tf_cpd_dgn needs the whole tensor (K == K_total); use tf_cpd_dgn_sharded");
+  if (prm->maxiter < 0) return set_err(c, TF_ERR_ARG, "maxiter < 0");
+  cudaSetDevice(c->device);
+  return dgn_impl(c, d, T, w, prm, res, hist, nullptr, nullptr, nullptr);
+}
+
+tf_status tf_cpd_dgn_sharded(tf_ctx* c, tf_dims d, const double* T, double* w, const tf_dgn_params* prm,
+                             tf_dgn_result* res, double* hist, tf_allreduce_fn allreduce, void* user, double* xbuf) {
+  tf_status s = check_dims(c, d);
+  if (s) return s;
+  if (!T || !w || !prm || !res || !allreduce || !xbuf || (prm->maxiter > 0 && !prm->cg_iters))
+    return set_err(c, TF_ERR_ARG, "null pointer");
+  if (prm->maxiter < 0) return set_err(c, TF_ERR_ARG, "maxiter < 0");
+  cudaSetDevice(c->device);
+  return dgn_impl(c, d, T, w, prm, res, hist, allreduce, user, xbuf);
 }
 
 tf_status tf_cg_solve(tf_ctx* c, tf_dims d, const double* grams, const double* w, const double* rhs, double lambda,

@@ -28,7 +28,9 @@ struct tf_ctx {
   DevBuf cpdU, cpdSig, cpdS, cpdW, cpdGrad, cpdScal;   // tf_cpd pipeline
   DevBuf alsKR, alsM, alsSmall, alsF;                 // CP-ALS
   DevBuf evGrams, evPart;                             // Pi-form evaluation: local Grams, guard partials
-  int eval_form = 0;                                  // 0 guarded Pi form, 1 residual form              // compression: Grams, U, core intermediates
+  int eval_form = 0;                                  // 0 auto, 1 residual form, 2 guarded Pi form
+  bool last_eval_pi = false;                          // the last evaluation ran the guarded Pi form
+  bool force_residual = false;                        // dGN loop: the guard fell back, stay residual              // compression: Grams, U, core intermediates
   double* scal_host = nullptr;              // pinned, dGN scalars
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};

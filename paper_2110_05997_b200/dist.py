@@ -77,3 +77,26 @@ class ShardedEvaluator:
         if allreduce and self.world > 1:
             dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group)
         return f, grad
+
+
+def allreduce_hook(group=None):
+    """The SUM all-reduce a K-sharded tf_cpd_dgn_sharded call needs (NCCL over NVLink on GPUs; any
+    torch.distributed backend): replaces `buf` in place by its elementwise sum over the ranks of `group`."""
+    def hook(buf: torch.Tensor):
+        if dist.is_initialized() and dist.get_world_size(group) > 1:
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+    return hook
+
+
+def sharded_dgn(ctx, I: int, J: int, K: int, R: int, T_local: torch.Tensor, w: torch.Tensor, cg_iters,
+                rank: int | None = None, world: int | None = None, group=None, **kw):
+    """Tensor Fox's dGN loop over K-sharded ranks: this rank holds T[:, :, k0:k1] (shard_range) and the full
+    replicated w; returns what Context.tf_cpd_dgn_sharded returns (identical w on every rank)."""
+    from . import Dims
+    if world is None:
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if rank is None:
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+    k0, k1 = shard_range(K, rank, world)
+    d = Dims(I, J, k1 - k0, R, K_total=K, k_begin=k0)
+    return ctx.tf_cpd_dgn_sharded(d, T_local, w, cg_iters, allreduce_hook(group), **kw)

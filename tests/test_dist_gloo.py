@@ -100,3 +100,60 @@ def test_sharded_generation_is_bit_identical():
     part = synth.make_problem("c3", "cpu", dims=(12, 9, 10, 3), k_range=(4, 7))
     assert torch.equal(full.T[4:7], part.T)
     assert torch.equal(full.w("random"), part.w("random"))
+
+
+def _hook_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2110_05997_b200.dist import allreduce_hook
+        import synth
+        # the exchange of the sharded dGN loop: partial [grad | F] of each rank's slices (here: the oracle's
+        # per-shard values packed like the library packs them) summed in place by the hook
+        I, J, K, R = 9, 8, 10, 3
+        from paper_2110_05997_b200.dist import shard_range
+        k0, k1 = shard_range(K, rank, world)
+        P = synth.make_problem("c2", "cpu", dims=(I, J, K, R), k_range=(k0, k1))
+        g = torch.zeros(R * (I + J + K) + 1, dtype=torch.float64)
+        _oracle_eval_fn(type("D", (), dict(I=I, J=J, K=k1 - k0, R=R, K_total=K, k_begin=k0))(), P.T,
+                        P.w("random"), g[-1:], g[:-1])
+        sums = torch.tensor([float(P.T.abs().sum()), float((P.T * P.T).sum())], dtype=torch.float64)
+        hook = allreduce_hook()
+        hook(g)
+        hook(sums)
+        q.put((rank, g.numpy().copy(), sums.numpy().copy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_dgn_exchange_gloo(world):
+    """The all-reduce hook of tf_cpd_dgn_sharded (dist.allreduce_hook) on gloo: the summed partial [grad | F]
+    of the ranks' K-shards is the full evaluation, the summed tensor sums are the full ||T||^2 and sum|t|, and
+    every rank holds the identical buffer (so the replicated CG/damping/stopping run identically)."""
+    pytest.importorskip("paper_2110_05997_b200")
+    import oracle
+    import synth
+    ctxm = mp.get_context("spawn")
+    q = ctxm.Queue()
+    port = _free_port()
+    procs = [ctxm.Process(target=_hook_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    I, J, K, R = 9, 8, 10, 3
+    P = synth.make_problem("c2", "cpu", dims=(I, J, K, R))
+    fr, gr = oracle.cpd_eval(P.T.numpy().reshape(-1), P.w("random").numpy(), I, J, K, R)
+    for _, g, sums in res:
+        np.testing.assert_allclose(g[:-1], gr, rtol=1e-11, atol=1e-12 * np.abs(gr).max())
+        assert abs(g[-1] - fr) <= 1e-12 * fr
+        assert abs(sums[1] - float((P.T * P.T).sum())) <= 1e-12 * sums[1]
+        assert abs(sums[0] - float(P.T.abs().sum())) <= 1e-12 * sums[0]
+    for _, g, sums in res[1:]:
+        assert np.array_equal(g, res[0][1]) and np.array_equal(sums, res[0][2])

@@ -507,3 +507,65 @@ def test_pi_form_and_residual_form_both_match_oracle(ctx, case, golden_dir):
         okg, eg, bg = within(g, gr, grad_floor(w_np, I, J, K, R))
         assert okf and okg, (case, form, ef, bf, eg, bg)
     ctx.set_eval_form("auto")
+
+
+# ------------------------------------------------------------------------- K-sharded dGN loop (hook exchange)
+def test_sharded_dgn_matches_single_device(ctx):
+    """tf_cpd_dgn_sharded on 3 K-shards (3 host threads with their own contexts and streams on this GPU; the
+    all-reduce hook sums the ranks' buffers on the host side, no kernel waits on another) follows the
+    single-device loop: same iterations and stop, F history and final w to rounding (only the reduction
+    order of the partial [grad | F] differs)."""
+    import threading
+    I, J, K, R = 14, 11, 12, 3
+    T, w0 = _exact_plus_noise(I, J, K, R, 7, 1e-2)
+    cgi = synth.cg_budget(30, seed=5)
+    wt = torch.from_numpy(w0.copy()).cuda()
+    ref, href = ctx.tf_cpd_dgn(tf.Dims(I, J, K, R), torch.from_numpy(T).cuda(), wt, cgi, maxiter=30, tol=1e-10)
+    world = 3
+    Tt = torch.from_numpy(T).reshape(K, J, I)
+    bufs = [None] * world
+    outs = [None] * world
+    barrier = threading.Barrier(world)
+    from paper_2110_05997_b200.dist import shard_range
+
+    def run(rank):
+        torch.cuda.set_device(0)
+        stream = torch.cuda.Stream()
+        with torch.cuda.stream(stream):
+            c = tf.Context(0, stream)
+            k0, k1 = shard_range(K, rank, world)
+            Tl = Tt[k0:k1].contiguous().cuda()
+            wl = torch.from_numpy(w0.copy()).cuda()
+            torch.cuda.synchronize()
+
+            def hook(buf):
+                bufs[rank] = buf
+                barrier.wait()
+                if rank == 0:
+                    total = bufs[0].clone()
+                    for r in range(1, world):
+                        total += bufs[r]
+                    torch.cuda.synchronize()
+                    for r in range(world):
+                        bufs[r].copy_(total)
+                    torch.cuda.synchronize()
+                barrier.wait()
+
+            out, hist = c.tf_cpd_dgn_sharded(tf.Dims(I, J, k1 - k0, R, K_total=K, k_begin=k0), Tl, wl, cgi, hook,
+                                             maxiter=30, tol=1e-10)
+            torch.cuda.synchronize()
+            outs[rank] = (out, hist, to_np(wl))
+            c.close()
+
+    ths = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    for r in range(world):
+        out, hist, wr = outs[r]
+        assert out["iters"] == ref["iters"] and out["reason"] == ref["reason"], (out, ref)
+        n0 = min(8, len(hist))
+        assert np.allclose(hist[:n0, 0], href[:n0, 0], rtol=1e-10, atol=0)
+        assert np.array_equal(wr, outs[0][2])                       # every rank holds the same w
+        assert np.linalg.norm(wr - to_np(wt)) <= 1e-6 * np.linalg.norm(to_np(wt))
