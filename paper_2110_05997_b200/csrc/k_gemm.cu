@@ -9,7 +9,7 @@
 // ptr[p + ld*k] (p contiguous), plus a batch stride. Batches are either summed into one C (the
 // unfolding Gram of mode 2, Σ_k T_k^T T_k) or produce one C each.
 //
-// Kernel: BM x BN output tile per CTA (128x{128,112,96,64}, 64x128 or 64x64), 8 warps, warp tile
+// Kernel: BM x BN output tile per CTA (128x{128,112,96,64,32}, 64x128 or 64x64), 8 warps, warp tile
 // 32 x (BN/WN) built from 8x8 DMMA fragments (mma.sync m8n8k4 f64 -> SASS DMMA.8x8x4); k-steps of
 // BK = 32 staged through a 3-deep shared-memory ring by TMA (cp.async.bulk.tensor, complete_tx on an
 // mbarrier; out-of-bounds boxes are zero-filled, which handles every ragged edge), or by 8-byte
@@ -310,6 +310,7 @@ cudaError_t launch_gemm(const CUtensorMap* ma, const CUtensorMap* mb, const Gemm
   if (g.BM == 128 && g.BN == 112) return launch_tma<128, 112>(ma, mb, g, items, tma, st);
   if (g.BM == 128 && g.BN == 96) return launch_tma<128, 96>(ma, mb, g, items, tma, st);
   if (g.BM == 128 && g.BN == 64) return launch_tma<128, 64>(ma, mb, g, items, tma, st);
+  if (g.BM == 128 && g.BN == 32) return launch_tma<128, 32>(ma, mb, g, items, tma, st);
   if (g.BM == 64 && g.BN == 128) return launch_tma<64, 128>(ma, mb, g, items, tma, st);
   return launch_tma<64, 64>(ma, mb, g, items, tma, st);
 }
