@@ -28,6 +28,8 @@ primitive per step — a matmul, `numpy.linalg.eigh` — no blocking or fusion):
   energy_init         the MLSVD-energy initialisation: the R
                       core entries of largest magnitude, S0 = sum_r s_j e ⊗ e ⊗ e
   uncompress          W~_l = U_l W_l
+  st_mlsvd            Alg. ST-MLSVD, the sequentially truncated
+                      variant Tensor Fox can switch to (1439)
 
 Readings (R23-R26):
   R23 sign of each singular vector: the paper fixes none (any sign gives an SVD);
@@ -43,6 +45,9 @@ Readings (R23-R26):
   R26 the truncated SVD computes the singular values P_l = min(I_l, R) only
       (PAPER.md:1424, 2559), so the relative error in Alg. Compression is
       measured against sum_{r<=P_l} sigma_r^2 (as printed, 2561).
+  R32 ST-MLSVD's truncation: the paper gives no rank rule for it; each step
+      applies Alg. Compression's rule (tail < mlsvd_tol / L) to that step's
+      singular values.
 
 Pins: tests/test_mlsvd_pins.py (Table 4.5 to its 8 printed digits, the printed
 core magnitudes 2934-2952, the 0.0153 initial error 3030, the 3.85e-14 truncation
@@ -208,3 +213,31 @@ def normalize_cpd(Ws):
         lam = lam * nrm
         out.append(np.where(nrm > 0, W / np.where(nrm > 0, nrm, 1.0), W))
     return out, lam
+
+
+def st_mlsvd(T_flat, I, J, K, R: int, mlsvd_tol: float):
+    """Alg. ST-MLSVD: S^(0) = T; for l = 1, 2, 3 the SVD of the current unfolding
+    S^(l-1)_(l) (through its Gram, truncated to P_l = min(I_l, R) singular values), the rank R~_l by the rule of
+    Alg. Compression applied to that step's singular values (reading R32), and S^(l) = the mode-l product of
+    S^(l-1) with U~_l^T (i.e. S^(l)_(l) = Sigma~ V~^T). Returns dict(U=[U~_l], Ufull=[U_l (P_l cols)],
+    sigma=[sigma_l], ranks, S=S^(3))."""
+    S = _t(T_flat, I, J, K)
+    Us, Ufull, sig, ranks = [], [], [], []
+    for mode in (1, 2, 3):
+        n = S.shape[mode - 1]
+        P = min(n, R)
+        X = jac.unfold(S, mode)
+        U, s, _ = mode_svd(X @ X.T, P)
+        r = truncation_ranks([s], mlsvd_tol * 3)[0]   # the per-mode rule: tail < mlsvd_tol / L, L = 3
+        Ut = U[:, :r]
+        if mode == 1:
+            S = np.einsum("ia,ijk->ajk", Ut, S)
+        elif mode == 2:
+            S = np.einsum("jb,ajk->abk", Ut, S)
+        else:
+            S = np.einsum("kc,abk->abc", Ut, S)
+        Us.append(Ut)
+        Ufull.append(U)
+        sig.append(s)
+        ranks.append(r)
+    return {"U": Us, "Ufull": Ufull, "sigma": sig, "ranks": tuple(ranks), "S": S}

@@ -124,3 +124,36 @@ def test_c5_full_size_mttkrp_sampled(ctx):
         S = Pb.T[k].cpu().numpy().T                   # S[i, j]
         ref = np.einsum("ij,ir,jr->r", S, A, B)
         assert np.linalg.norm(Ms[2][k] - ref) <= 1e-12 * np.linalg.norm(ref) * math.sqrt(I * J)
+
+
+def test_argument_errors_new_calls(ctx):
+    """The compression / ALS / sharded-dGN calls return their documented status codes (no exceptions or exits
+    across the ABI)."""
+    T = torch.zeros(4 * 5 * 6, dtype=torch.float64, device="cuda")
+    w = torch.zeros(3 * 15, dtype=torch.float64, device="cuda")
+    with pytest.raises(tf.TfError) as ei:
+        ctx.tf_mttkrp(tf.Dims(4, 5, 6, 3), T, w, 4)
+    assert ei.value.status == tf.TF_ERR_ARG
+    with pytest.raises(tf.TfError) as ei:   # compression needs the whole tensor
+        ctx.tf_unfolding_grams(tf.Dims(4, 5, 3, 1, K_total=6, k_begin=3), T[:60].contiguous())
+    assert ei.value.status == tf.TF_ERR_UNSUPPORTED
+    with pytest.raises(tf.TfError) as ei:
+        ctx.tf_sym_eig_top(4, torch.eye(4, dtype=torch.float64, device="cuda").reshape(-1), 5,
+                           torch.zeros(20, dtype=torch.float64, device="cuda"))
+    assert ei.value.status == tf.TF_ERR_ARG
+    with pytest.raises(tf.TfError) as ei:   # tf_als on a shard
+        ctx.tf_als(tf.Dims(4, 5, 3, 3, K_total=6, k_begin=0), T, w, 1)
+    assert ei.value.status == tf.TF_ERR_UNSUPPORTED
+    with pytest.raises(tf.TfError) as ei:   # energy init with more terms than core entries
+        ctx.tf_energy_init(1, 1, 2, torch.ones(2, dtype=torch.float64, device="cuda"), 3)
+    assert ei.value.status == tf.TF_ERR_ARG
+    with pytest.raises(tf.TfError) as ei:
+        ctx.set_eval_form("pi")
+        ctx.tf_compress(tf.Dims(4, 5, 6, 3), T, torch.zeros(45, dtype=torch.float64, device="cuda"), mlsvd_tol=0.0)
+    assert ei.value.status == tf.TF_ERR_ARG
+    ctx.set_eval_form("auto")
+    # a failing all-reduce hook surfaces as an exception, not a crash
+    def bad(buf):
+        raise RuntimeError("hook failed")
+    with pytest.raises(RuntimeError):
+        ctx.tf_cpd_dgn_sharded(tf.Dims(4, 5, 6, 3), T + 1.0, w + 0.5, [2] * 3, bad, maxiter=3)

@@ -216,3 +216,37 @@ def test_normalize_cpd_output_form():
     assert lam[2] == 0.0 and np.allclose(np.linalg.norm(c[:, [0, 1, 3]], axis=0), 1.0)
     assert np.allclose(lam[[0, 1, 3]], [np.linalg.norm(A[:, r]) * np.linalg.norm(B[:, r]) * np.linalg.norm(C[:, r])
                                        for r in (0, 1, 3)])
+
+
+def test_st_mlsvd_error_identity_and_special_cases(golden_dir):
+    """Alg. ST-MLSVD. (i) Its first step is the classic mode-1 SVD. (ii) Without
+    truncation it is exact: T = (U1, U2, U3)·S. (iii) The ST-HOSVD error identity (the projections are
+    orthogonal and nested): ||T - T~||^2 = sum over steps of the discarded squared singular values of that
+    step. (iv) On an exactly multilinear-rank-(2,3,4) tensor it recovers the ranks with ~0 error, and on the
+    warming-up tensor it gives the 3x3x3 core of the classic MLSVD up to signs (no truncation happens)."""
+    I, J, K = 8, 7, 6
+    A, B, C = (RNG.standard_normal((n, 3)) for n in (I, J, K))
+    t = np.einsum("ir,jr,kr->ijk", A, B, C) + 0.05 * RNG.standard_normal((I, J, K))
+    T = jac.storage_from_tensor(t)
+    st = M.st_mlsvd(T, I, J, K, 100, 1e-3)
+    cl = M.mlsvd(T, I, J, K, 100)
+    assert np.allclose(st["sigma"][0], cl["sigma"][0], rtol=1e-12)
+    rec = np.einsum("ia,jb,kc,abc->ijk", *st["U"], st["S"])
+    lhs = np.linalg.norm(t - rec) ** 2
+    rhs = sum(np.sum(st["sigma"][l][st["ranks"][l]:] ** 2) for l in range(3))
+    assert abs(lhs - rhs) <= 1e-10 * np.sum(t * t), (lhs, rhs)
+    assert max(st["ranks"]) < 6            # something was truncated (the identity is not vacuous)
+    full = M.st_mlsvd(T, I, J, K, 100, 1e-300)
+    assert full["ranks"] == (I, J, K)
+    assert np.allclose(np.einsum("ia,jb,kc,abc->ijk", *full["U"], full["S"]), t, atol=1e-12)
+    G = RNG.standard_normal((2, 3, 4))
+    M1, M2, M3 = (RNG.standard_normal((n, r)) for n, r in ((I, 2), (J, 3), (K, 4)))
+    t2 = np.einsum("ia,jb,kc,abc->ijk", M1, M2, M3, G)
+    s2 = M.st_mlsvd(jac.storage_from_tensor(t2), I, J, K, 6, 1e-10)
+    assert s2["ranks"] == (2, 3, 4)
+    assert np.linalg.norm(np.einsum("ia,jb,kc,abc->ijk", *s2["U"], s2["S"]) - t2) <= 1e-12 * np.linalg.norm(t2)
+    _, Tw = warmup_T(golden_dir)
+    sw = M.st_mlsvd(Tw, 6, 5, 4, 3, 1e-6)
+    cw = M.mlsvd(Tw, 6, 5, 4, 3)
+    assert sw["ranks"] == (3, 3, 3)
+    assert np.allclose(np.abs(sw["S"]), np.abs(cw["S"]), atol=1e-10)
