@@ -215,6 +215,16 @@ tf_status tf_compress(tf_ctx *ctx, tf_dims d, const double *T, const double *Ome
                       int eig_maxiter, double eig_tol, double *U, double *sigma, double *S, int64_t *ranks,
                       int *eig_iters);
 
+/* Alg. ST-MLSVD, the sequentially truncated variant Tensor Fox can switch to (1439):
+ * mode 1's SVD from T_(1) T_(1)^T, then X1 = U~1^T T_(1); mode 2's from the Gram of X1's mode-2 unfolding,
+ * X2 = X1 x_2 U~2^T; mode 3's from X2's, S = X2 x_3 U~3^T. Each step's rank follows Alg. Compression's rule
+ * on that step's singular values (reading R32). Same arguments and layouts as tf_compress (sigma holds each
+ * step's singular values; U_l all P_l columns). Cheaper than tf_compress: after mode 1 every pass reads the
+ * R~1 x J x K intermediate instead of T. */
+tf_status tf_compress_st(tf_ctx *ctx, tf_dims d, const double *T, const double *Omega, double mlsvd_tol,
+                         int eig_maxiter, double eig_tol, double *U, double *sigma, double *S, int64_t *ranks,
+                         int *eig_iters);
+
 /* MLSVD-energy initialisation on the core S (R1 x R2 x R3): w = [vec W1; vec W2; vec W3] (R*(R1+R2+R3))
  * with W1[:, r] = s_j e_{j1}, W2[:, r] = e_{j2}, W3[:, r] = e_{j3} for the R entries j of largest |s|. */
 tf_status tf_energy_init(tf_ctx *ctx, int64_t R1, int64_t R2, int64_t R3, const double *S, int64_t R, double *w);

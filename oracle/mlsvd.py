@@ -228,7 +228,7 @@ def st_mlsvd(T_flat, I, J, K, R: int, mlsvd_tol: float):
         P = min(n, R)
         X = jac.unfold(S, mode)
         U, s, _ = mode_svd(X @ X.T, P)
-        r = truncation_ranks([s], mlsvd_tol * 3)[0]   # the per-mode rule: tail < mlsvd_tol / L, L = 3
+        r = truncation_ranks([s], mlsvd_tol / 3)[0]   # the per-mode rule: tail < mlsvd_tol / L, L = 3
         Ut = U[:, :r]
         if mode == 1:
             S = np.einsum("ia,ijk->ajk", Ut, S)

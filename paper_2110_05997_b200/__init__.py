@@ -79,6 +79,8 @@ _lib.tf_sym_eig_top.argtypes = [_vp, _i64, _vp, _i64, _vp, ctypes.c_int, ctypes.
 _lib.tf_multilinear_core.argtypes = [_vp, TfDims, _vp, _vp, _i64, _vp, _i64, _vp, _i64, _vp]
 _lib.tf_compress.argtypes = [_vp, TfDims, _vp, _vp, ctypes.c_double, ctypes.c_int, ctypes.c_double, _vp, _vp, _vp,
                              ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_int)]
+_lib.tf_compress_st.argtypes = [_vp, TfDims, _vp, _vp, ctypes.c_double, ctypes.c_int, ctypes.c_double, _vp, _vp,
+                                _vp, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_int)]
 _lib.tf_energy_init.argtypes = [_vp, _i64, _i64, _i64, _vp, _i64, _vp]
 _lib.tf_uncompress.argtypes = [_vp, _i64, _i64, _vp, _vp, _i64, _vp]
 
@@ -107,7 +109,7 @@ EXPORTED = ["tf_ctx_create", "tf_ctx_destroy", "tf_ctx_set_stream", "tf_status_s
             "tf_reg_gamma", "tf_gn_matvec_damped", "tf_cg_solve_damped", "tf_cpd_dgn", "tf_ctx_set_timing",
             "tf_ctx_kernel_stats", "tf_unfolding_grams", "tf_sym_eig_top", "tf_multilinear_core", "tf_compress",
             "tf_energy_init", "tf_uncompress", "tf_cpd", "tf_mttkrp", "tf_als", "tf_ctx_set_eval_form",
-            "tf_ctx_eval_fallback", "tf_cpd_dgn_sharded"]
+            "tf_ctx_eval_fallback", "tf_cpd_dgn_sharded", "tf_compress_st"]
 
 TF_OK, TF_ERR_ARG, TF_ERR_ALIGN, TF_ERR_UNSUPPORTED, TF_ERR_CUDA, TF_ERR_NONFINITE, TF_ERR_ALLOC = range(7)
 MAX_R = 128
@@ -343,8 +345,9 @@ class Context:
         return S
 
     def tf_compress(self, d: Dims, T: torch.Tensor, Omega: torch.Tensor, mlsvd_tol: float = 1e-6,
-                    eig_maxiter: int = 100, eig_tol: float = 0.0):
-        """Alg. Compression. Returns dict(U=[U1, U2, U3] (I_l x P_l, column-major flat), sigma=[...],
+                    eig_maxiter: int = 100, eig_tol: float = 0.0, sequential: bool = False):
+        """Alg. Compression (sequential=True: Alg. ST-MLSVD). Returns dict(U=[U1, U2, U3] (I_l x P_l,
+        column-major flat), sigma=[...],
         S=core (R~1*R~2*R~3,), ranks=(R~1, R~2, R~3), P=(P1, P2, P3), eig_iters=[...])."""
         ldT = d.ldT or d.I
         _dev(T, "T", ldT * d.J * d.K - (ldT - d.I))
@@ -357,14 +360,20 @@ class Context:
         S = torch.empty(P[0] * P[1] * P[2], dtype=torch.float64, device=T.device)
         ranks = (ctypes.c_int64 * 3)()
         iters = (ctypes.c_int * 3)()
-        self._check(_lib.tf_compress(self._h, d.c(), _ptr(T), _ptr(Omega), float(mlsvd_tol), int(eig_maxiter),
-                                     float(eig_tol), _ptr(U), _ptr(sigma), _ptr(S), ranks, iters))
+        fn = _lib.tf_compress_st if sequential else _lib.tf_compress
+        self._check(fn(self._h, d.c(), _ptr(T), _ptr(Omega), float(mlsvd_tol), int(eig_maxiter),
+                       float(eig_tol), _ptr(U), _ptr(sigma), _ptr(S), ranks, iters))
         rk = tuple(int(r) for r in ranks)
         offs = [0, dims[0] * P[0], dims[0] * P[0] + dims[1] * P[1]]
         soffs = [0, P[0], P[0] + P[1]]
         return {"U": [U[offs[l]:offs[l] + dims[l] * P[l]] for l in range(3)],
                 "sigma": [sigma[soffs[l]:soffs[l] + P[l]] for l in range(3)],
                 "S": S[:rk[0] * rk[1] * rk[2]], "ranks": rk, "P": P, "eig_iters": [int(i) for i in iters]}
+
+    def tf_compress_st(self, d: Dims, T: torch.Tensor, Omega: torch.Tensor, mlsvd_tol: float = 1e-6,
+                       eig_maxiter: int = 100, eig_tol: float = 0.0):
+        """Alg. ST-MLSVD (the sequentially truncated compression); same outputs as tf_compress."""
+        return self.tf_compress(d, T, Omega, mlsvd_tol, eig_maxiter, eig_tol, sequential=True)
 
     def tf_energy_init(self, R1: int, R2: int, R3: int, S: torch.Tensor, R: int) -> torch.Tensor:
         """Packed w = [vec W1; vec W2; vec W3] of the MLSVD-energy initialisation on the core S."""
@@ -442,7 +451,7 @@ class Context:
         ldT = d.ldT or d.I
         _dev(T, "T", ldT * d.J * d.K - (ldT - d.I))
         _dev(w, "w", d.n)
-        rows = (d.I, d.J, d.K)[mode - 1]
+        rows = (d.I, d.J, d.K)[mode - 1] if mode in (1, 2, 3) else 1   # a bad mode is the library's TF_ERR_ARG
         if M is None:
             M = torch.empty(rows * d.R, dtype=torch.float64, device=T.device)
         _dev(M, "M", rows * d.R)

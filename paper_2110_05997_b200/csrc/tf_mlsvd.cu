@@ -389,6 +389,87 @@ tf_status tf_compress(tf_ctx* c, tf_dims d, const double* T, const double* Omega
   return core_impl(c, d, T, U + off[0], ranks[0], U + off[1], ranks[1], U + off[2], ranks[2], S);
 }
 
+tf_status tf_compress_st(tf_ctx* c, tf_dims d, const double* T, const double* Omega, double mlsvd_tol,
+                         int eig_maxiter, double eig_tol, double* U, double* sigma, double* S, int64_t* ranks,
+                         int* eig_iters) {
+  tf_status s = check_whole(c, d);
+  if (s) return s;
+  if (!T || !Omega || !U || !sigma || !S || !ranks) return set_err(c, TF_ERR_ARG, "null pointer");
+  if (d.R < 1) return set_err(c, TF_ERR_ARG, "R < 1");
+  if (!(mlsvd_tol > 0.0)) return set_err(c, TF_ERR_ARG, "mlsvd_tol must be > 0");
+  if (eig_maxiter < 1) return set_err(c, TF_ERR_ARG, "eig_maxiter < 1");
+  cudaSetDevice(c->device);
+  const int64_t I = d.I, J = d.J, K = d.K, ld = d.ldT;
+  const int64_t dims[3] = {I, J, K};
+  int64_t P[3], off[3], soff[3];
+  int64_t o = 0, so = 0;
+  for (int l = 0; l < 3; ++l) {
+    P[l] = std::min<int64_t>(dims[l], d.R);
+    if (P[l] > TF_MAX_R) return set_err(c, TF_ERR_UNSUPPORTED, "min(I_l, R) > TF_MAX_R");
+    off[l] = o;
+    soff[l] = so;
+    o += dims[l] * P[l];
+    so += P[l];
+  }
+  const int64_t nmax = std::max(I, std::max(J, K));
+  if ((s = ensure(c, c->mlG, (size_t)nmax * nmax * 8))) return s;
+  if ((s = ensure(c, c->mlLam, (size_t)TF_MAX_R * 8))) return s;
+  if ((s = ensure(c, c->mlRanks, 3 * sizeof(int64_t)))) return s;
+  double* G = (double*)c->mlG.p;
+  double* lam = (double*)c->mlLam.p;
+  int64_t* rk = (int64_t*)c->mlRanks.p;
+  // one mode: eigenpairs of the Gram in G, sigma, the Alg. Compression rank (synchronizes for it)
+  auto mode_step = [&](int l) -> tf_status {
+    tf_status st;
+    int it = 0;
+    if ((st = eig_top_impl(c, dims[l], G, (int)P[l], Omega + off[l], eig_maxiter, eig_tol, U + off[l], lam, &it)))
+      return st;
+    if (eig_iters) eig_iters[l] = it;
+    TF_CUDA(c, launch_sqrt_abs(P[l], lam, sigma + soff[l], c->stream));
+    TF_CUDA(c, launch_trunc_rank((int)P[l], sigma + soff[l], mlsvd_tol / 3.0, rk + l, c->stream));
+    TF_CUDA(c, cudaMemcpyAsync(ranks + l, rk + l, sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    TF_CUDA(c, cudaStreamSynchronize(c->stream));
+    c->total_launches += 2;
+    return TF_OK;
+  };
+  // step 1: T_(1) T_(1)^T, U1, then X1 = U~1^T T_(1)  (r1 x J x K, leading dimension r1e)
+  if ((s = grams_mode(c, d, T, 1, G))) return s;
+  if ((s = mode_step(0))) return s;
+  const int64_t r1 = ranks[0], r1e = even(r1);
+  if ((s = ensure(c, c->mlX, (size_t)r1e * J * K * 8))) return s;
+  double* X1 = (double*)c->mlX.p;
+  if ((s = gemm_run(c, gemm_args(opnd(U + off[0], I, true), opnd(T, ld, true), r1, J * K, I, X1, r1e)))) return s;
+  // step 2: Gram of the mode-2 unfolding of X1 (sum over slices of X1_k^T X1_k), U2, X2_k = X1_k U~2
+  {
+    GemmOperand a = opnd(X1, r1e, true, r1e * J);
+    GemmArgs g = gemm_args(a, a, J, J, r1, G, J);
+    g.batch = K;
+    g.sym = true;
+    if ((s = gemm_run(c, g))) return s;
+  }
+  if ((s = mode_step(1))) return s;
+  const int64_t r2 = ranks[1];
+  if ((s = ensure(c, c->mlY, (size_t)r1 * r2 * K * 8))) return s;
+  double* X2 = (double*)c->mlY.p;
+  {
+    GemmArgs g = gemm_args(opnd(X1, r1e, false, r1e * J), opnd(U + off[1], J, true), r1, r2, J, X2, r1);
+    g.batch = K;
+    g.sum_batch = false;
+    g.cstride = r1 * r2;
+    if ((s = gemm_run(c, g))) return s;
+  }
+  // step 3: Gram of X2 as (r1 r2) x K, U3, S = X2 x_3 U~3^T
+  {
+    GemmOperand a = opnd(X2, r1 * r2, true);
+    GemmArgs g = gemm_args(a, a, K, K, r1 * r2, G, K);
+    g.sym = true;
+    if ((s = gemm_run(c, g))) return s;
+  }
+  if ((s = mode_step(2))) return s;
+  const int64_t r3 = ranks[2];
+  return gemm_run(c, gemm_args(opnd(X2, r1 * r2, false), opnd(U + off[2], K, true), r1 * r2, r3, K, S, r1 * r2));
+}
+
 tf_status tf_energy_init(tf_ctx* c, int64_t R1, int64_t R2, int64_t R3, const double* S, int64_t R, double* w) {
   if (!c) return TF_ERR_ARG;
   if (R1 < 1 || R2 < 1 || R3 < 1 || R < 1 || !S || !w) return set_err(c, TF_ERR_ARG, "tf_energy_init: bad argument");
