@@ -247,6 +247,7 @@ typedef struct {
   int eig_maxiter;        /* subspace-iteration cap per mode */
   int init;               /* 1: MLSVD-energy initialisation; 0: w0_core */
   tf_dgn_params dgn;      /* the dGN loop on the core */
+  int sequential;         /* 1: compress by Alg. ST-MLSVD (tf_compress_st) instead of the classic MLSVD */
 } tf_cpd_params;
 
 typedef struct {

@@ -91,7 +91,7 @@ _lib.tf_als.argtypes = [_vp, TfDims, _vp, _vp, ctypes.c_int, ctypes.POINTER(ctyp
 
 class TfCpdParams(ctypes.Structure):
     _fields_ = [("mlsvd_tol", ctypes.c_double), ("eig_maxiter", ctypes.c_int), ("init", ctypes.c_int),
-                ("dgn", TfDgnParams)]
+                ("dgn", TfDgnParams), ("sequential", ctypes.c_int)]
 
 
 class TfCpdResult(ctypes.Structure):
@@ -415,8 +415,9 @@ class Context:
 
     def tf_cpd(self, d: Dims, T: torch.Tensor, Omega: torch.Tensor, cg_iters, w0_core: torch.Tensor | None = None,
                mlsvd_tol: float = 1e-6, eig_maxiter: int = 100, maxiter: int | None = None, tol: float = 1e-6,
-               mu0: float = 0.0, use_gamma: bool = True, jacobi: bool = True, balance: bool = True):
-        """The whole Tensor Fox flow: compression, initialisation (MLSVD energy when w0_core is None, else
+               mu0: float = 0.0, use_gamma: bool = True, jacobi: bool = True, balance: bool = True,
+               sequential: bool = False):
+        """The whole Tensor Fox flow: compression (sequential=True: Alg. ST-MLSVD), initialisation (MLSVD energy when w0_core is None, else
         the given [W1 | W2 | W3] random start on the P_l-row blocks), dGN on the core, uncompression and the
         unit-column output. Returns (W (n,), lambda (R,), result dict, dGN history on the core)."""
         import numpy as np
@@ -433,7 +434,7 @@ class Context:
             raise ValueError("cg_iters shorter than maxiter")
         dp = TfDgnParams(m, float(tol), float(mu0), int(bool(use_gamma)), int(bool(jacobi)), int(bool(balance)),
                          cgi.ctypes.data_as(ctypes.POINTER(ctypes.c_int)))
-        prm = TfCpdParams(float(mlsvd_tol), int(eig_maxiter), 0 if w0_core is not None else 1, dp)
+        prm = TfCpdParams(float(mlsvd_tol), int(eig_maxiter), 0 if w0_core is not None else 1, dp, int(bool(sequential)))
         res = TfCpdResult()
         W = torch.empty(d.R * sum(dims), dtype=torch.float64, device=T.device)
         lam = torch.empty(d.R, dtype=torch.float64, device=T.device)

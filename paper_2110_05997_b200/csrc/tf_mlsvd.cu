@@ -515,8 +515,8 @@ tf_status tf_cpd(tf_ctx* c, tf_dims d, const double* T, const double* Omega, con
   double* wc = (double*)c->cpdW.p;
   // 1. compression
   int64_t rk[3];
-  if ((s = tf_compress(c, d, T, Omega, prm->mlsvd_tol, prm->eig_maxiter, 0.0, U, (double*)c->cpdSig.p, S, rk,
-                       res->eig_iters)))
+  if ((s = (prm->sequential ? tf_compress_st : tf_compress)(c, d, T, Omega, prm->mlsvd_tol, prm->eig_maxiter, 0.0, U,
+                                                            (double*)c->cpdSig.p, S, rk, res->eig_iters)))
     return s;
   for (int l = 0; l < 3; ++l) res->ranks[l] = rk[l];
   // 2. initialisation on the core

@@ -362,3 +362,22 @@ def test_compress_st_matches_oracle(ctx, name, dims, tol, golden_dir):
     r1, r2, r3 = ref["ranks"]
     S = to_np(out["S"]).reshape(r3, r2, r1).transpose(2, 1, 0)
     assert np.linalg.norm(S - ref["S"]) / np.linalg.norm(T) <= 1e-9
+
+
+def test_tf_cpd_sequential_compression(ctx):
+    """The flow with ST-MLSVD compression on an exact-rank tensor (no truncation loss): converges to a fit below
+    1e-6 and the unit-column output reproduces T to that fit."""
+    I, J, K, R = 40, 30, 20, 3
+    A, B, C = (synth.randn((n, R), torch.device("cpu"), "cpd-st", n).numpy() for n in (I, J, K))
+    t = np.einsum("ir,jr,kr->ijk", A, B, C)
+    T = jac.storage_from_tensor(t)
+    cgi = synth.cg_budget(200, seed=3)
+    Om = synth.omega_blocks((I, J, K), R, "cpu")
+    W, lam, out, hist = ctx.tf_cpd(tf.Dims(I, J, K, R), torch.from_numpy(T).cuda(), Om.cuda(), cgi, tol=1e-12,
+                                   sequential=True)
+    assert out["ranks"] == (3, 3, 3)
+    assert out["rel_err"] < 1e-6, out
+    Wn = to_np(W)
+    a, b, c = (Wn[:I * R].reshape(R, I).T, Wn[I * R:(I + J) * R].reshape(R, J).T, Wn[(I + J) * R:].reshape(R, K).T)
+    rec = np.einsum("r,ir,jr,kr->ijk", to_np(lam), a, b, c)
+    assert abs(np.linalg.norm(t - rec) / np.linalg.norm(t) - out["rel_err"]) <= 1e-2 * out["rel_err"] + 1e-14
