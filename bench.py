@@ -362,7 +362,27 @@ def run_ours(args):
         torch.cuda.synchronize(dev)
         comp_ms = s0.elapsed_time(s1) / reps
         gram_flops = sum((nl + 1) for nl in (I, J, K)) * float(I) * J * K   # symmetric T_(l) T_(l)^T, algorithmic
-        stages = {"compress": {"ms": comp_ms, "ranks": list(comp["ranks"]), "eig_iters": comp["eig_iters"],
+        # one Gauss-Newton matvec (Thm Hv) and the CG of the step, timed alone
+        vv = rhs.clone()
+        yy = torch.empty_like(vv)
+        ctx.tf_gn_matvec(dglob, grams, w, vv, cfg.lam, yy)
+        torch.cuda.synchronize(dev)
+        s0.record(stream)
+        for _ in range(10):
+            ctx.tf_gn_matvec(dglob, grams, w, vv, cfg.lam, yy)
+        s1.record(stream)
+        torch.cuda.synchronize(dev)
+        mv_us = s0.elapsed_time(s1) * 100.0
+        s0.record(stream)
+        ctx.tf_cg_solve(dglob, grams, w, rhs, cfg.lam, cfg.cg_iters, 0.0, False, x)
+        s1.record(stream)
+        torch.cuda.synchronize(dev)
+        cg_ms = s0.elapsed_time(s1)
+        stages = {"gn_matvec": {"us": mv_us, "cg_ms": cg_ms, "cg_iters": cfg.cg_iters,
+                                "flops": (6 + 5 * (I + J + K)) * R * R,
+                                "what": "tf_gn_matvec (Thm Hv, PAPER.md:2352-2370, one persistent launch) and "
+                                        "tf_cg_solve(cg_iters) alone; latency-bound (O(R^2 sum I) work)"},
+                  "compress": {"ms": comp_ms, "ranks": list(comp["ranks"]), "eig_iters": comp["eig_iters"],
                                "unfolding_grams_ms": gram_ms,
                                "unfolding_grams_tflops": gram_flops / (gram_ms * 1e-3) / 1e12,
                                "unfolding_grams_frac": gram_flops / (gram_ms * 1e-3) / 1e12 / peak_tf,
