@@ -218,11 +218,15 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
   // Unscaled A, distributed over the CTA: thread (warp, g, q) owns A[8*warp + 2q + e][8t + g] (its
   // phase-2 P^T fragment positions); used for dF/dC and to rebuild sAc = -A diag(c_k) each slice.
   // Read from the staged tile; the first rebuild overwrites exactly these positions (same thread).
+  // (the Pi form keeps sAc = A unscaled for the whole CTA: phase 3 scales its per-slice product instead, so
+  // neither Areg nor the per-slice rebuild and its hand-off exist there)
   double Areg[NT][2];
+  if constexpr (RECON) {
 #pragma unroll
-  for (int t = 0; t < NT; ++t)
+    for (int t = 0; t < NT; ++t)
 #pragma unroll
-    for (int e = 0; e < 2; ++e) Areg[t][e] = sAc[(8 * warp + 2 * q + e) * LDF + 8 * t + g];
+      for (int e = 0; e < 2; ++e) Areg[t][e] = sAc[(8 * warp + 2 * q + e) * LDF + 8 * t + g];
+  }
   auto rebuild_sAc = [&](const double* c) {
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
@@ -234,7 +238,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
   if (nk > 0) {
     for (int u = 0; u < 2 && u < nk; ++u) load_c(kA + u, u);
     __syncthreads();
-    rebuild_sAc(sC);
+    if constexpr (RECON) rebuild_sAc(sC);
   }
   __syncthreads();
 
@@ -253,7 +257,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
     const double* sc = sC + (kk & 3) * RP;
     TL(kk, 0);
     if (kTMA) mbar_wait(&full[b], (kk >> 1) & 1);
-    if (kk > 0) mbar_wait(aready, (kk - 1) & 1);
+    if (RECON && kk > 0) mbar_wait(aready, (kk - 1) & 1);
     TL(kk, 1);
 
     // ---- phase 1: E = T + (-A diag(c)) B^T on a (BT/2) x 16 warp tile (MF x 2 fragments)
@@ -316,7 +320,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
     if (kk + 2 < nk) load_c(k + 2, (kk + 2) & 3);
 
     // ---- phase 3: accB^T += (-A diag c)^T E for j-cols 8*warp.., all R (prescaled sAc: no DMUL)
-    {
+    if constexpr (RECON) {
       const double* pe = sT + (8 * warp + g) * kLDE + q;
       const double* pa = sAc + q * LDF + g;
 #pragma unroll 4
@@ -325,9 +329,28 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
 #pragma unroll
         for (int t = 0; t < NT; ++t) dmma(accB[t], pa[4 * s * LDF + 8 * t], bb);
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p3done);
+    } else {
+      // Pi form: Q = A^T T_k (unscaled A, fresh per slice), then accB^T -= diag(c_k) Q (one DFMA per entry)
+      double Qt[NT][2];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) Qt[t][0] = Qt[t][1] = 0.0;
+      const double* pe = sT + (8 * warp + g) * kLDE + q;
+      const double* pa = sAc + q * LDF + g;
+#pragma unroll 4
+      for (int s = 0; s < kBI / 4; ++s) {
+        const double bb = pe[4 * s];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) dmma(Qt[t], pa[4 * s * LDF + 8 * t], bb);
+      }
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const double cr = -sc[8 * t + g];   // accB[t][e] is (r = 8t+g, j = 8w+2q+e)
+        accB[t][0] = fma(cr, Qt[t][0], accB[t][0]);
+        accB[t][1] = fma(cr, Qt[t][1], accB[t][1]);
+      }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(p3done);
     TL(kk, 4);
 
     // ---- phase 2: P^T_t = B_t^T E^T for i-cols 8*warp.. (t outer, E fragments in registers);
@@ -348,7 +371,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
       for (int j = NT; j < NV; ++j) gcv[j] = 0.0;
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
-        if (t == NT1 && kk + 1 < nk) {
+        if (RECON && t == NT1 && kk + 1 < nk) {
           TL(kk, 5);
           mbar_wait(p3done, kk & 1);          // every warp is done reading sAc_k
           TL(kk, 6);
@@ -367,9 +390,14 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
         const double P0 = p0[0] + p1[0], P1 = p0[1] + p1[1];   // P[i = 8w+2q+e][r = 8t+g]
         accA[t][0] = fma(cr, P0, accA[t][0]);
         accA[t][1] = fma(cr, P1, accA[t][1]);
-        gcv[t] = fma(Areg[t][0], P0, Areg[t][1] * P1);
+        if constexpr (RECON) {
+          gcv[t] = fma(Areg[t][0], P0, Areg[t][1] * P1);
+        } else {
+          const double* pa = sAc + (8 * warp + 2 * q) * LDF + 8 * t + g;
+          gcv[t] = fma(pa[0], P0, pa[LDF] * P1);
+        }
       }
-      if (NT1 >= NT && kk + 1 < nk) {   // NT == 1: hand-off after the only tile
+      if (RECON && NT1 >= NT && kk + 1 < nk) {   // NT == 1: hand-off after the only tile
         mbar_wait(p3done, kk & 1);
         rebuild_sAc(sC + ((kk + 1) & 3) * RP);
         __syncwarp();
