@@ -22,6 +22,11 @@
 
 namespace tfk {
 
+#ifndef TF_P3_UNROLL
+#define TF_P3_UNROLL 4
+#endif
+constexpr int kP3Unroll = TF_P3_UNROLL;   // Pi-form phase-3 k-loop unroll (development knob)
+
 // Tile geometry: a CTA owns a BT x BT tile (BT = 64: 8 warps, 1 CTA/SM; BT = 32: 4 warps, 2 CTAs/SM).
 template <int BT>
 struct EvalTile {
@@ -338,7 +343,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
       for (int t = 0; t < NT; ++t) Qt[t][0] = Qt[t][1] = 0.0;
       const double* pe = sT + (8 * warp + g) * kLDE + q;
       const double* pa = sAc + q * LDF + g;
-#pragma unroll 4
+#pragma unroll kP3Unroll
       for (int s = 0; s < kBI / 4; ++s) {
         const double bb = pe[4 * s];
 #pragma unroll
