@@ -123,6 +123,10 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
   if (p.run_if && *p.run_if == 0) return;   // guarded fallback not needed (uniform across the grid)
   using S = EvalSmem<NT, BT>;
   using Gm = EvalTile<BT>;
+  // phase 3 with the prescaled tile -A diag(c_k) (rebuilt per slice, needed by phase 1 of the residual form)
+  // or, in the Pi pass with R > 32, with unscaled A and the per-slice scaling on the product (measured: c4/c5
+  // 6%/2.5% faster; for R <= 32 the rebuild is cheaper than the extra accumulators, c3 9%)
+  constexpr bool kPre = RECON || NT <= 4;
   constexpr int kBI = Gm::BI, kBJ = Gm::BJ, kLDE = Gm::LDE, NW = Gm::NW, kThreads = Gm::THREADS;
   constexpr int MF = Gm::MF, NF = Gm::NF;
   constexpr int kTileBytes = Gm::TILE_BYTES;
@@ -226,7 +230,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
   // (the Pi form keeps sAc = A unscaled for the whole CTA: phase 3 scales its per-slice product instead, so
   // neither Areg nor the per-slice rebuild and its hand-off exist there)
   double Areg[NT][2];
-  if constexpr (RECON) {
+  if constexpr (kPre) {
 #pragma unroll
     for (int t = 0; t < NT; ++t)
 #pragma unroll
@@ -243,7 +247,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
   if (nk > 0) {
     for (int u = 0; u < 2 && u < nk; ++u) load_c(kA + u, u);
     __syncthreads();
-    if constexpr (RECON) rebuild_sAc(sC);
+    if constexpr (kPre) rebuild_sAc(sC);
   }
   __syncthreads();
 
@@ -262,7 +266,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
     const double* sc = sC + (kk & 3) * RP;
     TL(kk, 0);
     if (kTMA) mbar_wait(&full[b], (kk >> 1) & 1);
-    if (RECON && kk > 0) mbar_wait(aready, (kk - 1) & 1);
+    if (kPre && kk > 0) mbar_wait(aready, (kk - 1) & 1);
     TL(kk, 1);
 
     // ---- phase 1: E = T + (-A diag(c)) B^T on a (BT/2) x 16 warp tile (MF x 2 fragments)
@@ -325,7 +329,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
     if (kk + 2 < nk) load_c(k + 2, (kk + 2) & 3);
 
     // ---- phase 3: accB^T += (-A diag c)^T E for j-cols 8*warp.., all R (prescaled sAc: no DMUL)
-    if constexpr (RECON) {
+    if constexpr (kPre) {
       const double* pe = sT + (8 * warp + g) * kLDE + q;
       const double* pa = sAc + q * LDF + g;
 #pragma unroll 4
@@ -376,7 +380,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
       for (int j = NT; j < NV; ++j) gcv[j] = 0.0;
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
-        if (RECON && t == NT1 && kk + 1 < nk) {
+        if (kPre && t == NT1 && kk + 1 < nk) {
           TL(kk, 5);
           mbar_wait(p3done, kk & 1);          // every warp is done reading sAc_k
           TL(kk, 6);
@@ -395,14 +399,14 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
         const double P0 = p0[0] + p1[0], P1 = p0[1] + p1[1];   // P[i = 8w+2q+e][r = 8t+g]
         accA[t][0] = fma(cr, P0, accA[t][0]);
         accA[t][1] = fma(cr, P1, accA[t][1]);
-        if constexpr (RECON) {
+        if constexpr (kPre) {
           gcv[t] = fma(Areg[t][0], P0, Areg[t][1] * P1);
         } else {
           const double* pa = sAc + (8 * warp + 2 * q) * LDF + 8 * t + g;
           gcv[t] = fma(pa[0], P0, pa[LDF] * P1);
         }
       }
-      if (RECON && NT1 >= NT && kk + 1 < nk) {   // NT == 1: hand-off after the only tile
+      if (kPre && NT1 >= NT && kk + 1 < nk) {   // NT == 1: hand-off after the only tile
         mbar_wait(p3done, kk & 1);
         rebuild_sAc(sC + ((kk + 1) & 3) * RP);
         __syncwarp();
@@ -675,6 +679,50 @@ cudaError_t launch_eval_finalize(const EvalArgs& p, int RP, double* f, double* g
   if (blocks < 1) blocks = 1;
   k_eval_finalize<<<blocks, 256, 0, st>>>(p, RP, f, grad);
   return cudaGetLastError();
+}
+
+// Resident CTAs per SM of the evaluation kernel actually launched (small R leaves room for 2-3 CTAs of the
+// 64-wide tile; the k-chunk planner sizes the grid with it).
+template <int NT>
+static int eval_occ_nt(bool recon) {
+  const size_t smem = EvalSmem<NT, 64>::bytes;
+  int n = 0;
+  cudaError_t e;
+  if (recon) {
+    e = cudaFuncSetAttribute(k_eval_fused<NT, true, 64, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_eval_fused<NT, true, 64, true>,
+                                                        EvalTile<64>::THREADS, smem);
+  } else {
+    e = cudaFuncSetAttribute(k_eval_fused<NT, true, 64, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_eval_fused<NT, true, 64, false>,
+                                                        EvalTile<64>::THREADS, smem);
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return 1;
+  }
+  return n < 1 ? 1 : n;
+}
+
+int eval_ctas_per_sm(int NT, bool recon) {
+  static int cache[2][17] = {};
+  if (NT < 1 || NT > 16) return 1;
+  int& v = cache[recon ? 1 : 0][NT];
+  if (v) return v;
+  switch (NT) {
+#define TF_CASE(n) \
+  case n:          \
+    v = eval_occ_nt<n>(recon); \
+    break;
+    TF_CASE(1) TF_CASE(2) TF_CASE(3) TF_CASE(4) TF_CASE(5) TF_CASE(6) TF_CASE(7) TF_CASE(8)
+    TF_CASE(9) TF_CASE(10) TF_CASE(11) TF_CASE(12) TF_CASE(13) TF_CASE(14) TF_CASE(15) TF_CASE(16)
+#undef TF_CASE
+  }
+  return v;
 }
 
 size_t eval_smem_bytes(int NT, int BT) {

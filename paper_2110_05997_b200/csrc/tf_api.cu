@@ -142,7 +142,12 @@ tf_status eval_impl(tf_ctx* c, const tf_dims& d, const double* T, const double* 
   const int NT = (int)((d.R + 7) / 8);
   const int RP = 8 * NT;
   const int BT = eval_tile();
-  const int ctas_per_sm = BT == 32 ? 2 : 1;
+  // the form decides which kernel runs (and how many of its CTAs fit on an SM)
+  const bool pi_form = BT == 64 && !c->force_residual &&
+                       (c->eval_form == 2 || (c->eval_form == 0 && 6.0 * d.I * d.J * d.K * d.R >= 5e9));
+  // co-resident CTAs only pay off when one CTA leaves the DMMA pipe mostly idle (R <= 16; measured: c2's
+  // R = 10 gains 14%, c3's R = 20 loses 9% to the shorter k-chunks)
+  const int ctas_per_sm = BT == 32 ? 2 : (NT <= 2 ? eval_ctas_per_sm(NT, !pi_form) : 1);
   EvalArgs p;
   memset(&p, 0, sizeof(p));
   p.run_if = nullptr;
@@ -206,10 +211,8 @@ tf_status eval_impl(tf_ctx* c, const tf_dims& d, const double* T, const double* 
     c->ev_used_pairs++;
     TF_CUDA(c, cudaEventRecord(e0, c->stream));
   }
-  // small problems are launch-bound: the Pi form's extra launches (Grams, guard, conditional fallback) would
-  // cost more than the reconstruction flops it saves
-  const bool pi_form = BT == 64 && !c->force_residual &&
-                       (c->eval_form == 2 || (c->eval_form == 0 && 6.0 * d.I * d.J * d.K * d.R >= 5e9));
+  // (small problems are launch-bound: the Pi form's extra launches — Grams, guard, conditional fallback —
+  // would cost more than the reconstruction flops it saves, hence the 5e9-flop threshold above)
   c->last_eval_pi = pi_form;
   if (!pi_form) {
     TF_CUDA(c, launch_eval(&map, T, p, NT, tma, BT, c->stream));

@@ -36,6 +36,7 @@ cudaError_t launch_eval(const CUtensorMap* map, const double* T, const EvalArgs&
                         cudaStream_t st, bool recon = true);
 cudaError_t launch_eval_finalize(const EvalArgs& p, int RP, double* f, double* grad, int nsm, cudaStream_t st);
 size_t eval_smem_bytes(int NT, int BT);
+int eval_ctas_per_sm(int NT, bool recon);   // resident CTAs per SM of the 64-wide tile kernel
 
 // ---- small kernels (k_small.cu)
 struct Modes {
