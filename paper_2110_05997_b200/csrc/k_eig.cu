@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(kQrThreads) k_house_qr(int64_t n, int P, doubl
 // |theta| decreasing (the ordering of Lemma svd-transpose) with ties kept in index order.
 __global__ void __launch_bounds__(1024) k_jacobi_eig(int P, const double* __restrict__ H, int64_t ldh,
                                                      double* __restrict__ Vt, double* __restrict__ V,
-                                                     double* __restrict__ theta, int vsm) {
+                                                     double* __restrict__ theta, int vsm, int max_sweeps) {
   extern __shared__ double hs[];
   const int Pp = P + (P & 1);
   const int half = Pp / 2;
@@ -135,8 +135,18 @@ __global__ void __launch_bounds__(1024) k_jacobi_eig(int P, const double* __rest
     hs[r + Pp * c] = v;
   }
   for (int e = tid; e < P * P; e += nt) Vw[e] = (e % P == e / P) ? 1.0 : 0.0;
+  __shared__ double hmax_s;
+  if (tid == 0) {
+    double hm = 0.0;
+    for (int i = 0; i < P; ++i) hm = fmax(hm, fabs(hs[i + Pp * i]));
+    hmax_s = hm;
+  }
   __syncthreads();
-  for (int sweep = 0; sweep < 60; ++sweep) {
+  // rotations below DBL_EPSILON * 1e-3 * max|h_ii| cannot move an eigenvalue by more than ~1e-38 |H| or a
+  // vector by more than ~1e-19 |H| / gap: skipping them stops the sweeps that would only chase rounding noise
+  // among the (near-)zero eigenvalues of a rank-deficient Gram
+  const double abs_floor = DBL_EPSILON * 1e-3 * hmax_s;
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     if (tid == 0) rotated = 0;
     __syncthreads();
     for (int step = 0; step < Pp - 1; ++step) {
@@ -152,7 +162,7 @@ __global__ void __launch_bounds__(1024) k_jacobi_eig(int P, const double* __rest
         if (q < P) {
           const double apq = hs[p + Pp * q];
           const double app = hs[p + Pp * p], aqq = hs[q + Pp * q];
-          if (apq != 0.0 && fabs(apq) > DBL_EPSILON * 0.5 * sqrt(fabs(app)) * sqrt(fabs(aqq))) {
+          if (fabs(apq) > abs_floor && fabs(apq) > DBL_EPSILON * 0.5 * sqrt(fabs(app)) * sqrt(fabs(aqq))) {
             const double tau = (aqq - app) / (2.0 * apq);
             double t;
             if (fabs(tau) > 1e150) t = 0.5 / tau;
@@ -507,14 +517,14 @@ cudaError_t launch_house_qr(int64_t n, int P, double* Z, int64_t ldz, double* Q,
 }
 
 cudaError_t launch_jacobi_eig(int P, const double* H, int64_t ldh, double* Vtmp, double* V, double* theta,
-                              cudaStream_t st) {
+                              cudaStream_t st, int max_sweeps) {
   const int Pp = P + (P & 1);
   size_t smem = (size_t)Pp * Pp * 8 + (size_t)Pp * 8 + (size_t)Pp * 4 + 16;
   const int vsm = smem + (size_t)P * P * 8 <= 220 * 1024;
   if (vsm) smem += (size_t)P * P * 8;
   cudaError_t e = cudaFuncSetAttribute(k_jacobi_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_jacobi_eig<<<1, 1024, smem, st>>>(P, H, ldh, Vtmp, V, theta, vsm);
+  k_jacobi_eig<<<1, 1024, smem, st>>>(P, H, ldh, Vtmp, V, theta, vsm, max_sweeps);
   return cudaGetLastError();
 }
 

@@ -578,7 +578,8 @@ __global__ void __launch_bounds__(kPiThreads) k_eval_finalize_pi(EvalArgs p, int
 // a fixed order: strided per-thread partials, then warps, then thread 0 over the warps).
 __global__ void __launch_bounds__(256) k_eval_pi_guard(EvalArgs p, const double* __restrict__ grams,
                                                        const double* __restrict__ part, int nblk,
-                                                       double* __restrict__ f, int* __restrict__ flag) {
+                                                       double* __restrict__ f, int* __restrict__ flag,
+                                                       int check_grad) {
   __shared__ double red[5][8];
   const int64_t R = p.R, RR = R * R;
   double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};   // t2, x2, ip, g2, w2
@@ -601,7 +602,7 @@ __global__ void __launch_bounds__(256) k_eval_pi_guard(EvalArgs p, const double*
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t[u] += red[u][w];
     const double fv = (0.5 * t[0] - t[2]) + 0.5 * t[1];
     *f = fv;
-    const bool safe = (2.0 * fv >= 1e-3 * t[0]) && (t[3] >= 1e-6 * t[4]) && isfinite(fv);
+    const bool safe = (2.0 * fv >= 1e-3 * t[0]) && (!check_grad || t[3] >= 1e-6 * t[4]) && isfinite(fv);
     *flag = safe ? 0 : 1;
   }
 }
@@ -615,8 +616,8 @@ cudaError_t launch_eval_finalize_pi(const EvalArgs& p, int RP, double* grad, dou
 }
 
 cudaError_t launch_eval_pi_guard(const EvalArgs& p, const double* grams, const double* part, int nblk, double* f,
-                                 int* flag, cudaStream_t st) {
-  k_eval_pi_guard<<<1, 256, 0, st>>>(p, grams, part, nblk, f, flag);
+                                 int* flag, cudaStream_t st, bool check_grad) {
+  k_eval_pi_guard<<<1, 256, 0, st>>>(p, grams, part, nblk, f, flag, check_grad ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -67,6 +67,22 @@ void free_buf(DevBuf& b) {
 using namespace tfh;
 
 namespace {
+tf_status eval_impl(tf_ctx* c, const tf_dims& d, const double* T, const double* w, double* f, double* grad);
+}
+
+namespace tfh {
+// F alone (grad is scratch): the Pi-form guard then only asks the Gram expansion of F to be safe
+tf_status eval_f_only(tf_ctx* c, tf_dims d, const double* T, const double* w, double* f, double* grad_scratch) {
+  if (d.ldT == 0) d.ldT = d.I;
+  if (d.K_total == 0) d.K_total = d.K + d.k_begin;
+  c->eval_f_only = true;
+  tf_status s = eval_impl(c, d, T, w, f, grad_scratch);
+  c->eval_f_only = false;
+  return s;
+}
+}  // namespace tfh
+
+namespace {
 
 tf_status check_dims(tf_ctx* c, tf_dims& d) {
   if (!c) return TF_ERR_ARG;
@@ -261,7 +277,7 @@ tf_status eval_impl(tf_ctx* c, const tf_dims& d, const double* T, const double* 
       return s;
   }
   TF_CUDA(c, launch_eval_finalize_pi(p, RP, grad, part, nblk, c->stream));
-  TF_CUDA(c, launch_eval_pi_guard(p, grams, part, nblk, f, flag, c->stream));
+  TF_CUDA(c, launch_eval_pi_guard(p, grams, part, nblk, f, flag, c->stream, !c->eval_f_only));
   EvalArgs pr = p;
   pr.run_if = flag;
   TF_CUDA(c, launch_eval(&map, T, pr, NT, tma, BT, c->stream, true));

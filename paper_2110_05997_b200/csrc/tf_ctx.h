@@ -30,7 +30,8 @@ struct tf_ctx {
   DevBuf evGrams, evPart;                             // Pi-form evaluation: local Grams, guard partials
   int eval_form = 0;                                  // 0 auto, 1 residual form, 2 guarded Pi form
   bool last_eval_pi = false;                          // the last evaluation ran the guarded Pi form
-  bool force_residual = false;                        // dGN loop: the guard fell back, stay residual              // compression: Grams, U, core intermediates
+  bool force_residual = false;                        // dGN loop: the guard fell back, stay residual
+  bool eval_f_only = false;                           // the caller needs F only (guard ignores grad)              // compression: Grams, U, core intermediates
   double* scal_host = nullptr;              // pinned, dGN scalars
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
@@ -59,6 +60,8 @@ tfk::GemmOperand opnd(const double* p, int64_t ld, bool kc, int64_t bstride = 0)
 tfk::GemmArgs gemm_args(tfk::GemmOperand a, tfk::GemmOperand b, int64_t M, int64_t N, int64_t Kd, double* C,
                         int64_t ldc);
 tf_status gemm_run(tf_ctx* c, tfk::GemmArgs g);
+// F at w (grad_scratch: n doubles of scratch), the Pi-form guard checking the expansion of F only (tf_api.cu)
+tf_status eval_f_only(tf_ctx* c, tf_dims d, const double* T, const double* w, double* f, double* grad_scratch);
 
 }  // namespace tfh
 

@@ -29,7 +29,7 @@ struct EvalArgs {
 cudaError_t launch_eval_finalize_pi(const EvalArgs& p, int RP, double* grad, double* part, int nblk,
                                     cudaStream_t st);
 cudaError_t launch_eval_pi_guard(const EvalArgs& p, const double* grams, const double* part, int nblk, double* f,
-                                 int* flag, cudaStream_t st);
+                                 int* flag, cudaStream_t st, bool check_grad = true);
 int eval_pi_blocks(int nsm);
 
 cudaError_t launch_eval(const CUtensorMap* map, const double* T, const EvalArgs& p, int NT, bool tma, int BT,
@@ -136,7 +136,7 @@ cudaError_t launch_chol_inv(int P, const double* B, double* Linv, int* fail, cud
 // symmetric eigen-decomposition of (H + H^T)/2 (P x P) by parallel cyclic Jacobi in one CTA:
 // theta sorted by |theta| decreasing, V (P x P, ld P) the matching eigenvectors; Vtmp: P*P scratch
 cudaError_t launch_jacobi_eig(int P, const double* H, int64_t ldh, double* Vtmp, double* V, double* theta,
-                              cudaStream_t st);
+                              cudaStream_t st, int max_sweeps = 60);
 // res[j] = || ZV[:, j] - theta_j U[:, j] ||_2
 cudaError_t launch_eig_residual(int64_t n, int P, const double* ZV, const double* U, int64_t ld, const double* theta,
                                 double* res, cudaStream_t st);

@@ -248,7 +248,10 @@ tf_status eig_top_impl(tf_ctx* c, int64_t n, const double* G, int P, const doubl
     // Z = G Q ; H = Q^T Z ; (theta, V) = eig(H) ; U = Q V ; ZV = Z V
     if ((s = gemm_run(c, gemm_args(opnd(G, n, false), opnd(Q, ldw, true), n, P, n, Z, ldw)))) return s;
     if ((s = gemm_run(c, gemm_args(opnd(Q, ldw, true), opnd(Z, ldw, true), P, P, n, H, P)))) return s;
-    TF_CUDA(c, launch_jacobi_eig(P, H, P, Vt, V, theta, c->stream));
+    // the first two Rayleigh-Ritz steps act on a still-rotating subspace: a few Jacobi sweeps give a rotation
+    // good enough for the orthonormalisation; the converged iterations run Jacobi to the end
+    const bool early = it <= 2 && it < maxiter;
+    TF_CUDA(c, launch_jacobi_eig(P, H, P, Vt, V, theta, c->stream, early ? 4 : 60));
     if ((s = gemm_run(c, gemm_args(opnd(Q, ldw, false), opnd(V, P, true), n, P, P, Uw, ldw)))) return s;
     if ((s = gemm_run(c, gemm_args(opnd(Z, ldw, false), opnd(V, P, true), n, P, P, ZV, ldw)))) return s;
     TF_CUDA(c, launch_eig_residual(n, P, ZV, Uw, ldw, theta, res, c->stream));
@@ -260,8 +263,8 @@ tf_status eig_top_impl(tf_ctx* c, int64_t n, const double* G, int P, const doubl
     const double scale = std::fabs(host[0]);
     if (!std::isfinite(maxres) || !std::isfinite(scale))
       return set_err(c, TF_ERR_NONFINITE, "non-finite Ritz values in the subspace iteration");
-    const bool conv = maxres <= tol_eff * scale || scale == 0.0;
-    const bool stall = it >= 3 && maxres > 0.5 * prev && maxres <= 1e3 * tol_eff * scale;
+    const bool conv = !early && (maxres <= tol_eff * scale || scale == 0.0);
+    const bool stall = it >= 4 && maxres > 0.5 * prev && maxres <= 1e3 * tol_eff * scale;
     if (conv || stall || it == maxiter) break;
     prev = maxres;
     // orthonormalise the Ritz-rotated block ZV ~ U Theta for the next iteration
@@ -550,7 +553,7 @@ tf_status tf_cpd(tf_ctx* c, tf_dims d, const double* T, const double* Omega, con
   double* part = scal + 8;
   TF_CUDA(c, launch_tsums(d.I, d.J, d.K, d.ldT, T, part, scal, c->stream));
   c->total_launches += 1;
-  if ((s = tf_cpd_eval(c, d, T, W, scal + 2, (double*)c->cpdGrad.p, nullptr))) return s;
+  if ((s = eval_f_only(c, d, T, W, scal + 2, (double*)c->cpdGrad.p))) return s;
   TF_CUDA(c, launch_normalize_cpd(dims, R, W, lambda, c->stream));
   c->total_launches += 1;
   double h[3];
