@@ -270,15 +270,31 @@ __global__ void k_tsums_partial(int64_t I, int64_t JK, int64_t ldT, const double
   }
 }
 
-// out[c] = ordered combination over blocks of partial[b][c] (c < ncomp; component 3 of the dots is a max)
-__global__ void k_partial_final(int nblk, int ncomp, int max_comp, const double* __restrict__ partial,
-                                double* __restrict__ out) {
-  if (threadIdx.x < ncomp) {
+// out[c] = ordered combination over blocks of partial[b][c] (c < ncomp <= 4; component max_comp is a max):
+// every thread folds a fixed strided subset of the blocks, then the warps and the block combine in a fixed
+// order (deterministic; independent loads instead of one serial chain of L2 round trips)
+__global__ void __launch_bounds__(256) k_partial_final(int nblk, int ncomp, int max_comp,
+                                                       const double* __restrict__ partial, double* __restrict__ out) {
+  __shared__ double red[4][8];
+  for (int c = 0; c < ncomp; ++c) {
+    const bool mx = c == max_comp;
     double v = 0.0;
-    for (int b = 0; b < nblk; ++b) {
-      const double p = partial[b * ncomp + threadIdx.x];
-      v = (int)threadIdx.x == max_comp ? fmax(v, p) : v + p;
+    for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
+      const double p = partial[b * ncomp + c];
+      v = mx ? fmax(v, p) : v + p;
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double u = __shfl_xor_sync(0xffffffffu, v, o);
+      v = mx ? fmax(v, u) : v + u;
+    }
+    if ((threadIdx.x & 31) == 0) red[c][threadIdx.x >> 5] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < ncomp) {
+    const bool mx = (int)threadIdx.x == max_comp;
+    double v = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v = mx ? fmax(v, red[threadIdx.x][w]) : v + red[threadIdx.x][w];
     out[threadIdx.x] = v;
   }
 }
@@ -307,14 +323,14 @@ __global__ void k_balance(Modes m, const double* __restrict__ grams, double* __r
 cudaError_t launch_dots(int64_t n, const double* g, const double* x, const double* y, double* partial, double* out,
                         cudaStream_t st) {
   k_dots_partial<<<kRedBlocks, 256, 0, st>>>(n, g, x, y, partial);
-  k_partial_final<<<1, 32, 0, st>>>(kRedBlocks, 4, 3, partial, out);
+  k_partial_final<<<1, 256, 0, st>>>(kRedBlocks, 4, 3, partial, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_tsums(int64_t I, int64_t J, int64_t K, int64_t ldT, const double* T, double* partial, double* out,
                          cudaStream_t st) {
   k_tsums_partial<<<kRedBlocks, 256, 0, st>>>(I, J * K, ldT, T, partial);
-  k_partial_final<<<1, 32, 0, st>>>(kRedBlocks, 2, -1, partial, out);
+  k_partial_final<<<1, 256, 0, st>>>(kRedBlocks, 2, -1, partial, out);
   return cudaGetLastError();
 }
 
