@@ -225,6 +225,18 @@ tf_status tf_compress_st(tf_ctx *ctx, tf_dims d, const double *T, const double *
                          int eig_maxiter, double eig_tol, double *U, double *sigma, double *S, int64_t *ranks,
                          int *eig_iters);
 
+/* K-sharded Alg. ST-MLSVD: this rank holds slices k_begin .. k_begin+K-1 (d.K local, d.K_total global). The
+ * mode-1 and mode-2 Grams are sums over slices and are summed over the ranks through the all-reduce hook
+ * (tf_allreduce_fn: the contract described at tf_cpd_dgn_sharded); mode 3 needs every slice of X2 = T x1 U~1^T x2 U~2^T,
+ * which each rank writes into its columns of a zeroed R~1 R~2 x K_total buffer completed by the same hook.
+ * Outputs as tf_compress_st, identical on every rank (U3 has K_total rows). xbuf (device, caller-owned) must
+ * hold max(I^2, J^2, P1 P2 K_total) doubles. */
+typedef int (*tf_allreduce_fn)(double *buf, int64_t count, void *user);
+tf_status tf_compress_st_sharded(tf_ctx *ctx, tf_dims d, const double *T_local, const double *Omega,
+                                 double mlsvd_tol, int eig_maxiter, double eig_tol, double *U, double *sigma,
+                                 double *S, int64_t *ranks, int *eig_iters, tf_allreduce_fn allreduce, void *user,
+                                 double *xbuf);
+
 /* MLSVD-energy initialisation on the core S (R1 x R2 x R3): w = [vec W1; vec W2; vec W3] (R*(R1+R2+R3))
  * with W1[:, r] = s_j e_{j1}, W2[:, r] = e_{j2}, W3[:, r] = e_{j3} for the R entries j of largest |s|. */
 tf_status tf_energy_init(tf_ctx *ctx, int64_t R1, int64_t R2, int64_t R3, const double *S, int64_t R, double *w);
@@ -259,6 +271,14 @@ typedef struct {
 
 tf_status tf_cpd(tf_ctx *ctx, tf_dims d, const double *T, const double *Omega, const double *w0_core,
                  const tf_cpd_params *prm, double *W, double *lambda, tf_cpd_result *res, double *hist);
+
+/* The flow on a K-sharded tensor (T_local = slices k_begin .. k_begin+K-1): compression by
+ * tf_compress_st_sharded (always ST-MLSVD), then the dGN on the core, the uncompression and the unit-column
+ * form replicated on every rank; the final fit sums the ranks' partial F and ||T||^2 through the hook.
+ * xbuf as for tf_compress_st_sharded (>= 3 doubles in any case). */
+tf_status tf_cpd_sharded(tf_ctx *ctx, tf_dims d, const double *T_local, const double *Omega, const double *w0_core,
+                         const tf_cpd_params *prm, double *W, double *lambda, tf_cpd_result *res, double *hist,
+                         tf_allreduce_fn allreduce, void *user, double *xbuf);
 
 /* ---------------------------------------------------------------------------------------------------
  * NEXT #4 -- CP-ALS (Alg. ALS), the second workload on the slice-streaming MTTKRP. */
@@ -299,7 +319,6 @@ tf_status tf_ctx_eval_fallback(tf_ctx *ctx, int *fell_back);
  * after the library synchronized its stream, with `buf` = xbuf (device, caller-owned, >= n + 1 doubles,
  * n = R(I+J+K_total)) holding `count` doubles; it must replace them with their elementwise SUM over the
  * ranks (e.g. an NCCL all-reduce of the tensor that owns xbuf) before returning 0 (nonzero -> TF_ERR_CUDA). */
-typedef int (*tf_allreduce_fn)(double *buf, int64_t count, void *user);
 tf_status tf_cpd_dgn_sharded(tf_ctx *ctx, tf_dims d, const double *T_local, double *w, const tf_dgn_params *prm,
                              tf_dgn_result *res, double *hist, tf_allreduce_fn allreduce, void *user, double *xbuf);
 

@@ -35,6 +35,7 @@ class TfDims(ctypes.Structure):
 
 
 _vp = ctypes.c_void_p
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_int64, ctypes.c_void_p)
 _lib.tf_ctx_create.argtypes = [ctypes.POINTER(_vp), ctypes.c_int, _vp]
 _lib.tf_ctx_destroy.argtypes = [_vp]
 _lib.tf_ctx_set_stream.argtypes = [_vp, _vp]
@@ -67,7 +68,6 @@ class TfDgnResult(ctypes.Structure):
 _lib.tf_cpd_dgn.argtypes = [_vp, TfDims, _vp, _vp, ctypes.POINTER(TfDgnParams), ctypes.POINTER(TfDgnResult),
                             ctypes.POINTER(ctypes.c_double)]
 _lib.tf_ctx_set_timing.argtypes = [_vp, ctypes.c_int]
-ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.c_int64, ctypes.c_void_p)
 _lib.tf_ctx_set_eval_form.argtypes = [_vp, ctypes.c_int]
 _lib.tf_cpd_dgn_sharded.argtypes = [_vp, TfDims, _vp, _vp, ctypes.POINTER(TfDgnParams), ctypes.POINTER(TfDgnResult),
                                     ctypes.POINTER(ctypes.c_double), ALLREDUCE_FN, ctypes.c_void_p, _vp]
@@ -81,6 +81,9 @@ _lib.tf_compress.argtypes = [_vp, TfDims, _vp, _vp, ctypes.c_double, ctypes.c_in
                              ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_int)]
 _lib.tf_compress_st.argtypes = [_vp, TfDims, _vp, _vp, ctypes.c_double, ctypes.c_int, ctypes.c_double, _vp, _vp,
                                 _vp, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_int)]
+_lib.tf_compress_st_sharded.argtypes = [_vp, TfDims, _vp, _vp, ctypes.c_double, ctypes.c_int, ctypes.c_double, _vp,
+                                        _vp, _vp, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_int), ALLREDUCE_FN,
+                                        ctypes.c_void_p, _vp]
 _lib.tf_energy_init.argtypes = [_vp, _i64, _i64, _i64, _vp, _i64, _vp]
 _lib.tf_uncompress.argtypes = [_vp, _i64, _i64, _vp, _vp, _i64, _vp]
 
@@ -101,6 +104,9 @@ class TfCpdResult(ctypes.Structure):
 
 _lib.tf_cpd.argtypes = [_vp, TfDims, _vp, _vp, _vp, ctypes.POINTER(TfCpdParams), _vp, _vp, ctypes.POINTER(TfCpdResult),
                         ctypes.POINTER(ctypes.c_double)]
+_lib.tf_cpd_sharded.argtypes = [_vp, TfDims, _vp, _vp, _vp, ctypes.POINTER(TfCpdParams), _vp, _vp,
+                                ctypes.POINTER(TfCpdResult), ctypes.POINTER(ctypes.c_double), ALLREDUCE_FN,
+                                ctypes.c_void_p, _vp]
 _lib.tf_ctx_kernel_stats.argtypes = [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64),
                                      ctypes.POINTER(ctypes.c_int64), ctypes.c_int]
 
@@ -109,7 +115,8 @@ EXPORTED = ["tf_ctx_create", "tf_ctx_destroy", "tf_ctx_set_stream", "tf_status_s
             "tf_reg_gamma", "tf_gn_matvec_damped", "tf_cg_solve_damped", "tf_cpd_dgn", "tf_ctx_set_timing",
             "tf_ctx_kernel_stats", "tf_unfolding_grams", "tf_sym_eig_top", "tf_multilinear_core", "tf_compress",
             "tf_energy_init", "tf_uncompress", "tf_cpd", "tf_mttkrp", "tf_als", "tf_ctx_set_eval_form",
-            "tf_ctx_eval_fallback", "tf_cpd_dgn_sharded", "tf_compress_st"]
+            "tf_ctx_eval_fallback", "tf_cpd_dgn_sharded", "tf_compress_st",
+            "tf_compress_st_sharded", "tf_cpd_sharded"]
 
 TF_OK, TF_ERR_ARG, TF_ERR_ALIGN, TF_ERR_UNSUPPORTED, TF_ERR_CUDA, TF_ERR_NONFINITE, TF_ERR_ALLOC = range(7)
 MAX_R = 128
@@ -156,6 +163,24 @@ def _dev(t: torch.Tensor, name: str, numel: int | None = None):
         raise ValueError(f"{name} must be contiguous")
     if numel is not None and t.numel() < numel:
         raise ValueError(f"{name} has {t.numel()} elements, needs {numel}")
+
+
+def _make_hook(xbuf: torch.Tensor, allreduce):
+    """A C all-reduce hook (tf_allreduce_fn) that SUM-reduces the first `count` doubles of the torch tensor
+    xbuf (the exchange buffer the library was given) with the Python callable allreduce(view); exceptions
+    are kept (never raised across the C ABI) and re-raised by the caller."""
+    errors = []
+
+    def hook(buf, count, user):
+        try:
+            allreduce(xbuf[:count])
+            torch.cuda.current_stream(xbuf.device).synchronize()
+            return 0
+        except Exception as e:
+            errors.append(e)
+            return 1
+
+    return ALLREDUCE_FN(hook), errors
 
 
 class Context:
@@ -375,6 +400,38 @@ class Context:
         """Alg. ST-MLSVD (the sequentially truncated compression); same outputs as tf_compress."""
         return self.tf_compress(d, T, Omega, mlsvd_tol, eig_maxiter, eig_tol, sequential=True)
 
+    def tf_compress_st_sharded(self, d: Dims, T_local: torch.Tensor, Omega: torch.Tensor, allreduce,
+                               mlsvd_tol: float = 1e-6, eig_maxiter: int = 100, eig_tol: float = 0.0):
+        """K-sharded Alg. ST-MLSVD (this rank: d.K slices from d.k_begin of d.K_total). allreduce(buf) must SUM
+        the float64 CUDA tensor buf over the ranks in place. Same outputs as tf_compress (identical on every
+        rank; U3 has K_total rows)."""
+        ldT = d.ldT or d.I
+        _dev(T_local, "T_local", ldT * d.J * d.K - (ldT - d.I))
+        dims = (d.I, d.J, d.Kt)
+        P = tuple(min(n, d.R) for n in dims)
+        nU = sum(n * p for n, p in zip(dims, P))
+        _dev(Omega, "Omega", nU)
+        U = torch.empty(nU, dtype=torch.float64, device=T_local.device)
+        sigma = torch.empty(sum(P), dtype=torch.float64, device=T_local.device)
+        S = torch.empty(P[0] * P[1] * P[2], dtype=torch.float64, device=T_local.device)
+        ranks = (ctypes.c_int64 * 3)()
+        iters = (ctypes.c_int * 3)()
+        xbuf = torch.empty(max(d.I * d.I, d.J * d.J, P[0] * P[1] * d.Kt, 3), dtype=torch.float64,
+                           device=T_local.device)
+        cb, errors = _make_hook(xbuf, allreduce)
+        st = _lib.tf_compress_st_sharded(self._h, d.c(), _ptr(T_local), _ptr(Omega), float(mlsvd_tol),
+                                         int(eig_maxiter), float(eig_tol), _ptr(U), _ptr(sigma), _ptr(S), ranks, iters,
+                                         cb, None, _ptr(xbuf))
+        if errors:
+            raise errors[0]
+        self._check(st)
+        rk = tuple(int(r) for r in ranks)
+        offs = [0, dims[0] * P[0], dims[0] * P[0] + dims[1] * P[1]]
+        soffs = [0, P[0], P[0] + P[1]]
+        return {"U": [U[offs[l]:offs[l] + dims[l] * P[l]] for l in range(3)],
+                "sigma": [sigma[soffs[l]:soffs[l] + P[l]] for l in range(3)],
+                "S": S[:rk[0] * rk[1] * rk[2]], "ranks": rk, "P": P, "eig_iters": [int(i) for i in iters]}
+
     def tf_energy_init(self, R1: int, R2: int, R3: int, S: torch.Tensor, R: int) -> torch.Tensor:
         """Packed w = [vec W1; vec W2; vec W3] of the MLSVD-energy initialisation on the core S."""
         _dev(S, "S", R1 * R2 * R3)
@@ -490,19 +547,7 @@ class Context:
         res = TfDgnResult()
         hist = np.zeros(5 * max(m, 1))
         xbuf = torch.empty(d.n + 1, dtype=torch.float64, device=w.device)
-        errors = []
-
-        def hook(buf, count, user):
-            try:
-                view = xbuf[:count]
-                allreduce(view)
-                torch.cuda.current_stream(w.device).synchronize()
-                return 0
-            except Exception as e:   # never raise across the C ABI
-                errors.append(e)
-                return 1
-
-        cb = ALLREDUCE_FN(hook)
+        cb, errors = _make_hook(xbuf, allreduce)
         st = _lib.tf_cpd_dgn_sharded(self._h, d.c(), _ptr(T_local), _ptr(w), ctypes.byref(prm), ctypes.byref(res),
                                      hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), cb, None, _ptr(xbuf))
         if errors:
@@ -510,6 +555,45 @@ class Context:
         self._check(st)
         out = {"iters": res.iters, "reason": res.reason, "f": res.f, "rel_err": res.rel_err, "mu": res.mu}
         return out, hist.reshape(-1, 5)[:res.iters]
+
+    def tf_cpd_sharded(self, d: Dims, T_local: torch.Tensor, Omega: torch.Tensor, cg_iters, allreduce,
+                       w0_core: torch.Tensor | None = None, mlsvd_tol: float = 1e-6, eig_maxiter: int = 100,
+                       maxiter: int | None = None, tol: float = 1e-6, mu0: float = 0.0, use_gamma: bool = True,
+                       jacobi: bool = True, balance: bool = True):
+        """The whole flow on a K-sharded tensor (always ST-MLSVD compression); returns what tf_cpd returns,
+        identical on every rank."""
+        import numpy as np
+        ldT = d.ldT or d.I
+        _dev(T_local, "T_local", ldT * d.J * d.K - (ldT - d.I))
+        dims = (d.I, d.J, d.Kt)
+        P = [min(x, d.R) for x in dims]
+        _dev(Omega, "Omega", sum(x * p for x, p in zip(dims, P)))
+        if w0_core is not None:
+            _dev(w0_core, "w0_core", d.R * sum(P))
+        cgi = np.ascontiguousarray(np.asarray(cg_iters, dtype=np.int32))
+        m = int(maxiter if maxiter is not None else cgi.size)
+        if cgi.size < m:
+            raise ValueError("cg_iters shorter than maxiter")
+        dp = TfDgnParams(m, float(tol), float(mu0), int(bool(use_gamma)), int(bool(jacobi)), int(bool(balance)),
+                         cgi.ctypes.data_as(ctypes.POINTER(ctypes.c_int)))
+        prm = TfCpdParams(float(mlsvd_tol), int(eig_maxiter), 0 if w0_core is not None else 1, dp, 1)
+        res = TfCpdResult()
+        W = torch.empty(d.R * sum(dims), dtype=torch.float64, device=T_local.device)
+        lam = torch.empty(d.R, dtype=torch.float64, device=T_local.device)
+        hist = np.zeros(5 * max(m, 1))
+        xbuf = torch.empty(max(d.I * d.I, d.J * d.J, P[0] * P[1] * d.Kt, 3), dtype=torch.float64,
+                           device=T_local.device)
+        cb, errors = _make_hook(xbuf, allreduce)
+        st = _lib.tf_cpd_sharded(self._h, d.c(), _ptr(T_local), _ptr(Omega), _ptr(w0_core), ctypes.byref(prm),
+                                 _ptr(W), _ptr(lam), ctypes.byref(res),
+                                 hist.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), cb, None, _ptr(xbuf))
+        if errors:
+            raise errors[0]
+        self._check(st)
+        out = {"ranks": tuple(int(x) for x in res.ranks), "eig_iters": [int(x) for x in res.eig_iters],
+               "dgn": {"iters": res.dgn.iters, "reason": res.dgn.reason, "f": res.dgn.f, "rel_err": res.dgn.rel_err,
+                       "mu": res.dgn.mu}, "rel_err": res.rel_err}
+        return W, lam, out, hist.reshape(-1, 5)[:res.dgn.iters]
 
     def set_eval_form(self, form: str):
         """'auto' (default: the guarded Pi form, 4IJKR flops, when large enough), 'pi' (guarded Pi form at any

@@ -392,18 +392,31 @@ tf_status tf_compress(tf_ctx* c, tf_dims d, const double* T, const double* Omega
   return core_impl(c, d, T, U + off[0], ranks[0], U + off[1], ranks[1], U + off[2], ranks[2], S);
 }
 
-tf_status tf_compress_st(tf_ctx* c, tf_dims d, const double* T, const double* Omega, double mlsvd_tol,
-                         int eig_maxiter, double eig_tol, double* U, double* sigma, double* S, int64_t* ranks,
-                         int* eig_iters) {
-  tf_status s = check_whole(c, d);
-  if (s) return s;
-  if (!T || !Omega || !U || !sigma || !S || !ranks) return set_err(c, TF_ERR_ARG, "null pointer");
-  if (d.R < 1) return set_err(c, TF_ERR_ARG, "R < 1");
-  if (!(mlsvd_tol > 0.0)) return set_err(c, TF_ERR_ARG, "mlsvd_tol must be > 0");
-  if (eig_maxiter < 1) return set_err(c, TF_ERR_ARG, "eig_maxiter < 1");
-  cudaSetDevice(c->device);
-  const int64_t I = d.I, J = d.J, K = d.K, ld = d.ldT;
-  const int64_t dims[3] = {I, J, K};
+}  // extern "C"
+
+namespace {
+
+// Exchange of a device buffer through the caller's all-reduce hook (K-sharded calls): src -> xbuf, SUM over
+// the ranks, xbuf -> src. No-op without a hook.
+tf_status exchange(tf_ctx* c, tf_allreduce_fn xfn, void* xuser, double* xbuf, double* src, int64_t cnt) {
+  if (!xfn) return TF_OK;
+  TF_CUDA(c, cudaMemcpyAsync(xbuf, src, cnt * 8, cudaMemcpyDeviceToDevice, c->stream));
+  TF_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (xfn(xbuf, cnt, xuser) != 0) return set_err(c, TF_ERR_CUDA, "the all-reduce hook reported a failure");
+  TF_CUDA(c, cudaMemcpyAsync(src, xbuf, cnt * 8, cudaMemcpyDeviceToDevice, c->stream));
+  return TF_OK;
+}
+
+// Alg. ST-MLSVD on the local slices d.k_begin .. d.k_begin + d.K - 1 of a K_total-slice tensor. Modes 1 and 2
+// only need sums over slices (their Grams are all-reduced); mode 3 needs every slice of X2 = T x1 U~1^T x2 U~2^T,
+// which each rank writes into its columns of a zeroed R~1 R~2 x K_total buffer that the all-reduce completes.
+// Everything after that (G3, U3, the core) is computed identically on every rank.
+tf_status compress_st_impl(tf_ctx* c, const tf_dims& d, const double* T, const double* Omega, double mlsvd_tol,
+                           int eig_maxiter, double eig_tol, double* U, double* sigma, double* S, int64_t* ranks,
+                           int* eig_iters, tf_allreduce_fn xfn, void* xuser, double* xbuf) {
+  tf_status s;
+  const int64_t I = d.I, J = d.J, Kl = d.K, Kt = d.K_total, kb = d.k_begin, ld = d.ldT;
+  const int64_t dims[3] = {I, J, Kt};
   int64_t P[3], off[3], soff[3];
   int64_t o = 0, so = 0;
   for (int l = 0; l < 3; ++l) {
@@ -414,7 +427,7 @@ tf_status tf_compress_st(tf_ctx* c, tf_dims d, const double* T, const double* Om
     o += dims[l] * P[l];
     so += P[l];
   }
-  const int64_t nmax = std::max(I, std::max(J, K));
+  const int64_t nmax = std::max(I, std::max(J, Kt));
   if ((s = ensure(c, c->mlG, (size_t)nmax * nmax * 8))) return s;
   if ((s = ensure(c, c->mlLam, (size_t)TF_MAX_R * 8))) return s;
   if ((s = ensure(c, c->mlRanks, 3 * sizeof(int64_t)))) return s;
@@ -435,42 +448,95 @@ tf_status tf_compress_st(tf_ctx* c, tf_dims d, const double* T, const double* Om
     c->total_launches += 2;
     return TF_OK;
   };
-  // step 1: T_(1) T_(1)^T, U1, then X1 = U~1^T T_(1)  (r1 x J x K, leading dimension r1e)
+  // step 1: T_(1) T_(1)^T (summed over the ranks' slices), U1, then X1 = U~1^T T_(1)  (r1 x J x K local)
   if ((s = grams_mode(c, d, T, 1, G))) return s;
+  if ((s = exchange(c, xfn, xuser, xbuf, G, I * I))) return s;
   if ((s = mode_step(0))) return s;
   const int64_t r1 = ranks[0], r1e = even(r1);
-  if ((s = ensure(c, c->mlX, (size_t)r1e * J * K * 8))) return s;
+  if ((s = ensure(c, c->mlX, (size_t)r1e * J * Kl * 8))) return s;
   double* X1 = (double*)c->mlX.p;
-  if ((s = gemm_run(c, gemm_args(opnd(U + off[0], I, true), opnd(T, ld, true), r1, J * K, I, X1, r1e)))) return s;
+  if ((s = gemm_run(c, gemm_args(opnd(U + off[0], I, true), opnd(T, ld, true), r1, J * Kl, I, X1, r1e)))) return s;
   // step 2: Gram of the mode-2 unfolding of X1 (sum over slices of X1_k^T X1_k), U2, X2_k = X1_k U~2
   {
     GemmOperand a = opnd(X1, r1e, true, r1e * J);
     GemmArgs g = gemm_args(a, a, J, J, r1, G, J);
-    g.batch = K;
+    g.batch = Kl;
     g.sym = true;
     if ((s = gemm_run(c, g))) return s;
   }
+  if ((s = exchange(c, xfn, xuser, xbuf, G, J * J))) return s;
   if ((s = mode_step(1))) return s;
   const int64_t r2 = ranks[1];
-  if ((s = ensure(c, c->mlY, (size_t)r1 * r2 * K * 8))) return s;
-  double* X2 = (double*)c->mlY.p;
+  if ((s = ensure(c, c->mlY, (size_t)r1 * r2 * Kt * 8))) return s;
+  double* X2 = (double*)c->mlY.p;   // r1 r2 x K_total; this rank's columns kb .. kb + Kl - 1
+  if (xfn) TF_CUDA(c, cudaMemsetAsync(X2, 0, (size_t)r1 * r2 * Kt * 8, c->stream));
   {
-    GemmArgs g = gemm_args(opnd(X1, r1e, false, r1e * J), opnd(U + off[1], J, true), r1, r2, J, X2, r1);
-    g.batch = K;
+    GemmArgs g = gemm_args(opnd(X1, r1e, false, r1e * J), opnd(U + off[1], J, true), r1, r2, J, X2 + kb * r1 * r2,
+                           r1);
+    g.batch = Kl;
     g.sum_batch = false;
     g.cstride = r1 * r2;
     if ((s = gemm_run(c, g))) return s;
   }
-  // step 3: Gram of X2 as (r1 r2) x K, U3, S = X2 x_3 U~3^T
+  if ((s = exchange(c, xfn, xuser, xbuf, X2, r1 * r2 * Kt))) return s;
+  // step 3: Gram of X2 as (r1 r2) x K_total, U3, S = X2 x_3 U~3^T
   {
     GemmOperand a = opnd(X2, r1 * r2, true);
-    GemmArgs g = gemm_args(a, a, K, K, r1 * r2, G, K);
+    GemmArgs g = gemm_args(a, a, Kt, Kt, r1 * r2, G, Kt);
     g.sym = true;
     if ((s = gemm_run(c, g))) return s;
   }
   if ((s = mode_step(2))) return s;
   const int64_t r3 = ranks[2];
-  return gemm_run(c, gemm_args(opnd(X2, r1 * r2, false), opnd(U + off[2], K, true), r1 * r2, r3, K, S, r1 * r2));
+  return gemm_run(c, gemm_args(opnd(X2, r1 * r2, false), opnd(U + off[2], Kt, true), r1 * r2, r3, Kt, S, r1 * r2));
+}
+
+tf_status check_compress_args(tf_ctx* c, const tf_dims& d, const double* T, const double* Omega, double mlsvd_tol,
+                              int eig_maxiter, double* U, double* sigma, double* S, int64_t* ranks) {
+  if (!T || !Omega || !U || !sigma || !S || !ranks) return set_err(c, TF_ERR_ARG, "null pointer");
+  if (d.R < 1) return set_err(c, TF_ERR_ARG, "R < 1");
+  if (!(mlsvd_tol > 0.0)) return set_err(c, TF_ERR_ARG, "mlsvd_tol must be > 0");
+  if (eig_maxiter < 1) return set_err(c, TF_ERR_ARG, "eig_maxiter < 1");
+  return TF_OK;
+}
+
+tf_status check_shard(tf_ctx* c, tf_dims& d) {
+  if (!c) return TF_ERR_ARG;
+  if (d.ldT == 0) d.ldT = d.I;
+  if (d.K_total == 0) d.K_total = d.K + d.k_begin;
+  if (d.I < 1 || d.J < 1 || d.K < 1) return set_err(c, TF_ERR_ARG, "dimensions must be >= 1");
+  if (d.ldT < d.I) return set_err(c, TF_ERR_ARG, "ldT < I");
+  if (d.k_begin < 0 || d.k_begin + d.K > d.K_total) return set_err(c, TF_ERR_ARG, "k_begin + K > K_total");
+  if (d.I > (1LL << 31) - 1 || d.J > (1LL << 31) - 1 || d.K_total > (1LL << 31) - 1)
+    return set_err(c, TF_ERR_UNSUPPORTED, "mode size >= 2^31");
+  return TF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+tf_status tf_compress_st(tf_ctx* c, tf_dims d, const double* T, const double* Omega, double mlsvd_tol,
+                         int eig_maxiter, double eig_tol, double* U, double* sigma, double* S, int64_t* ranks,
+                         int* eig_iters) {
+  tf_status s = check_whole(c, d);
+  if (s) return s;
+  if ((s = check_compress_args(c, d, T, Omega, mlsvd_tol, eig_maxiter, U, sigma, S, ranks))) return s;
+  cudaSetDevice(c->device);
+  return compress_st_impl(c, d, T, Omega, mlsvd_tol, eig_maxiter, eig_tol, U, sigma, S, ranks, eig_iters, nullptr,
+                          nullptr, nullptr);
+}
+
+tf_status tf_compress_st_sharded(tf_ctx* c, tf_dims d, const double* T_local, const double* Omega, double mlsvd_tol,
+                                 int eig_maxiter, double eig_tol, double* U, double* sigma, double* S, int64_t* ranks,
+                                 int* eig_iters, tf_allreduce_fn allreduce, void* user, double* xbuf) {
+  tf_status s = check_shard(c, d);
+  if (s) return s;
+  if ((s = check_compress_args(c, d, T_local, Omega, mlsvd_tol, eig_maxiter, U, sigma, S, ranks))) return s;
+  if (!allreduce || !xbuf) return set_err(c, TF_ERR_ARG, "null all-reduce hook or exchange buffer");
+  cudaSetDevice(c->device);
+  return compress_st_impl(c, d, T_local, Omega, mlsvd_tol, eig_maxiter, eig_tol, U, sigma, S, ranks, eig_iters,
+                          allreduce, user, xbuf);
 }
 
 tf_status tf_energy_init(tf_ctx* c, int64_t R1, int64_t R2, int64_t R3, const double* S, int64_t R, double* w) {
@@ -490,23 +556,26 @@ tf_status tf_uncompress(tf_ctx* c, int64_t n, int64_t Rl, const double* U, const
   return gemm_run(c, gemm_args(opnd(U, n, false), opnd(W, Rl, true), n, R, Rl, out, n));
 }
 
-tf_status tf_cpd(tf_ctx* c, tf_dims d, const double* T, const double* Omega, const double* w0_core,
-                 const tf_cpd_params* prm, double* W, double* lambda, tf_cpd_result* res, double* hist) {
-  tf_status s = check_whole(c, d);
-  if (s) return s;
-  if (!T || !Omega || !prm || !W || !lambda || !res) return set_err(c, TF_ERR_ARG, "null pointer");
-  if (!prm->init && !w0_core) return set_err(c, TF_ERR_ARG, "init = 0 needs w0_core");
-  if (d.R < 1 || d.R > TF_MAX_R) return set_err(c, d.R < 1 ? TF_ERR_ARG : TF_ERR_UNSUPPORTED, "bad R");
-  cudaSetDevice(c->device);
+}  // extern "C"
+
+namespace {
+
+// The whole flow on the local slices of a K_total-slice tensor; with an exchange hook the compression is the
+// K-sharded ST-MLSVD and the final fit sums the ranks' partial F and ||T||^2; the dGN on the core and the
+// uncompression run replicated (every rank holds the full core and U).
+tf_status cpd_impl(tf_ctx* c, const tf_dims& d, const double* T, const double* Omega, const double* w0_core,
+                   const tf_cpd_params* prm, double* W, double* lambda, tf_cpd_result* res, double* hist,
+                   tf_allreduce_fn xfn, void* xuser, double* xbuf) {
+  tf_status s;
   const int64_t R = d.R;
-  const int64_t dims[3] = {d.I, d.J, d.K};
+  const int64_t dims[3] = {d.I, d.J, d.K_total};
   int64_t P[3];
   int64_t nU = 0;
   for (int l = 0; l < 3; ++l) {
     P[l] = std::min<int64_t>(dims[l], R);
     nU += dims[l] * P[l];
   }
-  const int64_t n = R * (d.I + d.J + d.K);
+  const int64_t n = R * (d.I + d.J + d.K_total);
   if ((s = ensure(c, c->cpdU, (size_t)nU * 8))) return s;
   if ((s = ensure(c, c->cpdSig, (size_t)(P[0] + P[1] + P[2]) * 8))) return s;
   if ((s = ensure(c, c->cpdS, (size_t)P[0] * P[1] * P[2] * 8))) return s;
@@ -518,9 +587,13 @@ tf_status tf_cpd(tf_ctx* c, tf_dims d, const double* T, const double* Omega, con
   double* wc = (double*)c->cpdW.p;
   // 1. compression
   int64_t rk[3];
-  if ((s = (prm->sequential ? tf_compress_st : tf_compress)(c, d, T, Omega, prm->mlsvd_tol, prm->eig_maxiter, 0.0, U,
-                                                            (double*)c->cpdSig.p, S, rk, res->eig_iters)))
-    return s;
+  if (xfn || prm->sequential)
+    s = compress_st_impl(c, d, T, Omega, prm->mlsvd_tol, prm->eig_maxiter, 0.0, U, (double*)c->cpdSig.p, S, rk,
+                         res->eig_iters, xfn, xuser, xbuf);
+  else
+    s = tf_compress(c, d, T, Omega, prm->mlsvd_tol, prm->eig_maxiter, 0.0, U, (double*)c->cpdSig.p, S, rk,
+                    res->eig_iters);
+  if (s) return s;
   for (int l = 0; l < 3; ++l) res->ranks[l] = rk[l];
   // 2. initialisation on the core
   if (prm->init) {
@@ -548,12 +621,14 @@ tf_status tf_cpd(tf_ctx* c, tf_dims d, const double* T, const double* Omega, con
     woff += rk[l] * R;
     ooff += dims[l] * R;
   }
-  // 5. relative error on the original tensor (one fused evaluation), then the unit-column form
+  // 5. relative error on the original tensor (one F-only evaluation of the local slices, summed over the
+  //    ranks with ||T||^2), then the unit-column form
   double* scal = (double*)c->cpdScal.p;
   double* part = scal + 8;
   TF_CUDA(c, launch_tsums(d.I, d.J, d.K, d.ldT, T, part, scal, c->stream));
   c->total_launches += 1;
   if ((s = eval_f_only(c, d, T, W, scal + 2, (double*)c->cpdGrad.p))) return s;
+  if ((s = exchange(c, xfn, xuser, xbuf, scal, 3))) return s;
   TF_CUDA(c, launch_normalize_cpd(dims, R, W, lambda, c->stream));
   c->total_launches += 1;
   double h[3];
@@ -561,6 +636,39 @@ tf_status tf_cpd(tf_ctx* c, tf_dims d, const double* T, const double* Omega, con
   TF_CUDA(c, cudaStreamSynchronize(c->stream));
   res->rel_err = h[1] > 0.0 ? std::sqrt(2.0 * std::max(h[2], 0.0) / h[1]) : 0.0;
   return TF_OK;
+}
+
+tf_status check_cpd_args(tf_ctx* c, const tf_dims& d, const double* T, const double* Omega, const double* w0_core,
+                         const tf_cpd_params* prm, double* W, double* lambda, tf_cpd_result* res) {
+  if (!T || !Omega || !prm || !W || !lambda || !res) return set_err(c, TF_ERR_ARG, "null pointer");
+  if (!prm->init && !w0_core) return set_err(c, TF_ERR_ARG, "init = 0 needs w0_core");
+  if (d.R < 1 || d.R > TF_MAX_R) return set_err(c, d.R < 1 ? TF_ERR_ARG : TF_ERR_UNSUPPORTED, "bad R");
+  if (!(prm->mlsvd_tol > 0.0) || prm->eig_maxiter < 1) return set_err(c, TF_ERR_ARG, "bad compression parameters");
+  return TF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+tf_status tf_cpd(tf_ctx* c, tf_dims d, const double* T, const double* Omega, const double* w0_core,
+                 const tf_cpd_params* prm, double* W, double* lambda, tf_cpd_result* res, double* hist) {
+  tf_status s = check_whole(c, d);
+  if (s) return s;
+  if ((s = check_cpd_args(c, d, T, Omega, w0_core, prm, W, lambda, res))) return s;
+  cudaSetDevice(c->device);
+  return cpd_impl(c, d, T, Omega, w0_core, prm, W, lambda, res, hist, nullptr, nullptr, nullptr);
+}
+
+tf_status tf_cpd_sharded(tf_ctx* c, tf_dims d, const double* T_local, const double* Omega, const double* w0_core,
+                         const tf_cpd_params* prm, double* W, double* lambda, tf_cpd_result* res, double* hist,
+                         tf_allreduce_fn allreduce, void* user, double* xbuf) {
+  tf_status s = check_shard(c, d);
+  if (s) return s;
+  if ((s = check_cpd_args(c, d, T_local, Omega, w0_core, prm, W, lambda, res))) return s;
+  if (!allreduce || !xbuf) return set_err(c, TF_ERR_ARG, "null all-reduce hook or exchange buffer");
+  cudaSetDevice(c->device);
+  return cpd_impl(c, d, T_local, Omega, w0_core, prm, W, lambda, res, hist, allreduce, user, xbuf);
 }
 
 }  // extern "C"

@@ -100,3 +100,18 @@ def sharded_dgn(ctx, I: int, J: int, K: int, R: int, T_local: torch.Tensor, w: t
     k0, k1 = shard_range(K, rank, world)
     d = Dims(I, J, k1 - k0, R, K_total=K, k_begin=k0)
     return ctx.tf_cpd_dgn_sharded(d, T_local, w, cg_iters, allreduce_hook(group), **kw)
+
+
+def sharded_cpd(ctx, I: int, J: int, K: int, R: int, T_local: torch.Tensor, Omega: torch.Tensor, cg_iters,
+                rank: int | None = None, world: int | None = None, group=None, **kw):
+    """The whole Tensor Fox flow over K-sharded ranks (ST-MLSVD compression with the Grams and the mode-3
+    intermediate all-reduced, then the dGN on the core and the uncompression replicated): returns what
+    Context.tf_cpd_sharded returns, identical on every rank."""
+    from . import Dims
+    if world is None:
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if rank is None:
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+    k0, k1 = shard_range(K, rank, world)
+    d = Dims(I, J, k1 - k0, R, K_total=K, k_begin=k0)
+    return ctx.tf_cpd_sharded(d, T_local, Omega, cg_iters, allreduce_hook(group), **kw)

@@ -381,3 +381,114 @@ def test_tf_cpd_sequential_compression(ctx):
     a, b, c = (Wn[:I * R].reshape(R, I).T, Wn[I * R:(I + J) * R].reshape(R, J).T, Wn[(I + J) * R:].reshape(R, K).T)
     rec = np.einsum("r,ir,jr,kr->ijk", to_np(lam), a, b, c)
     assert abs(np.linalg.norm(t - rec) / np.linalg.norm(t) - out["rel_err"]) <= 1e-2 * out["rel_err"] + 1e-14
+
+
+# ------------------------------------------------------------------------- K-sharded compression and flow
+def _run_ranks(world, fn):
+    """Run fn(rank, hook) on `world` host threads, each with its own context and stream on this GPU; hook(buf)
+    sums the ranks' buffers on the host side (no kernel waits on another rank's kernels)."""
+    import threading
+    bufs = [None] * world
+    outs = [None] * world
+    errs = []
+    barrier = threading.Barrier(world)
+
+    def hook_for(rank):
+        def hook(buf):
+            bufs[rank] = buf
+            barrier.wait()
+            if rank == 0:
+                total = bufs[0].clone()
+                for r in range(1, world):
+                    total += bufs[r]
+                torch.cuda.synchronize()
+                for r in range(world):
+                    bufs[r].copy_(total)
+                torch.cuda.synchronize()
+            barrier.wait()
+        return hook
+
+    def run(rank):
+        try:
+            torch.cuda.set_device(0)
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                c = tf.Context(0, stream)
+                outs[rank] = fn(rank, c, hook_for(rank))
+                torch.cuda.synchronize()
+                c.close()
+        except Exception as e:   # surface in the main thread
+            errs.append(e)
+            barrier.abort()
+
+    ths = [threading.Thread(target=run, args=(r,)) for r in range(world)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    if errs:
+        raise errs[0]
+    return outs
+
+
+@pytest.mark.parametrize("name,dims,world", [("c3", (80, 70, 60, 12), 3), ("c4", (120, 64, 40, 20), 2)])
+def test_compress_st_sharded_matches_single_device(ctx, name, dims, world):
+    """tf_compress_st_sharded over K-shards equals tf_compress_st on the whole tensor (only the reduction order of
+    the all-reduced Grams differs): same ranks, sigma, U (where unique) and core; every rank holds the same."""
+    from paper_2110_05997_b200.dist import shard_range
+    Pb = synth.make_problem(name, "cpu", dims=dims)
+    c = Pb.cfg
+    I, J, K, R = c.I, c.J, c.K, c.R
+    Om = synth.omega_blocks((I, J, K), R, "cpu").cuda()
+    ref = ctx.tf_compress(tf.Dims(I, J, K, R), Pb.T.cuda(), Om, mlsvd_tol=1e-6, sequential=True)
+    torch.cuda.synchronize()
+
+    def fn(rank, c_, hook):
+        k0, k1 = shard_range(K, rank, world)
+        Tl = Pb.T[k0:k1].contiguous().cuda()
+        out = c_.tf_compress_st_sharded(tf.Dims(I, J, k1 - k0, R, K_total=K, k_begin=k0), Tl, Om, hook,
+                                        mlsvd_tol=1e-6)
+        return {k: ([to_np(x) for x in v] if isinstance(v, list) and v and isinstance(v[0], torch.Tensor)
+                    else (to_np(v) if isinstance(v, torch.Tensor) else v)) for k, v in out.items()}
+
+    outs = _run_ranks(world, fn)
+    for o in outs:
+        assert o["ranks"] == ref["ranks"]
+        for l, n in enumerate((I, J, K)):
+            P = min(n, R)
+            lam_ref = to_np(ref["sigma"][l]) ** 2
+            check_eig(o["sigma"][l] ** 2, colmaj(o["U"][l], n, P), lam_ref, colmaj(to_np(ref["U"][l]), n, P), n,
+                      (name, l), base=1e-9)
+        assert np.linalg.norm(o["S"] - to_np(ref["S"])) <= 1e-9 * np.linalg.norm(to_np(Pb.T))
+    for o in outs[1:]:
+        assert np.array_equal(o["S"], outs[0]["S"])
+
+
+def test_cpd_sharded_matches_single_device(ctx):
+    """The K-sharded flow (tf_cpd_sharded) on 2 ranks against tf_cpd (sequential) on the whole tensor: same ranks,
+    the dGN on the (identical up to rounding) core takes the same first steps, and the fits agree."""
+    from paper_2110_05997_b200.dist import shard_range
+    I, J, K, R = 40, 30, 24, 3
+    A, B, C = (synth.randn((n, R), torch.device("cpu"), "cpd-shard", n).numpy() for n in (I, J, K))
+    t = np.einsum("ir,jr,kr->ijk", A, B, C) + 1e-3 * synth.randn((I, J, K), torch.device("cpu"), "cpd-shard-n").numpy()
+    T = torch.from_numpy(jac.storage_from_tensor(t)).reshape(K, J, I)
+    Om = synth.omega_blocks((I, J, K), R, "cpu").cuda()
+    cgi = synth.cg_budget(40, seed=8)
+    W, lam, ref, href = ctx.tf_cpd(tf.Dims(I, J, K, R), T.reshape(-1).cuda(), Om, cgi, maxiter=40, tol=1e-10,
+                                   sequential=True)
+    world = 2
+
+    def fn(rank, c_, hook):
+        k0, k1 = shard_range(K, rank, world)
+        Tl = T[k0:k1].contiguous().cuda()
+        Wr, lr, out, hist = c_.tf_cpd_sharded(tf.Dims(I, J, k1 - k0, R, K_total=K, k_begin=k0), Tl, Om, cgi, hook,
+                                              maxiter=40, tol=1e-10)
+        return to_np(Wr), to_np(lr), out, hist
+
+    outs = _run_ranks(world, fn)
+    for Wr, lr, out, hist in outs:
+        assert out["ranks"] == ref["ranks"]
+        n0 = min(6, len(hist), len(href))
+        assert np.allclose(hist[:n0, 0], href[:n0, 0], rtol=1e-8)
+        assert abs(out["rel_err"] - ref["rel_err"]) <= 1e-3 * ref["rel_err"] + 1e-12
+    assert np.array_equal(outs[0][0], outs[1][0])
