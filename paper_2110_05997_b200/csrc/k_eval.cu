@@ -26,6 +26,9 @@ namespace tfk {
 #define TF_P3_UNROLL 4
 #endif
 constexpr int kP3Unroll = TF_P3_UNROLL;   // Pi-form phase-3 k-loop unroll (development knob)
+#ifndef TF_TMEM_A
+#define TF_TMEM_A 1   // 1: phase-3 A fragments in tensor memory; 2: phase-2 B fragments instead; 0: neither
+#endif
 
 // Tile geometry: a CTA owns a BT x BT tile (BT = 64: 8 warps, 1 CTA/SM; BT = 32: 4 warps, 2 CTAs/SM).
 template <int BT>
@@ -127,6 +130,12 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
   // or, in the Pi pass with R > 32, with unscaled A and the per-slice scaling on the product (measured: c4/c5
   // 6%/2.5% faster; for R <= 32 the rebuild is cheaper than the extra accumulators, c3 9%)
   constexpr bool kPre = RECON || NT <= 4;
+  // Pi pass with the unscaled A: phase 3's A fragments are the same for every slice and every warp, so they
+  // are parked once in tensor memory (16 k-steps x NT4 doubles per lane = 512 columns) and read with
+  // tcgen05.ld instead of 13 shared-memory loads per k-step
+  constexpr bool kTmemA = !kPre && TF_TMEM_A == 1;
+  constexpr bool kTmemB = !kPre && TF_TMEM_A == 2;
+  constexpr int NT4 = 4 * ((NT + 3) / 4);
   constexpr int kBI = Gm::BI, kBJ = Gm::BJ, kLDE = Gm::LDE, NW = Gm::NW, kThreads = Gm::THREADS;
   constexpr int MF = Gm::MF, NF = Gm::NF;
   constexpr int kTileBytes = Gm::TILE_BYTES;
@@ -135,6 +144,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
   constexpr int NV = ((NT + 3) / 4) * 4;   // dF/dC values per lane, padded for the butterfly
   constexpr int NT1 = (NT + 1) / 2;        // r-tiles of phase 2 before the sAc hand-off
   extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint32_t tmem_base_s;
   double* sTE = reinterpret_cast<double*>(smem + S::off_te);
   double* sAc = reinterpret_cast<double*>(smem + S::off_a);   // -A diag(c_k)
   double* sB = reinterpret_cast<double*>(smem + S::off_b);    // B (unscaled)
@@ -235,6 +245,53 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
     for (int t = 0; t < NT; ++t)
 #pragma unroll
       for (int e = 0; e < 2; ++e) Areg[t][e] = sAc[(8 * warp + 2 * q + e) * LDF + 8 * t + g];
+  }
+  uint32_t ta = 0;
+  if constexpr (kTmemB) {   // phase-2 B fragments B[4s + q][8t + g], per lane: t-major, 16 k-steps per t
+    if (warp == 0) tmem_alloc(&tmem_base_s, 512);
+    tmem_fence_before_sync();
+    __syncthreads();
+    tmem_fence_after_sync();
+    ta = tmem_base_s + ((uint32_t)(32 * (warp & 3)) << 16);
+    if (warp < 4) {
+#pragma unroll 1
+      for (int t = 0; t < NT; ++t) {
+#pragma unroll
+        for (int s0 = 0; s0 < kBJ / 4; s0 += 4) {
+          double v[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) v[j] = sB[(4 * (s0 + j) + q) * LDF + 8 * t + g];
+          tmem_st4(ta + 2 * (t * 16 + s0), v);
+        }
+      }
+      tmem_wait_st();
+    }
+    tmem_fence_before_sync();
+    __syncthreads();
+    tmem_fence_after_sync();
+  }
+  if constexpr (kTmemA) {
+    if (warp == 0) tmem_alloc(&tmem_base_s, 512);
+    tmem_fence_before_sync();
+    __syncthreads();
+    tmem_fence_after_sync();
+    ta = tmem_base_s + ((uint32_t)(32 * (warp & 3)) << 16);
+    if (warp < 4) {   // one warp per lane quadrant writes the fragments A[4s + q][8t + g] of every (s, t)
+#pragma unroll 1
+      for (int s2 = 0; s2 < kBI / 4; ++s2) {
+#pragma unroll
+        for (int t0 = 0; t0 < NT4; t0 += 4) {
+          double v[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) v[j] = (t0 + j < NT) ? sAc[(4 * s2 + q) * LDF + 8 * (t0 + j) + g] : 0.0;
+          tmem_st4(ta + 2 * (s2 * NT4 + t0), v);
+        }
+      }
+      tmem_wait_st();
+    }
+    tmem_fence_before_sync();
+    __syncthreads();
+    tmem_fence_after_sync();
   }
   auto rebuild_sAc = [&](const double* c) {
 #pragma unroll
@@ -347,11 +404,23 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
       for (int t = 0; t < NT; ++t) Qt[t][0] = Qt[t][1] = 0.0;
       const double* pe = sT + (8 * warp + g) * kLDE + q;
       const double* pa = sAc + q * LDF + g;
-#pragma unroll kP3Unroll
-      for (int s = 0; s < kBI / 4; ++s) {
-        const double bb = pe[4 * s];
+      if constexpr (kTmemA) {
+#pragma unroll 2
+        for (int s = 0; s < kBI / 4; ++s) {
+          double af[NT];
+          tmem_ld_doubles<NT>(ta + 2 * s * NT4, af);
+          const double bb = pe[4 * s];
+          tmem_wait_ld();
 #pragma unroll
-        for (int t = 0; t < NT; ++t) dmma(Qt[t], pa[4 * s * LDF + 8 * t], bb);
+          for (int t = 0; t < NT; ++t) dmma(Qt[t], af[t], bb);
+        }
+      } else {
+#pragma unroll kP3Unroll
+        for (int s = 0; s < kBI / 4; ++s) {
+          const double bb = pe[4 * s];
+#pragma unroll
+          for (int t = 0; t < NT; ++t) dmma(Qt[t], pa[4 * s * LDF + 8 * t], bb);
+        }
       }
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
@@ -390,10 +459,21 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
         }
         double p0[2] = {0.0, 0.0}, p1[2] = {0.0, 0.0};
         const double* pbt = sB + q * LDF + 8 * t + g;
+        if constexpr (kTmemB) {
+          double bf[16];
+          tmem_ld_d16(ta + 32 * t, bf);
+          tmem_wait_ld();
 #pragma unroll
-        for (int s = 0; s < kBJ / 4; s += 2) {
-          dmma(p0, pbt[(4 * s) * LDF], ea[s]);
-          dmma(p1, pbt[(4 * s + 4) * LDF], ea[s + 1]);
+          for (int s = 0; s < kBJ / 4; s += 2) {
+            dmma(p0, bf[s], ea[s]);
+            dmma(p1, bf[s + 1], ea[s + 1]);
+          }
+        } else {
+#pragma unroll
+          for (int s = 0; s < kBJ / 4; s += 2) {
+            dmma(p0, pbt[(4 * s) * LDF], ea[s]);
+            dmma(p1, pbt[(4 * s + 4) * LDF], ea[s + 1]);
+          }
         }
         const double cr = sc[8 * t + g];
         const double P0 = p0[0] + p1[0], P1 = p0[1] + p1[1];   // P[i = 8w+2q+e][r = 8t+g]
@@ -430,6 +510,10 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
   }
   __syncthreads();
   TLC(2);
+  if constexpr (kTmemA || kTmemB) {
+    tmem_fence_after_sync();
+    if (warp == 0) tmem_dealloc(tmem_base_s, 512);
+  }
   if (nk > 0 && tid < RP) {
     const double* gsrc = sGC + ((nk - 1) & 1) * NW * RP;
     double v = 0.0;
