@@ -136,6 +136,9 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
   constexpr bool kTmemA = !kPre && TF_TMEM_A == 1;
   constexpr bool kTmemB = !kPre && TF_TMEM_A == 2;
   constexpr int NT4 = 4 * ((NT + 3) / 4);
+  // sAc pitch: with the fragments in TMEM the only per-slice reads of sAc are dF/dC's rows 8w + 2q + e, which a
+  // pitch = 2 (mod 8) doubles makes conflict-free (2 * pitch = 4 mod 16); otherwise the fragment pitch LDF
+  constexpr int LDA = kTmemA ? 8 * NT + 2 : S::LDF;
   constexpr int kBI = Gm::BI, kBJ = Gm::BJ, kLDE = Gm::LDE, NW = Gm::NW, kThreads = Gm::THREADS;
   constexpr int MF = Gm::MF, NF = Gm::NF;
   constexpr int kTileBytes = Gm::TILE_BYTES;
@@ -216,20 +219,20 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
         if (idx < kBJ * LDF) sB[(idx % kBJ) * LDF + idx / kBJ] = v[u];
       }
     }
-    for (int base = tid; base < kBI * LDF; base += kLoadBatch * kThreads) {
+    for (int base = tid; base < kBI * LDA; base += kLoadBatch * kThreads) {
       double v[kLoadBatch];
 #pragma unroll
       for (int u = 0; u < kLoadBatch; ++u) {
         const int idx = base + u * kThreads;
         const int i = idx % kBI, r = idx / kBI;
         const int64_t gi = i0 + i;
-        const bool ok = idx < kBI * LDF && gi < p.I && r < p.R;
+        const bool ok = idx < kBI * LDA && gi < p.I && r < p.R;
         v[u] = ok ? p.A[gi + p.I * r] : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < kLoadBatch; ++u) {
         const int idx = base + u * kThreads;
-        if (idx < kBI * LDF) sAc[(idx % kBI) * LDF + idx / kBI] = v[u];
+        if (idx < kBI * LDA) sAc[(idx % kBI) * LDA + idx / kBI] = v[u];
       }
     }
   }
@@ -244,7 +247,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
 #pragma unroll
     for (int t = 0; t < NT; ++t)
 #pragma unroll
-      for (int e = 0; e < 2; ++e) Areg[t][e] = sAc[(8 * warp + 2 * q + e) * LDF + 8 * t + g];
+      for (int e = 0; e < 2; ++e) Areg[t][e] = sAc[(8 * warp + 2 * q + e) * LDA + 8 * t + g];
   }
   uint32_t ta = 0;
   if constexpr (kTmemB) {   // phase-2 B fragments B[4s + q][8t + g], per lane: t-major, 16 k-steps per t
@@ -283,7 +286,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
         for (int t0 = 0; t0 < NT4; t0 += 4) {
           double v[4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) v[j] = (t0 + j < NT) ? sAc[(4 * s2 + q) * LDF + 8 * (t0 + j) + g] : 0.0;
+          for (int j = 0; j < 4; ++j) v[j] = (t0 + j < NT) ? sAc[(4 * s2 + q) * LDA + 8 * (t0 + j) + g] : 0.0;
           tmem_st4(ta + 2 * (s2 * NT4 + t0), v);
         }
       }
@@ -297,8 +300,8 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
 #pragma unroll
     for (int t = 0; t < NT; ++t) {
       const double cr = -c[8 * t + g];
-      sAc[(8 * warp + 2 * q) * LDF + 8 * t + g] = Areg[t][0] * cr;
-      sAc[(8 * warp + 2 * q + 1) * LDF + 8 * t + g] = Areg[t][1] * cr;
+      sAc[(8 * warp + 2 * q) * LDA + 8 * t + g] = Areg[t][0] * cr;
+      sAc[(8 * warp + 2 * q + 1) * LDA + 8 * t + g] = Areg[t][1] * cr;
     }
   };
   if (nk > 0) {
@@ -336,7 +339,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
 #pragma unroll
           for (int e = 0; e < 2; ++e)
             E[m][n][e] = sT[(16 * wj + 8 * n + 2 * q + e) * kLDE + (kBI / 2) * wi + 8 * m + g];
-      const double* pa = sAc + ((kBI / 2) * wi + g) * LDF + q;
+      const double* pa = sAc + ((kBI / 2) * wi + g) * LDA + q;
       const double* pb = sB + (16 * wj + g) * LDF + q;
 #pragma unroll
       for (int s = 0; s < RP / 4; ++s) {
@@ -388,7 +391,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
     // ---- phase 3: accB^T += (-A diag c)^T E for j-cols 8*warp.., all R (prescaled sAc: no DMUL)
     if constexpr (kPre) {
       const double* pe = sT + (8 * warp + g) * kLDE + q;
-      const double* pa = sAc + q * LDF + g;
+      const double* pa = sAc + q * LDA + g;
 #pragma unroll 4
       for (int s = 0; s < kBI / 4; ++s) {
         const double bb = pe[4 * s];
@@ -403,7 +406,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
 #pragma unroll
       for (int t = 0; t < NT; ++t) Qt[t][0] = Qt[t][1] = 0.0;
       const double* pe = sT + (8 * warp + g) * kLDE + q;
-      const double* pa = sAc + q * LDF + g;
+      const double* pa = sAc + q * LDA + g;
       if constexpr (kTmemA) {
 #pragma unroll 2
         for (int s = 0; s < kBI / 4; ++s) {
@@ -482,8 +485,8 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
         if constexpr (kPre) {
           gcv[t] = fma(Areg[t][0], P0, Areg[t][1] * P1);
         } else {
-          const double* pa = sAc + (8 * warp + 2 * q) * LDF + 8 * t + g;
-          gcv[t] = fma(pa[0], P0, pa[LDF] * P1);
+          const double* pa = sAc + (8 * warp + 2 * q) * LDA + 8 * t + g;
+          gcv[t] = fma(pa[0], P0, pa[LDA] * P1);
         }
       }
       if (kPre && NT1 >= NT && kk + 1 < nk) {   // NT == 1: hand-off after the only tile
