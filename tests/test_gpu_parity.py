@@ -150,6 +150,23 @@ def test_host_streamed_eval_matches_device(ctx):
     assert rel_err(to_np(gh), gr) <= TOL
 
 
+@pytest.mark.slow
+def test_host_streamed_eval_c3_full_size(ctx):
+    """The e2e path at c3's full size (1 GB: two 512 MB slabs, each a K-shard large enough for the guarded Pi
+    form): the streamed result equals the device-resident evaluation to rounding (the slabs' partial sums
+    only change the reduction order), and the device one is pinned to the oracle by test_c3_full_size_sampled."""
+    P = synth.make_problem("c3", "cuda")
+    c = P.cfg
+    d = tf.Dims(c.I, c.J, c.K, c.R)
+    w = P.w("random")
+    fd, gd = ctx.tf_cpd_eval(d, P.T, w)
+    torch.cuda.synchronize()
+    assert ctx.eval_fell_back() == 0   # the Pi form ran
+    fh, gh = ctx.tf_cpd_eval_host(d, P.T.cpu().contiguous(), w.cpu().contiguous())
+    assert rel_err(to_np(fh), to_np(fd)) <= 1e-12
+    assert rel_err(to_np(gh), to_np(gd)) <= 1e-12
+
+
 # ------------------------------------------------------------------------- paper fixtures
 def _w_of(A, B, C):
     return np.concatenate([A.T.reshape(-1), B.T.reshape(-1), C.T.reshape(-1)])
