@@ -586,3 +586,25 @@ def test_sharded_dgn_matches_single_device(ctx):
         assert np.allclose(hist[:n0, 0], href[:n0, 0], rtol=1e-10, atol=0)
         assert np.array_equal(wr, outs[0][2])                       # every rank holds the same w
         assert np.linalg.norm(wr - to_np(wt)) <= 1e-6 * np.linalg.norm(to_np(wt))
+
+
+@pytest.mark.parametrize("dims", [(37, 29, 23, 1), (37, 29, 23, 5), (70, 66, 40, 9), (64, 64, 17, 33),
+                                  (45, 80, 30, 104), (30, 40, 25, 128), (130, 70, 20, 57)])
+def test_pi_form_shapes(ctx, dims):
+    """The guarded Pi-form pass forced at every fragment-count regime (R = 1 .. 128: the prescaled phase 3 for
+    R <= 32, the tensor-memory fragments above, R = 128 filling all 512 TMEM columns), ragged tiles, at a
+    random point (no fallback): F and grad against the oracle."""
+    I, J, K, R = dims
+    P = synth.make_problem("c2", "cpu", dims=dims)
+    T_np, w_np = to_np(P.T).reshape(-1), to_np(P.w("random"))
+    fr, gr = oracle.cpd_eval(T_np, w_np, I, J, K, R)
+    ctx.set_eval_form("pi")
+    try:
+        fd, gd = ctx.tf_cpd_eval(tf.Dims(I, J, K, R), torch.from_numpy(T_np).cuda(), torch.from_numpy(w_np).cuda())
+        torch.cuda.synchronize()
+        assert ctx.eval_fell_back() == 0
+    finally:
+        ctx.set_eval_form("auto")
+    okf, ef, bf = within([fd.item()], [fr], f_floor(T_np, fr))
+    okg, eg, bg = within(to_np(gd), gr, grad_floor(w_np, I, J, K, R))
+    assert okf and okg, (dims, ef, bf, eg, bg)
