@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
   // are parked once in tensor memory (16 k-steps x NT4 doubles per lane = 512 columns) and read with
   // tcgen05.ld instead of 13 shared-memory loads per k-step
   constexpr bool kTmemA = !kPre && TF_TMEM_A == 1;
-  constexpr bool kTmemB = !kPre && TF_TMEM_A == 2;
+  constexpr bool kTmemB = (RECON && NT > 4) || (!kPre && TF_TMEM_A == 2);   // residual form: B of phase 2 in TMEM
   constexpr int NT4 = 4 * ((NT + 3) / 4);
   // sAc pitch: with the fragments in TMEM the only per-slice reads of sAc are dF/dC's rows 8w + 2q + e, which a
   // pitch = 2 (mod 8) doubles makes conflict-free (2 * pitch = 4 mod 16); otherwise the fragment pitch LDF
