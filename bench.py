@@ -339,6 +339,12 @@ def run_ours(args):
         Ts = P.T[:k_sl].cpu().numpy().reshape(-1)
         v, sample, _ = oracle_sample(cfg, Ts, wn, k_sl, 1 if cfg.cg_iters else 0, threads)
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample}
+        # the same oracle on one host thread (BASELINE.md §4 asks for both), on a smaller slice sample
+        k1 = max(1, k_sl // max(1, threads))
+        v1, sample1, _ = oracle_sample(cfg, P.T[:k1].cpu().numpy().reshape(-1), wn, k1, 0, 1)
+        cpu["single_thread"] = {"value": v1, "unit": UNIT, "cores": 1,
+                                "sample": sample1 + " (evaluation only; the CG share is as in the multi-thread "
+                                                    "sample, negligible)"}
 
     # compression stage (NEXT #3), measured once beside the step on the resident T (not part of `value`)
     stages = None
