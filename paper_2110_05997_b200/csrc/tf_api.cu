@@ -439,7 +439,15 @@ tf_status tf_cpd_eval(tf_ctx* c, tf_dims d, const double* T, const double* w, do
   if (reinterpret_cast<uintptr_t>(T) & 7) return set_err(c, TF_ERR_ALIGN, "T not 8-byte aligned");
   cudaSetDevice(c->device);
   if ((s = eval_impl(c, d, T, w, f, grad))) return s;
-  if (grams) return grams_impl(c, d, w, grams);
+  if (grams) {
+    // the Pi-form pass already formed [A^T A | B^T B | C^T C] (the whole tensor: K == K_total)
+    if (c->last_eval_pi && d.K == d.K_total) {
+      TF_CUDA(c, cudaMemcpyAsync(grams, c->evGrams.p, (size_t)3 * d.R * d.R * 8, cudaMemcpyDeviceToDevice,
+                                 c->stream));
+      return TF_OK;
+    }
+    return grams_impl(c, d, w, grams);
+  }
   return TF_OK;
 }
 
