@@ -29,6 +29,9 @@ constexpr int kP3Unroll = TF_P3_UNROLL;   // Pi-form phase-3 k-loop unroll (deve
 #ifndef TF_TMEM_A
 #define TF_TMEM_A 1   // 1: phase-3 A fragments in tensor memory; 2: phase-2 B fragments instead; 0: neither
 #endif
+#ifndef TF_TMEM_PIPE
+#define TF_TMEM_PIPE 1   // phase-3 tensor-memory loads one k-step ahead (c4 -1.7%, c5 -0.2%)
+#endif
 
 // Tile geometry: a CTA owns a BT x BT tile (BT = 64: 8 warps, 1 CTA/SM; BT = 32: 4 warps, 2 CTAs/SM).
 template <int BT>
@@ -408,6 +411,21 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
       const double* pe = sT + (8 * warp + g) * kLDE + q;
       const double* pa = sAc + q * LDA + g;
       if constexpr (kTmemA) {
+#if TF_TMEM_PIPE
+        // the fragments of k-step s+1 are loaded before the DMMAs of step s issue; the wait for them sits
+        // after those DMMAs (fully unrolled: both fragment buffers are static registers)
+        double af[2][NT];
+        tmem_ld_doubles<NT>(ta, af[0]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int s = 0; s < kBI / 4; ++s) {
+          if (s + 1 < kBI / 4) tmem_ld_doubles<NT>(ta + 2 * (s + 1) * NT4, af[(s + 1) & 1]);
+          const double bb = pe[4 * s];
+#pragma unroll
+          for (int t = 0; t < NT; ++t) dmma(Qt[t], af[s & 1][t], bb);
+          if (s + 1 < kBI / 4) tmem_wait_ld();
+        }
+#else
 #pragma unroll 2
         for (int s = 0; s < kBI / 4; ++s) {
           double af[NT];
@@ -417,6 +435,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
 #pragma unroll
           for (int t = 0; t < NT; ++t) dmma(Qt[t], af[t], bb);
         }
+#endif
       } else {
 #pragma unroll kP3Unroll
         for (int s = 0; s < kBI / 4; ++s) {
