@@ -55,10 +55,16 @@ struct EvalSmem {
   static constexpr size_t off_a = off_te + 2 * (size_t)G::TILE_BYTES;     // [BI][LDF]
   static constexpr size_t off_b = off_a + (size_t)G::BI * LDF * 8;        // [BJ][LDF]
   static constexpr size_t off_c = off_b + (size_t)G::BJ * LDF * 8;        // 4 x [RP]  (ring of c_k rows)
-  static constexpr size_t off_gc = off_c + 4 * (size_t)RP * 8;            // 2 x [NW][RP] (per-warp dF/dC partials)
-  static constexpr size_t off_red = off_gc + 2 * G::NW * (size_t)RP * 8;  // [NW]
+  // Per-warp dF/dC rows: lane quarter q of the butterfly holds t in [q NV/4, (q+1) NV/4) and stores at
+  // 8t + g + q GCP, so each quarter's run starts 4 doubles further round the banks (conflict-free STS).
+  static constexpr int NV = ((NT + 3) / 4) * 4;
+  static constexpr int GCP = ((4 - 2 * NV) % 16 + 16) % 16;   // 2 NV + GCP = 4 mod 16
+  static constexpr int GCS = RP + 3 * GCP;                     // row stride of the dF/dC partials
+  static constexpr size_t off_gc = off_c + 4 * (size_t)RP * 8;            // 2 x [NW][GCS] (per-warp dF/dC partials)
+  static constexpr size_t off_red = off_gc + 2 * G::NW * (size_t)GCS * 8; // [NW]
   static constexpr size_t off_bar = off_red + G::NW * 8;                  // 4 mbarriers: full[2], p3done, aready
   static constexpr size_t bytes = off_bar + 4 * 8;
+  static_assert(bytes <= 232448, "exceeds the 227 KB per-CTA shared memory of sm_100a");
 };
 
 // Butterfly sum over the 4 lanes that share g = lane/4 (lane bits 0..1) of N values per lane;
@@ -383,10 +389,10 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
       }
     }
     if (kk > 0 && tid < RP) {
-      const double* gsrc = sGC + ((kk - 1) & 1) * NW * RP;
+      const double* gsrc = sGC + ((kk - 1) & 1) * NW * S::GCS + tid + ((tid >> 3) / (NV / 4)) * S::GCP;
       double v = 0.0;
 #pragma unroll
-      for (int w = 0; w < NW; ++w) v += gsrc[w * RP + tid];
+      for (int w = 0; w < NW; ++w) v += gsrc[w * S::GCS];
       p.gCp[((int64_t)(it * p.nTj + jt) * p.K + (k - 1)) * RP + tid] = v;
     }
     if (kk + 2 < nk) load_c(k + 2, (kk + 2) & 3);
@@ -517,7 +523,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
       TL(kk, 7);
       butterfly4<NV>(gcv, q);
       const int base = ((q >> 1) & 1) * (NV / 2) + (q & 1) * (NV / 4);
-      double* gdst = sGC + (kk & 1) * NW * RP + warp * RP;
+      double* gdst = sGC + (kk & 1) * NW * S::GCS + warp * S::GCS + q * S::GCP;
 #pragma unroll
       for (int j = 0; j < NV / 4; ++j) {
         const int t = base + j;
@@ -537,10 +543,10 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
     if (warp == 0) tmem_dealloc(tmem_base_s, 512);
   }
   if (nk > 0 && tid < RP) {
-    const double* gsrc = sGC + ((nk - 1) & 1) * NW * RP;
+    const double* gsrc = sGC + ((nk - 1) & 1) * NW * S::GCS + tid + ((tid >> 3) / (NV / 4)) * S::GCP;
     double v = 0.0;
 #pragma unroll
-    for (int w = 0; w < NW; ++w) v += gsrc[w * RP + tid];
+    for (int w = 0; w < NW; ++w) v += gsrc[w * S::GCS];
     p.gCp[((int64_t)(it * p.nTj + jt) * p.K + (kB - 1)) * RP + tid] = v;
   }
 
