@@ -169,7 +169,7 @@ __host__ __device__ constexpr int apply_rows() { return NT > 13 ? 16 : 32; }
 
 template <int NT>
 __host__ __device__ constexpr size_t apply_smem_doubles(int R4) {
-  return (size_t)3 * apply_rows<NT>() * (R4 + 4) + (size_t)(2 * R4) * (8 * ((NT + 1) / 2) + 4);
+  return (size_t)3 * R4 * (apply_rows<NT>() + 8) + (size_t)(2 * R4) * (8 * ((NT + 1) / 2) + 4);
 }
 
 template <int NT>
@@ -184,11 +184,12 @@ __device__ double stage_apply(const CgArgs& A, const VSrc& V, double* y, double*
   const int R = (int)m.R;
   const int64_t RR = (int64_t)R * R;
   const int R4 = 4 * ((R + 3) / 4);
-  const int LDX = R4 + 4;                    // 4 mod 8 in doubles -> conflict-free A fragments
-  double* sXr = smem;                        // [YR][LDX]
-  double* sXp = sXr + YR * LDX;
-  double* sW = sXp + YR * LDX;
-  double* sM = sW + YR * LDX;                // [2 R4][LDM]
+  constexpr int LDX = YR + 8;                // [r][row] staging, 8 mod 16 doubles: conflict-free copies
+                                             // (consecutive rows) and A fragments (lane (g,q) -> 8q + g)
+  double* sXr = smem;                        // [R4][LDX]
+  double* sXp = sXr + R4 * LDX;
+  double* sW = sXp + R4 * LDX;
+  double* sM = sW + R4 * LDX;                // [2 R4][LDM]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
   const int mt = warp % MT, tw = warp / MT;
   const int nh = NT > 1 ? 2 : 1;
@@ -199,7 +200,9 @@ __device__ double stage_apply(const CgArgs& A, const VSrc& V, double* y, double*
   }
   const double bet = V.b ? V.beta : 0.0;
   double dsum = 0.0;
-  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+  int nit = 0;
+  for (int item = blockIdx.x; item < items; item += gridDim.x, ++nit) {
+    stamp(A, 40 + 4 * nit);
     int l = 0, c = item;
     while (c >= chunks[l]) {
       c -= chunks[l];
@@ -222,12 +225,17 @@ __device__ double stage_apply(const CgArgs& A, const VSrc& V, double* y, double*
       const int a = idx % YR, kk = idx / YR;
       const bool ok = kk < R && a0 + a < n;
       const int64_t ix = ok ? a0 + a + n * kk : 0;
-      cp_async8(&sXr[a * LDX + kk], va + ix, ok);
-      cp_async8(&sXp[a * LDX + kk], vb + ix, ok && V.b != nullptr);
-      cp_async8(&sW[a * LDX + kk], W + ix, ok);
+      cp_async8(&sXr[kk * LDX + a], va + ix, ok);
+      cp_async8(&sXp[kk * LDX + a], vb + ix, ok && V.b != nullptr);
+      cp_async8(&sW[kk * LDX + a], W + ix, ok);
     }
-    for (int idx = threadIdx.x; idx < R4 * 8 * NTH; idx += blockDim.x) {
-      const int kk = idx % R4, cc = idx / R4;
+    // [Pi; S] columns: a warp copies 8 consecutive k x 4 columns (64-byte global runs; the shared-memory
+    // rows kk*LDM, LDM = 4 mod 8, land on distinct banks)
+    const int nkb = (R4 + 7) / 8;
+    for (int idx = threadIdx.x; idx < nkb * 8 * 8 * NTH; idx += blockDim.x) {
+      const int ln = idx & 31, blk = idx >> 5;
+      const int kk = 8 * (blk % nkb) + (ln & 7), cc = 4 * (blk / nkb) + (ln >> 3);
+      if (kk >= R4) continue;
       const bool ok = kk < R && s_lo + cc < R;
       const int64_t ix = ok ? kk + (int64_t)R * (s_lo + cc) : 0;
       cp_async8(&sM[kk * LDM + cc], P + ix, ok);
@@ -235,6 +243,7 @@ __device__ double stage_apply(const CgArgs& A, const VSrc& V, double* y, double*
     }
     cp_async_wait_all();
     __syncthreads();
+    stamp(A, 41 + 4 * nit);
     double acc[NTW][2] = {};
     const int row = 8 * mt + g;
     // V Pi^(l): A fragment = D_r (r + beta p)
@@ -242,7 +251,7 @@ __device__ double stage_apply(const CgArgs& A, const VSrc& V, double* y, double*
     for (int ks = 0; ks < R4 / 4; ++ks) {
       const int r = 4 * ks + q;
       const double dr = D ? D[min(r, R - 1)] : 1.0;
-      const double fa = dr * fma(bet, sXp[row * LDX + r], sXr[row * LDX + r]);
+      const double fa = dr * fma(bet, sXp[r * LDX + row], sXr[r * LDX + row]);
 #pragma unroll
       for (int j = 0; j < NTW; ++j) {
         const int tl = tw + WG * j;
@@ -253,13 +262,14 @@ __device__ double stage_apply(const CgArgs& A, const VSrc& V, double* y, double*
 #pragma unroll 4
     for (int ks = 0; ks < R4 / 4; ++ks) {
       const int r = 4 * ks + q;
-      const double fa = sW[row * LDX + r];
+      const double fa = sW[r * LDX + row];
 #pragma unroll
       for (int j = 0; j < NTW; ++j) {
         const int tl = tw + WG * j;
         if (tl < NTH && t0 + tl < NT) dmma(acc[j], fa, sM[(R4 + r) * LDM + 8 * tl + g]);
       }
     }
+    stamp(A, 42 + 4 * nit);
     // epilogue: row a = a0 + 8 mt + g, cols s = 8 (t0 + tl) + 2q + e
     const int64_t arow = a0 + row;
     const bool rok = arow < n;
@@ -272,7 +282,7 @@ __device__ double stage_apply(const CgArgs& A, const VSrc& V, double* y, double*
         pnew[j][e] = 0.0;
         const int sc = 8 * (t0 + tl) + 2 * q + e;
         if (tl < NTH && rok && sc < R) {
-          const double pr = fma(bet, sXp[row * LDX + sc], sXr[row * LDX + sc]);
+          const double pr = fma(bet, sXp[sc * LDX + row], sXr[sc * LDX + row]);
           const double ds = D ? D[sc] : 1.0;
           const double lam = A.damp ? A.lambda * A.damp[l * R + sc] : A.lambda;
           const double yv = ds * fma(lam, ds * pr, acc[j][e]);
@@ -516,5 +526,9 @@ extern "C" void tf_cg_debug_dump(void) {
     printf("iter %d: gram %.2f us, sync %.2f, S+sync %.2f, apply %.2f, sync+alpha %.2f, update %.2f us\n", it + 1,
            (b[1] - b[0]) * 1e-3, (b[2] - b[1]) * 1e-3, (b[3] - b[2]) * 1e-3, (b[4] - b[3]) * 1e-3,
            (b[5] - b[4]) * 1e-3, (b[6] - b[5]) * 1e-3);
+  }
+  for (int i = 0; i < 2; ++i) {
+    const unsigned long long* b = h + 40 + 4 * i;
+    printf("apply item %d: staging %.2f us, compute %.2f us, epilogue->next %.2f us\n", i, (b[1] - b[0]) * 1e-3, (b[2] - b[1]) * 1e-3, (b[4] - b[2]) * 1e-3);
   }
 }
