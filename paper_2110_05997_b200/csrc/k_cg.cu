@@ -33,7 +33,7 @@ struct CgArgs {
   const double* rhs;      // CG right-hand side (w-coordinates)
   const double* v;        // matvec input (matvec mode)
   double* x;              // CG solution / matvec output y
-  double *r, *p, *z;      // CG vectors
+  double *r, *p, *z;      // CG vectors; p holds 2n doubles: the current and the next direction
   double* G;              // kGramZ x 3 x R x R Gram partials
   double* S;              // 3 x R x R
   double* part;           // 2 * gridDim partials
@@ -370,8 +370,12 @@ __global__ void __launch_bounds__(kCgThreads, 1) k_cg_persistent(CgArgs A) {
   double rr = grid_total(part1, red);
   double beta = 0.0;
   int iters = 0, nonfinite = 0;
+  // The apply stage writes the new direction into the other half of p: blocks that still stage rows of the
+  // current direction (the other column half of the same rows) never see a partially updated vector.
+  double* pc = A.p;
+  double* pn = A.p + n;
   for (int it = 1; it <= A.maxiter; ++it) {
-    VSrc V{A.r, A.p, beta, A.dscale};
+    VSrc V{A.r, pc, beta, A.dscale};
     const int sb = 8 * (it - 1);
     stamp(A, sb + 0);
     stage_gram(A, V, red);
@@ -381,8 +385,8 @@ __global__ void __launch_bounds__(kCgThreads, 1) k_cg_persistent(CgArgs A) {
     stage_s(A);
     grid.sync();
     stamp(A, sb + 3);
-    // z = B p_new, p <- p_new, partial <p, z>
-    const double pz_part = stage_apply<NT>(A, V, A.z, A.p, cg_smem);
+    // z = B p_new, pn <- p_new, partial <p_new, z>
+    const double pz_part = stage_apply<NT>(A, V, A.z, pn, cg_smem);
     stamp(A, sb + 4);
     const double pzb = block_reduce(pz_part, red);
     if (threadIdx.x == 0) part0[blockIdx.x] = pzb;
@@ -400,7 +404,7 @@ __global__ void __launch_bounds__(kCgThreads, 1) k_cg_persistent(CgArgs A) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int64_t qi = min(q0 + u * stride, n - 1);
-        xp[u] = A.p[qi];
+        xp[u] = pn[qi];
         xx[u] = A.x[qi];
         xz[u] = A.z[qi];
         xr[u] = A.r[qi];
@@ -424,6 +428,9 @@ __global__ void __launch_bounds__(kCgThreads, 1) k_cg_persistent(CgArgs A) {
     beta = rr_new / rr;
     rr = rr_new;
     iters = it;
+    double* const tswap = pc;
+    pc = pn;
+    pn = tswap;
     if (!isfinite(beta)) {
       nonfinite = it;
       break;

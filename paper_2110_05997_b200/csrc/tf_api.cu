@@ -565,7 +565,7 @@ static tf_status cg_impl(tf_ctx* c, const tf_dims& d, const double* grams, const
   tf_status s;
   if ((s = matvec_ws(c, d, m, ws))) return s;
   if ((s = ensure(c, c->cgR, n * 8))) return s;
-  if ((s = ensure(c, c->cgP, n * 8))) return s;
+  if ((s = ensure(c, c->cgP, 2 * n * 8))) return s;   // current and next CG direction
   if ((s = ensure(c, c->cgZ, n * 8))) return s;
   if ((s = ensure(c, c->cgState, sizeof(CgState)))) return s;
   CgState* st = (CgState*)c->cgState.p;
