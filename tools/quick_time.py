@@ -17,6 +17,8 @@ c = P.cfg
 print(f"{name}: generated in {time.time()-t0:.1f}s", flush=True)
 d = tf.Dims(c.I, c.J, c.K, c.R)
 ctx = tf.Context(0)
+if len(sys.argv) > 3:
+    ctx.set_eval_form(sys.argv[3])   # auto | residual | pi
 w = P.w(P.cfg.points[-1])
 f, g = ctx.tf_cpd_eval(d, P.T, w)
 torch.cuda.synchronize()
