@@ -201,15 +201,21 @@ __device__ double stage_apply(const CgArgs& A, const VSrc& V, double* y, double*
   const double bet = V.b ? V.beta : 0.0;
   double dsum = 0.0;
   int nit = 0;
-  for (int item = blockIdx.x; item < items; item += gridDim.x, ++nit) {
+  // contiguous item ranges per block, items ordered (mode, column half, row chunk): a block's consecutive
+  // items share [Pi; S] columns, which are then staged once
+  const int per = (items + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int it_end = min(items, ((int)blockIdx.x + 1) * per);
+  int staged_l = -1, staged_h = -1;
+  for (int item = (int)blockIdx.x * per; item < it_end; ++item, ++nit) {
     stamp(A, 40 + 4 * nit);
     int l = 0, c = item;
     while (c >= chunks[l]) {
       c -= chunks[l];
       ++l;
     }
-    const int h = c % nh;
-    const int64_t a0 = (int64_t)(c / nh) * YR;
+    const int nck = chunks[l] / nh;
+    const int h = c / nck;
+    const int64_t a0 = (int64_t)(c % nck) * YR;
     const int64_t n = m.n[l];
     const int64_t off = m.off[l];
     const double* W = m.W[l];
@@ -232,7 +238,10 @@ __device__ double stage_apply(const CgArgs& A, const VSrc& V, double* y, double*
     // [Pi; S] columns: a warp copies 8 consecutive k x 4 columns (64-byte global runs; the shared-memory
     // rows kk*LDM, LDM = 4 mod 8, land on distinct banks)
     const int nkb = (R4 + 7) / 8;
-    for (int idx = threadIdx.x; idx < nkb * 8 * 8 * NTH; idx += blockDim.x) {
+    const bool restage = l != staged_l || h != staged_h;
+    staged_l = l;
+    staged_h = h;
+    for (int idx = threadIdx.x; restage && idx < nkb * 8 * 8 * NTH; idx += blockDim.x) {
       const int ln = idx & 31, blk = idx >> 5;
       const int kk = 8 * (blk % nkb) + (ln & 7), cc = 4 * (blk / nkb) + (ln >> 3);
       if (kk >= R4) continue;
