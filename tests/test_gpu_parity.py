@@ -102,8 +102,18 @@ def test_padded_leading_dimension(ctx):
         assert rel_err(to_np(g), gr) <= TOL
 
 
-def test_k_sharded_partials_sum_to_full(ctx):
-    """shard partials [grad | f] summed elementwise equal the full evaluation."""
+@pytest.mark.parametrize("form", ["residual", "pi"])
+def test_k_sharded_partials_sum_to_full(ctx, form):
+    """shard partials [grad | f] summed elementwise equal the full evaluation (both
+    algebraic forms of reading R31; in the Pi form each shard uses the C Gram over its own slices)."""
+    ctx.set_eval_form(form)
+    try:
+        _sharded_partials(ctx)
+    finally:
+        ctx.set_eval_form("auto")
+
+
+def _sharded_partials(ctx):
     I, J, K, R = 50, 40, 23, 6
     rng = np.random.default_rng(11)
     t = rng.standard_normal((K, J, I))
@@ -112,7 +122,7 @@ def test_k_sharded_partials_sum_to_full(ctx):
     f_full, g_full = ctx.tf_cpd_eval(tf.Dims(I, J, K, R), Tt, w)
     acc_f = torch.zeros(1, dtype=torch.float64, device="cuda")
     acc_g = torch.zeros_like(g_full)
-    for world in (2, 3, 5):
+    for world in (2, 3, 5, 8):
         acc_f.zero_()
         acc_g.zero_()
         for rank in range(world):
