@@ -232,8 +232,7 @@ def run_ours(args):
         if world == 1:   # one call: F, grad and the Grams (which the evaluation forms anyway)
             f, g = ctx.tf_cpd_eval(dglob, P.T, w, f1, g1, grams=grams)
         else:            # local partials + one all-reduce of [grad | f]; the Grams of the full factors
-            f, g = ev(P.T, w)
-            ctx.tf_grams(dglob, w, grams)
+            f, g = ev(P.T, w, grams=grams)
         torch.neg(g, out=rhs)
         if cfg.cg_iters:
             ctx.tf_cg_solve(dglob, grams, w, rhs, cfg.lam, cfg.cg_iters, 0.0, False, x)
@@ -449,7 +448,7 @@ def run_ours(args):
                        "parallelism": f"K-sharded x{world} + 1 NCCL all-reduce of [grad|f]" if world > 1 else "1 GPU",
                        "l2": f"inputs larger than L2 (T = {cfg.t_bytes / 1e9:.2f} GB > 126 MB), no flush",
                        "step": "tf_cpd_eval (F, grad, Grams) + tf_cg_solve(cg_iters)" if world == 1 else
-                               "tf_cpd_eval (local) + all_reduce([grad|f]) + tf_grams + tf_cg_solve(cg_iters)"},
+                               "tf_cpd_eval (local, + Grams of the full factors) + all_reduce([grad|f]) + tf_cg_solve(cg_iters)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": int(launches), "stages": stages,
         }

@@ -440,11 +440,18 @@ tf_status tf_cpd_eval(tf_ctx* c, tf_dims d, const double* T, const double* w, do
   cudaSetDevice(c->device);
   if ((s = eval_impl(c, d, T, w, f, grad))) return s;
   if (grams) {
-    // the Pi-form pass already formed [A^T A | B^T B | C^T C] (the whole tensor: K == K_total)
-    if (c->last_eval_pi && d.K == d.K_total) {
-      TF_CUDA(c, cudaMemcpyAsync(grams, c->evGrams.p, (size_t)3 * d.R * d.R * 8, cudaMemcpyDeviceToDevice,
-                                 c->stream));
-      return TF_OK;
+    // the Pi-form pass already formed [A^T A | B^T B | C^T C] (the whole tensor: K == K_total); for a K-shard
+    // it formed A^T A, B^T B and the local C Gram, so only the full C^T C remains (one symmetric GEMM)
+    if (c->last_eval_pi) {
+      const int64_t R = d.R;
+      const size_t nb = (size_t)(d.K == d.K_total ? 3 : 2) * R * R * 8;
+      TF_CUDA(c, cudaMemcpyAsync(grams, c->evGrams.p, nb, cudaMemcpyDeviceToDevice, c->stream));
+      if (d.K == d.K_total) return TF_OK;
+      const double* C = w + (d.I + d.J) * R;
+      GemmArgs gc = gemm_args(opnd(C, d.K_total, true), opnd(C, d.K_total, true), R, R, d.K_total, grams + 2 * R * R,
+                              R);
+      gc.sym = true;
+      return gemm_run(c, gc);
     }
     return grams_impl(c, d, w, grams);
   }

@@ -49,8 +49,8 @@ class ShardedEvaluator:
                 raise ValueError("need a Context (CUDA path) or an explicit eval_fn")
             from . import Dims
 
-            def eval_fn(d, T, w, f, g):
-                ctx.tf_cpd_eval(d, T, w, f, g)
+            def eval_fn(d, T, w, f, g, grams=None):
+                ctx.tf_cpd_eval(d, T, w, f, g, grams)
             self._Dims = Dims
         else:
             from types import SimpleNamespace
@@ -69,11 +69,15 @@ class ShardedEvaluator:
             self.buf = torch.empty(self.n + 1, dtype=torch.float64, device=device)
         return self.buf
 
-    def __call__(self, T_local: torch.Tensor, w: torch.Tensor, allreduce: bool = True):
-        """Returns views (f[1], grad[n]) of the packed buffer, globally reduced when allreduce=True."""
+    def __call__(self, T_local: torch.Tensor, w: torch.Tensor, allreduce: bool = True, grams=None):
+        """Returns views (f[1], grad[n]) of the packed buffer, globally reduced when allreduce=True. With
+        `grams` (3R^2, device) the CUDA evaluator also returns the Grams of the full (replicated) factors."""
         buf = self.packed(w.device)
         grad, f = buf[:self.n], buf[self.n:]
-        self.eval_fn(self.local_dims, T_local, w, f, grad)
+        if grams is not None:
+            self.eval_fn(self.local_dims, T_local, w, f, grad, grams)
+        else:
+            self.eval_fn(self.local_dims, T_local, w, f, grad)
         if allreduce and self.world > 1:
             dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group)
         return f, grad

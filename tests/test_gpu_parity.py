@@ -120,6 +120,7 @@ def _sharded_partials(ctx):
     w = torch.from_numpy(rng.standard_normal(R * (I + J + K))).cuda()
     Tt = torch.from_numpy(t).cuda()
     f_full, g_full = ctx.tf_cpd_eval(tf.Dims(I, J, K, R), Tt, w)
+    grams_full = ctx.tf_grams(tf.Dims(I, J, K, R), w)
     acc_f = torch.zeros(1, dtype=torch.float64, device="cuda")
     acc_g = torch.zeros_like(g_full)
     for world in (2, 3, 5, 8):
@@ -127,7 +128,11 @@ def _sharded_partials(ctx):
         acc_g.zero_()
         for rank in range(world):
             k0, k1 = synth.shard_range(K, rank, world)
-            f, g = ctx.tf_cpd_eval(tf.Dims(I, J, k1 - k0, R, K_total=K, k_begin=k0), Tt[k0:k1].contiguous(), w)
+            grams = torch.empty(3 * R * R, dtype=torch.float64, device="cuda")
+            f, g = ctx.tf_cpd_eval(tf.Dims(I, J, k1 - k0, R, K_total=K, k_begin=k0), Tt[k0:k1].contiguous(), w,
+                                   grams=grams)
+            # the Grams returned with a shard's evaluation are those of the full (replicated) factors
+            assert rel_err(to_np(grams), to_np(grams_full)) <= 1e-13
             # rows of dF/dC outside the shard are exactly zero
             gC = g[(I + J) * R:].view(R, K)
             assert torch.all(gC[:, :k0] == 0) and torch.all(gC[:, k1:] == 0)

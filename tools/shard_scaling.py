@@ -1,6 +1,6 @@
 """Single-GPU projection of the K-sharded step: for N = 1, 2, 4, 8 time, on one B200, exactly the
 work one rank of an N-GPU run does per step — tf_cpd_eval on its K/N-slice shard (k_begin = 0, K_total = K),
-tf_grams and the replicated tf_cg_solve — and report t(1)/t(N). The NCCL all-reduce of [grad | f]
+with the Grams of the full factors, and the replicated tf_cg_solve — and report t(1)/t(N). The NCCL all-reduce of [grad | f]
 (R(I+J+K)+1 doubles, 2.9 MB at c5) is not included (a few tens of microseconds over NVLink). This is a
 projection from per-rank work, not a multi-GPU measurement."""
 import json
@@ -30,8 +30,7 @@ for N in (1, 2, 4, 8):
     Tl = P.T[:k1]
 
     def step():
-        f, g = ctx.tf_cpd_eval(d, Tl, w)
-        ctx.tf_grams(dglob, w, grams)
+        f, g = ctx.tf_cpd_eval(d, Tl, w, grams=grams)
         if cfg.cg_iters:
             ctx.tf_cg_solve(dglob, grams, w, -g, cfg.lam, cfg.cg_iters, 0.0, False, x)
 

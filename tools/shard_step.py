@@ -1,4 +1,4 @@
-"""One rank's K-sharded c5 step at N GPUs (tf_cpd_eval on the K/N shard + tf_grams + tf_cg_solve), timed with
+"""One rank's K-sharded c5 step at N GPUs (tf_cpd_eval on the K/N shard, returning the full-factor Grams, + tf_cg_solve), timed with
 CUDA events; run under `ncu --metrics gpu__time_duration.sum` for the per-kernel split (development aid)."""
 import sys
 
@@ -27,8 +27,7 @@ g = torch.empty(cfg.n, dtype=torch.float64, device="cuda")
 
 
 def step():
-    ctx.tf_cpd_eval(d, Tl, w, f, g)
-    ctx.tf_grams(dg, w, grams)
+    ctx.tf_cpd_eval(d, Tl, w, f, g, grams)
     ctx.tf_cg_solve(dg, grams, w, -g, cfg.lam, cfg.cg_iters or 10, 0.0, False, x)
 
 
@@ -39,8 +38,7 @@ e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
 tot_eval = tot_cg = 0.0
 for _ in range(reps):
     e[0].record()
-    ctx.tf_cpd_eval(d, Tl, w, f, g)
-    ctx.tf_grams(dg, w, grams)
+    ctx.tf_cpd_eval(d, Tl, w, f, g, grams)
     e[1].record()
     ctx.tf_cg_solve(dg, grams, w, -g, cfg.lam, cfg.cg_iters or 10, 0.0, False, x)
     e[2].record()
