@@ -688,14 +688,15 @@ __global__ void __launch_bounds__(kPiThreads) k_eval_finalize_pi(EvalArgs p, int
 
 // f = 1/2 ||T||^2 - <A, M1> + 1/2 1^T (piA * piB * piC) 1 and the cancellation guard (one block; every sum in
 // a fixed order: strided per-thread partials, then warps, then thread 0 over the warps).
-__global__ void __launch_bounds__(256) k_eval_pi_guard(EvalArgs p, const double* __restrict__ grams,
+__global__ void __launch_bounds__(1024) k_eval_pi_guard(EvalArgs p, const double* __restrict__ grams,
                                                        const double* __restrict__ part, int nblk,
                                                        double* __restrict__ f, int* __restrict__ flag,
                                                        int check_grad) {
-  __shared__ double red[5][8];
+  __shared__ double red[5][32];
   const int64_t R = p.R, RR = R * R;
   double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};   // t2, x2, ip, g2, w2
   for (int64_t s = threadIdx.x; s < p.nCta; s += blockDim.x) v[0] += p.fp[s];
+#pragma unroll 4
   for (int64_t e = threadIdx.x; e < RR; e += blockDim.x) v[1] += grams[e] * grams[RR + e] * grams[2 * RR + e];
   for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
     v[2] += part[3 * b];
@@ -729,7 +730,7 @@ cudaError_t launch_eval_finalize_pi(const EvalArgs& p, int RP, double* grad, dou
 
 cudaError_t launch_eval_pi_guard(const EvalArgs& p, const double* grams, const double* part, int nblk, double* f,
                                  int* flag, cudaStream_t st, bool check_grad) {
-  k_eval_pi_guard<<<1, 256, 0, st>>>(p, grams, part, nblk, f, flag, check_grad ? 1 : 0);
+  k_eval_pi_guard<<<1, 1024, 0, st>>>(p, grams, part, nblk, f, flag, check_grad ? 1 : 0);
   return cudaGetLastError();
 }
 
