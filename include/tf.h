@@ -91,8 +91,11 @@ tf_status tf_hadamard(tf_ctx *ctx, int64_t R, const double *grams, double *pi);
  *        With K < K_total, the dF/dA and dF/dB blocks and f are partial sums over
  *        the local slices and dF/dC holds rows k_begin..k_begin+K-1 (other rows 0):
  *        an elementwise SUM over shards of [grad | f] gives the global result.
- *   grams (nullable, 3*R*R) the Grams at w, as tf_grams.
- * The three MTTKRPs and the residual are fused in one pass over T. */
+ *   grams (nullable, 3*R*R) the Grams of the full factors at w, exactly what tf_grams returns, also
+ *        for a K-shard (C^T C over all K_total rows); the evaluation forms most of them anyway.
+ * The three MTTKRPs are fused in one pass over T: by default the guarded Pi form (grad = W Pi - M,
+ * f by the Gram expansion, rerun in the residual form on the device when cancellation would cost
+ * accuracy; reading R31), or the residual form (tf_ctx_set_eval_form). */
 tf_status tf_cpd_eval(tf_ctx *ctx, tf_dims d, const double *T, const double *w, double *f, double *grad,
                       double *grams);
 
