@@ -205,9 +205,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TF_BENCH_BACKEND=gloo (development only): a functional check of the multi-rank path on a box with fewer
+    # GPUs than ranks (ranks share a device; the all-reduce goes through the host, so no kernel waits on another
+    # rank). Numbers from such a run are not scaling measurements.
+    backend = os.environ.get("TF_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     cfg = synth.CONFIGS[args.config]
@@ -240,7 +249,10 @@ def run_ours(args):
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            if backend == "nccl":
+                dist.barrier(device_ids=[local])
+            else:
+                dist.barrier()
         torch.cuda.synchronize(dev)
 
     for _ in range(args.warmup):
