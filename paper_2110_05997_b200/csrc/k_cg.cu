@@ -21,7 +21,7 @@ namespace tfk {
 
 unsigned long long* cg_debug_tstamp();
 constexpr int kCgThreads = 256;
-constexpr int kGramZ = 16;   // max row splits of one Gram output tile
+constexpr int kGramZ = 64;   // max row splits of one mode's Gram (full-width partials)
 
 struct CgArgs {
   Modes m;
@@ -61,100 +61,22 @@ struct VSrc {
   __device__ __forceinline__ double raw(int64_t q) const { return b ? fma(beta, b[q], a[q]) : a[q]; }
 };
 
-// ---- stage G: G_l[r + R s] = sum_a V_l[a, r] W_l[a, s]; items (l, 32x32 output tile); the 8 warps
-// split the rows, each warp runs 4x4 DMMA fragments straight from L2 with 2 k-steps in flight, and the
-// 8 partial tiles are summed in a fixed order through shared memory (red: 8 x 1024 doubles).
+// ---- stage G: G_l[r + R s] = sum_a V_l[a, r] W_l[a, s]. Items (mode l, row split z): every item computes
+// the FULL R x R partial of its rows, so each row of V (= D (r + beta p)) and W is read once per
+// iteration (32 x 32 output tiles re-read every column block 4x: the stage was bound by L2 -> SM traffic).
+// The item's rows are staged by cp.async in chunks of kGRows as [column][row] (pitch 4 mod 16: conflict-free
+// fragments); warp w owns the r-tiles mi = w, w + 8 (all 8-column tiles ni), so per k-step it loads <= 2 A
+// and NT B fragments for <= 2 NT DMMAs. The Z partials per mode are summed in stage S in a fixed order.
+#ifndef TF_GRAM_DIV
+#define TF_GRAM_DIV 3
+#endif
+constexpr int kGRows = 32, kGLd = kGRows + 4;
 __device__ __forceinline__ int gram_splits(const Modes& m) {
-  const int nt = (int)((m.R + 31) / 32);
-  return max(1, min(kGramZ, (int)(gridDim.x / (3 * nt * nt))));
+  (void)m;
+  return max(1, min(kGramZ, (int)gridDim.x / TF_GRAM_DIV));
 }
+__host__ __device__ constexpr size_t gram_smem_doubles(int R4) { return (size_t)3 * R4 * kGLd; }
 
-__device__ void stage_gram(const CgArgs& A, const VSrc& V, double* red) {
-  const Modes& m = A.m;
-  const int R = (int)m.R;
-  const int nt = (R + 31) / 32;
-  const int Z = gram_splits(m);
-  const int items = 3 * nt * nt * Z;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
-  for (int item = blockIdx.x; item < items; item += gridDim.x) {
-    const int z = item % Z, li = item / Z;
-    const int l = li / (nt * nt), tt = li % (nt * nt);
-    const int r0 = (tt % nt) * 32, s0 = (tt / nt) * 32;
-    const int64_t n = m.n[l];
-    const double* W = m.W[l];
-    const int64_t off = m.off[l];
-    const double* D = V.D ? V.D + l * R : nullptr;
-    double acc[4][4][2] = {};
-    const int64_t rps = ((n + 4 * Z - 1) / (4 * Z)) * 4;          // rows per split
-    const int64_t zb = z * rps, ze = min(n, zb + rps);
-    const int64_t rpw = ((rps + 31) / 32) * 4;                    // rows per warp
-    const int64_t a_begin = zb + warp * rpw, a_end = min(ze, a_begin + rpw);
-    double dr[4];
-    bool rv[4], sv[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int r = r0 + 8 * i + g, sc = s0 + 8 * i + g;
-      rv[i] = r < R;
-      sv[i] = sc < R;
-      dr[i] = (D && rv[i]) ? D[r] : 1.0;
-    }
-#pragma unroll 4
-    for (int64_t a0 = a_begin; a0 < a_end; a0 += 4) {
-      const int64_t a = a0 + q;
-      const bool ok = a < a_end;
-      double fa[4], fb[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        fa[i] = (ok && rv[i]) ? V.raw(off + a + n * (r0 + 8 * i + g)) * dr[i] : 0.0;
-        fb[i] = (ok && sv[i]) ? W[a + n * (s0 + 8 * i + g)] : 0.0;
-      }
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], fa[mi], fb[ni]);
-    }
-#pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) red[warp * 1024 + ((mi * 4 + ni) * 2 + e) * 32 + lane] = acc[mi][ni][e];
-    __syncthreads();
-    for (int idx = threadIdx.x; idx < 1024; idx += blockDim.x) {
-      double sum = 0.0;
-#pragma unroll
-      for (int w = 0; w < 8; ++w) sum += red[w * 1024 + idx];
-      const int ln = idx & 31, e = (idx >> 5) & 1, ni = (idx >> 6) & 3, mi = (idx >> 8) & 3;
-      const int gg = ln >> 2, qq = ln & 3;
-      const int r = r0 + 8 * mi + gg, c = s0 + 8 * ni + 2 * qq + e;
-      if (r < R && c < R) A.G[((int64_t)z * 3 + l) * R * R + r + (int64_t)R * c] = sum;
-    }
-    __syncthreads();
-  }
-}
-
-// ---- stage S: S_l = sum_{l' != l} Pi^(l,l') * G_l' with G_l' = sum_z Gpart[z][l'] (fixed order).
-__device__ void stage_s(const CgArgs& A) {
-  const int64_t R = A.m.R, RR = R * R;
-  const int Z = gram_splits(A.m);
-  for (int64_t qi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; qi < RR; qi += (int64_t)gridDim.x * blockDim.x) {
-    double gsum[3] = {0.0, 0.0, 0.0};
-    for (int z = 0; z < Z; ++z)
-#pragma unroll
-      for (int l = 0; l < 3; ++l) gsum[l] += A.G[((int64_t)z * 3 + l) * RR + qi];
-    const double p12 = A.pi[3 * RR + qi], p13 = A.pi[4 * RR + qi], p23 = A.pi[5 * RR + qi];
-    A.S[qi] = p12 * gsum[1] + p13 * gsum[2];
-    A.S[RR + qi] = p12 * gsum[0] + p23 * gsum[2];
-    A.S[2 * RR + qi] = p13 * gsum[0] + p23 * gsum[1];
-  }
-}
-
-// ---- stage Y: for rows of mode l: y = D (V Pi^(l) + W S_l + lambda V) with V = D (r + beta p).
-// items (l, YR-row chunk, column half h). The operands of the whole 2R contraction are staged once into
-// shared memory with cp.async (8-byte LDGSTS, zero-fill for padding, all copies of a thread in flight at
-// once): sXr/sXp/sW = rows of r, p, W (YR x R4), sM = [Pi^(l) ; S_l] columns of the half (2R4 x 8*NTH).
-// Warp w: m-tile w % (YR/8), n-tiles w / (YR/8) + (8*8/YR) j. If write_p != nullptr the raw V values (the
-// new CG direction) are written after a block barrier. Returns the block's partial sum of raw(V) . y.
 __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool valid) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
                "r"(valid ? 8 : 0)
@@ -164,6 +86,132 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
+template <int NT>
+__device__ void stage_gram(const CgArgs& A, const VSrc& V, double* smem) {
+  const Modes& m = A.m;
+  const int R = (int)m.R;
+  const int R4 = 4 * ((R + 3) / 4);
+  const int Z = gram_splits(m);
+  const int items = 3 * Z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const bool hasP = V.b != nullptr;
+  double* sR = smem;                 // [R4][kGLd]
+  double* sP = sR + R4 * kGLd;
+  double* sW = sP + R4 * kGLd;
+  constexpr int MT = (NT + 7) / 8;   // r-tiles per warp (<= 2)
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    const int z = item % Z, l = item / Z;
+    const int64_t n = m.n[l];
+    const double* W = m.W[l];
+    const int64_t off = m.off[l];
+    const double* D = V.D ? V.D + l * R : nullptr;
+    const int64_t rps = ((n + 4 * Z - 1) / (4 * Z)) * 4;          // rows per split
+    const int64_t zb = z * rps, ze = min(n, zb + rps);
+    double dr[MT];
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      const int r = 8 * (warp + 8 * i) + g;
+      dr[i] = (D && r < R) ? D[r] : 1.0;
+    }
+    double acc[MT][NT][2] = {};
+    for (int64_t c0 = zb; c0 < ze; c0 += kGRows) {
+      __syncthreads();   // the previous chunk (or item) is consumed
+      for (int idx = threadIdx.x; idx < kGRows * R4; idx += blockDim.x) {
+        const int a = idx % kGRows, col = idx / kGRows;
+        const bool ok = col < R && c0 + a < ze;
+        const int64_t ix = ok ? c0 + a + n * col : 0;
+        cp_async8(&sR[col * kGLd + a], V.a + off + ix, ok);
+        if (hasP) cp_async8(&sP[col * kGLd + a], V.b + off + ix, ok);
+        cp_async8(&sW[col * kGLd + a], W + ix, ok);
+      }
+      cp_async_wait_all();
+      __syncthreads();
+#pragma unroll 2
+      for (int ks = 0; ks < kGRows / 4; ++ks) {
+        const int a = 4 * ks + q;
+        double fa[MT], fb[NT];
+#pragma unroll
+        for (int i = 0; i < MT; ++i) {
+          const int o = (8 * (warp + 8 * i) + g) * kGLd + a;
+          fa[i] = (warp + 8 * i < NT) ? dr[i] * (hasP ? fma(V.beta, sP[o], sR[o]) : sR[o]) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < NT; ++j) fb[j] = sW[(8 * j + g) * kGLd + a];
+#pragma unroll
+        for (int i = 0; i < MT; ++i)
+          if (warp + 8 * i < NT) {
+#pragma unroll
+            for (int j = 0; j < NT; ++j) dmma(acc[i][j], fa[i], fb[j]);
+          }
+      }
+    }
+    // partial (z, l): element (r = 8 mi + g, c = 8 j + 2q + e)
+    double* Gz = A.G + ((int64_t)z * 3 + l) * R * R;
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      const int r = 8 * (warp + 8 * i) + g;
+      if (warp + 8 * i >= NT || r >= R) continue;
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = 8 * j + 2 * q + e;
+          if (c < R) Gz[r + (int64_t)R * c] = acc[i][j][e];
+        }
+    }
+  }
+}
+
+// ---- stage S: G_l = sum_z Gpart[z][l] (fixed order) and S_l = sum_{l' != l} Pi^(l,l') * G_l'. Four lanes
+// share one entry: lane t of the group sums the splits z = t, t + 4, ... of the three modes, and the four
+// partial sums are combined by a fixed butterfly.
+__device__ void stage_s(const CgArgs& A) {
+  const int64_t R = A.m.R, RR = R * R;
+  const int Z = gram_splits(A.m);
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int sub = (int)(gt & 3);
+  for (int64_t base = gt >> 2; base < ((RR + 7) / 8) * 8; base += nthr >> 2) {
+    const int64_t qi = base;
+    double gsum[3] = {0.0, 0.0, 0.0};
+    if (qi < RR) {
+      const double* gp = A.G + qi;
+      int z = sub;
+      for (; z + 12 < Z; z += 16) {   // four splits per step: 12 loads in flight, added in z order
+        double v[4][3];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int l = 0; l < 3; ++l) v[u][l] = gp[((int64_t)(z + 4 * u) * 3 + l) * RR];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int l = 0; l < 3; ++l) gsum[l] += v[u][l];
+      }
+      for (; z < Z; z += 4)
+#pragma unroll
+        for (int l = 0; l < 3; ++l) gsum[l] += gp[((int64_t)z * 3 + l) * RR];
+    }
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+      gsum[l] += __shfl_xor_sync(0xffffffffu, gsum[l], 1);
+      gsum[l] += __shfl_xor_sync(0xffffffffu, gsum[l], 2);
+    }
+    if (sub == 0 && qi < RR) {
+      const double p12 = A.pi[3 * RR + qi], p13 = A.pi[4 * RR + qi], p23 = A.pi[5 * RR + qi];
+      A.S[qi] = p12 * gsum[1] + p13 * gsum[2];
+      A.S[RR + qi] = p12 * gsum[0] + p23 * gsum[2];
+      A.S[2 * RR + qi] = p13 * gsum[0] + p23 * gsum[1];
+    }
+  }
+}
+
+// ---- stage Y: for rows of mode l: y = D (V Pi^(l) + W S_l + lambda V) with V = D (r + beta p).
+// items (l, YR-row chunk, column half h). The operands of the whole 2R contraction are staged once into
+// shared memory with cp.async (8-byte LDGSTS, zero-fill for padding, all copies of a thread in flight at
+// once): sXr/sXp/sW = rows of r, p, W (YR x R4), sM = [Pi^(l) ; S_l] columns of the half (2R4 x 8*NTH).
+// Warp w: m-tile w % (YR/8), n-tiles w / (YR/8) + (8*8/YR) j. If write_p != nullptr the raw V values (the
+// new CG direction) are written after a block barrier. Returns the block's partial sum of raw(V) . y.
 template <int NT>
 __host__ __device__ constexpr int apply_rows() { return NT > 13 ? 16 : 32; }
 
@@ -351,7 +399,7 @@ __global__ void __launch_bounds__(kCgThreads, 1) k_cg_persistent(CgArgs A) {
 
   if (A.mode == 1) {   // single matvec: y = (J^T J + lambda I) v
     VSrc V{A.v, nullptr, 0.0, nullptr};
-    stage_gram(A, V, red);
+    stage_gram<NT>(A, V, cg_smem);
     grid.sync();
     stage_s(A);
     grid.sync();
@@ -387,7 +435,7 @@ __global__ void __launch_bounds__(kCgThreads, 1) k_cg_persistent(CgArgs A) {
     VSrc V{A.r, pc, beta, A.dscale};
     const int sb = 8 * (it - 1);
     stamp(A, sb + 0);
-    stage_gram(A, V, red);
+    stage_gram<NT>(A, V, cg_smem);
     stamp(A, sb + 1);
     grid.sync();
     stamp(A, sb + 2);
@@ -465,7 +513,7 @@ template <int NT>
 static cudaError_t launch_persistent_nt(const CgArgs& a, int nsm, cudaStream_t st) {
   auto kern = k_cg_persistent<NT>;
   const int R4 = (int)(4 * ((a.m.R + 3) / 4));
-  const size_t smem = 8 * std::max<size_t>(8 * 1024, apply_smem_doubles<NT>(R4));
+  const size_t smem = 8 * std::max<size_t>(std::max<size_t>(1024, gram_smem_doubles(R4)), apply_smem_doubles<NT>(R4));
   cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (ea != cudaSuccess) return ea;
   int per_sm = 0;
