@@ -426,6 +426,26 @@ def run_ours(args):
                             "noise_rel": P.sigma * math.sqrt(I * J * K) / math.sqrt(float(torch.sum(P.T * P.T))),
                             "what": "tf_cpd: ST-MLSVD compression + random N(0,1) core start + dGN on the R~^3 core "
                                     "(PAPER.md:2514-2533, defaults 2626/3137) + uncompression; rel_err on the full T"}
+        # the dGN loop itself on the uncompressed tensor (NEXT #2; the paper's uncompressed 2000^3 run,
+        # PAPER.md:4048): per iteration one guarded evaluation, Grams, gamma, CG with the paper's random budget,
+        # the x^T J^T J x matvec of the gain ratio, norm balancing and the stopping tests (one host sync)
+        wd = w.clone()
+        cgb = synth.cg_budget(4, seed=0)
+        ctx.tf_cpd_dgn(dglob, P.T, wd, cgb, maxiter=1, tol=0.0)   # warm-up
+        dms = {}
+        for its in (1, 4):   # the difference removes the set-up pass (||T||^2, mean|T|, F and grad at w0)
+            wd.copy_(w)
+            torch.cuda.synchronize(dev)
+            s0.record(stream)
+            dout, _ = ctx.tf_cpd_dgn(dglob, P.T, wd, cgb, maxiter=its, tol=0.0)
+            s1.record(stream)
+            torch.cuda.synchronize(dev)
+            dms[its] = (s0.elapsed_time(s1), dout["iters"])
+        stages["dgn"] = {"ms_per_iteration": (dms[4][0] - dms[1][0]) / max(1, dms[4][1] - dms[1][1]),
+                         "setup_plus_first_ms": dms[1][0], "cg_budget": [int(x) for x in cgb],
+                         "what": "tf_cpd_dgn on the uncompressed T from the evaluation point: Tensor Fox's dGN "
+                                 "iteration (PAPER.md:2611-2793) with the paper's random CG budget, tol=0; "
+                                 "(t(4 iterations) - t(1)) / 3"}
         # CP-ALS (NEXT #4): the three single-mode MTTKRPs and one sweep from the same point
         wa = w.clone()
         mt = []
