@@ -248,32 +248,48 @@ tf_status eval_impl(tf_ctx* c, const tf_dims& d, const double* T, const double* 
   double* part = (double*)c->evPart.p;
   int* flag = reinterpret_cast<int*>(part + 3 * nblk);
   TF_CUDA(c, launch_eval(&map, T, p, NT, tma, BT, c->stream, false));
-  if (d.K == d.K_total) {
+  // Equal-size modes sit I*R apart in w (and their Grams / Pi blocks R*R apart), so their small GEMMs run as
+  // one batched launch: the three Grams (whole tensor, I = J = K) or A^T A and B^T B (I = J).
+  const bool cube = d.I == d.J && d.J == d.K && d.K == d.K_total;
+  if (d.K == d.K_total && !cube) {
     if ((s = grams_impl(c, d, w, grams))) return s;
-  } else {   // C Gram over the local slices only (the partial f and grad of a K-shard)
-    const int64_t R = d.R;
-    GemmArgs ga = gemm_args(opnd(p.A, d.I, true), opnd(p.A, d.I, true), R, R, d.I, grams, R);
+  } else {   // for a K-shard the C Gram is over the local slices only (the partial f and grad)
+    const int64_t R = d.R, RR = R * R;
+    const int nab = cube ? 3 : (d.I == d.J ? 2 : 1);
+    GemmArgs ga = gemm_args(opnd(p.A, d.I, true, d.I * R), opnd(p.A, d.I, true, d.I * R), R, R, d.I, grams, R);
     ga.sym = true;
+    ga.batch = nab;
+    ga.sum_batch = nab == 1;
+    ga.cstride = RR;
     if ((s = gemm_run(c, ga))) return s;
-    GemmArgs gb = gemm_args(opnd(p.B, d.J, true), opnd(p.B, d.J, true), R, R, d.J, grams + R * R, R);
-    gb.sym = true;
-    if ((s = gemm_run(c, gb))) return s;
-    GemmArgs gc = gemm_args(opnd(p.C + d.k_begin, d.K_total, true), opnd(p.C + d.k_begin, d.K_total, true), R, R,
-                            d.K, grams + 2 * R * R, R);
-    gc.sym = true;
-    if ((s = gemm_run(c, gc))) return s;
+    if (nab == 1) {
+      GemmArgs gb = gemm_args(opnd(p.B, d.J, true), opnd(p.B, d.J, true), R, R, d.J, grams + RR, R);
+      gb.sym = true;
+      if ((s = gemm_run(c, gb))) return s;
+    }
+    if (!cube) {
+      GemmArgs gc = gemm_args(opnd(p.C + d.k_begin, d.K_total, true), opnd(p.C + d.k_begin, d.K_total, true), R,
+                              R, d.K, grams + 2 * RR, R);
+      gc.sym = true;
+      if ((s = gemm_run(c, gc))) return s;
+    }
   }
   // W Pi into grad: Pi = [Pi1 | Pi2 | Pi3 | ...] from the (local) Grams, then one small GEMM per mode
   double* pi = grams + 3 * d.R * d.R;
   TF_CUDA(c, launch_hadamard(d.R, grams, pi, c->stream));
   {
     const int64_t R = d.R, RR = R * R;
-    if ((s = gemm_run(c, gemm_args(opnd(p.A, d.I, false), opnd(pi, R, true), d.I, R, R, grad, d.I)))) return s;
-    if ((s = gemm_run(c, gemm_args(opnd(p.B, d.J, false), opnd(pi + RR, R, true), d.J, R, R, grad + d.I * R,
-                                   d.J))))
+    const int nab = cube ? 3 : (d.I == d.J ? 2 : 1);
+    GemmArgs ga = gemm_args(opnd(p.A, d.I, false, d.I * R), opnd(pi, R, true, RR), d.I, R, R, grad, d.I);
+    ga.batch = nab;
+    ga.sum_batch = nab == 1;
+    ga.cstride = d.I * R;
+    if ((s = gemm_run(c, ga))) return s;
+    if (nab == 1 &&
+        (s = gemm_run(c, gemm_args(opnd(p.B, d.J, false), opnd(pi + RR, R, true), d.J, R, R, grad + d.I * R, d.J))))
       return s;
-    if ((s = gemm_run(c, gemm_args(opnd(p.C + d.k_begin, d.K_total, false), opnd(pi + 2 * RR, R, true), d.K, R, R,
-                                   grad + (d.I + d.J) * R + d.k_begin, d.K_total))))
+    if (!cube && (s = gemm_run(c, gemm_args(opnd(p.C + d.k_begin, d.K_total, false), opnd(pi + 2 * RR, R, true), d.K,
+                                            R, R, grad + (d.I + d.J) * R + d.k_begin, d.K_total))))
       return s;
   }
   TF_CUDA(c, launch_eval_finalize_pi(p, RP, grad, part, nblk, c->stream));
