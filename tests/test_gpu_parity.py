@@ -384,6 +384,12 @@ def test_c3_full_size_sampled(ctx):
 
 
 @pytest.mark.slow
+def test_c4_full_size_sampled(ctx):
+    """Unequal modes at full size (4000 x 800 x 400, R = 50): edge tiles in every mode, no batched GEMMs."""
+    _sampled_full_size(ctx, "c4", "random_uniform", n_rows=1)
+
+
+@pytest.mark.slow
 def test_c5_full_size_sampled(ctx):
     _sampled_full_size(ctx, "c5", "random", n_rows=1)
 
