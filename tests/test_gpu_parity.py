@@ -85,8 +85,17 @@ def test_shapes(ctx, dims):
     check_eval(ctx, T, w, I, J, K, R)
 
 
-def test_padded_leading_dimension(ctx):
-    """ldT > I (both an even ldT -> TMA path and an odd ldT -> cooperative-load path)."""
+@pytest.mark.parametrize("form", ["auto", "pi"])
+def test_padded_leading_dimension(ctx, form):
+    """ldT > I (both an even ldT -> TMA path and an odd ldT -> cooperative-load path), both forms."""
+    ctx.set_eval_form(form)
+    try:
+        _padded_ld(ctx)
+    finally:
+        ctx.set_eval_form("auto")
+
+
+def _padded_ld(ctx):
     I, J, K, R = 30, 17, 6, 5
     rng = np.random.default_rng(5)
     t = rng.standard_normal((K, J, I))
@@ -103,18 +112,19 @@ def test_padded_leading_dimension(ctx):
 
 
 @pytest.mark.parametrize("form", ["residual", "pi"])
-def test_k_sharded_partials_sum_to_full(ctx, form):
+@pytest.mark.parametrize("dims", [(50, 40, 23, 6), (40, 40, 23, 6)])
+def test_k_sharded_partials_sum_to_full(ctx, form, dims):
     """shard partials [grad | f] summed elementwise equal the full evaluation (both
-    algebraic forms of reading R31; in the Pi form each shard uses the C Gram over its own slices)."""
+    algebraic forms of reading R31; in the Pi form each shard uses the C Gram over its own slices; I = J takes
+    the batched Gram / W Pi launches)."""
     ctx.set_eval_form(form)
     try:
-        _sharded_partials(ctx)
+        _sharded_partials(ctx, *dims)
     finally:
         ctx.set_eval_form("auto")
 
 
-def _sharded_partials(ctx):
-    I, J, K, R = 50, 40, 23, 6
+def _sharded_partials(ctx, I, J, K, R):
     rng = np.random.default_rng(11)
     t = rng.standard_normal((K, J, I))
     w = torch.from_numpy(rng.standard_normal(R * (I + J + K))).cuda()
@@ -610,7 +620,8 @@ def test_sharded_dgn_matches_single_device(ctx):
 
 
 @pytest.mark.parametrize("dims", [(37, 29, 23, 1), (37, 29, 23, 5), (70, 66, 40, 9), (64, 64, 17, 33),
-                                  (45, 80, 30, 104), (30, 40, 25, 128), (130, 70, 20, 57)])
+                                  (45, 80, 30, 104), (30, 40, 25, 128), (130, 70, 20, 57),
+                                  (41, 41, 41, 13), (52, 52, 19, 100)])
 def test_pi_form_shapes(ctx, dims):
     """The guarded Pi-form pass forced at every fragment-count regime (R = 1 .. 128: the prescaled phase 3 for
     R <= 32, the tensor-memory fragments above, R = 128 filling all 512 TMEM columns), ragged tiles, at a
