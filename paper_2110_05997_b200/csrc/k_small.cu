@@ -244,23 +244,61 @@ __global__ void k_dots_partial(int64_t n, const double* __restrict__ g, const do
 }
 
 // partial[b][0..1] = { sum |t|, sum t^2 } over the I x J x K tensor with leading dimension ldT
-__global__ void k_tsums_partial(int64_t I, int64_t JK, int64_t ldT, const double* __restrict__ T,
-                                double* __restrict__ partial) {
+// sum |t| and sum t^2 over the tensor (one streaming pass). Dense storage (ldT = I, 16-byte aligned) is read as
+// a flat array of double2 with 8 independent loads in flight per thread; a padded leading dimension walks the
+// rows. Each thread's sums follow a fixed order (deterministic).
+__global__ void __launch_bounds__(256) k_tsums_partial(int64_t I, int64_t JK, int64_t ldT,
+                                                       const double* __restrict__ T, double* __restrict__ partial) {
   __shared__ double red[2][8];
-  double sa = 0.0, s2 = 0.0;
-  const int64_t N = I * JK;
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < N; q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = q % I, jk = q / I;
-    const double t = T[i + ldT * jk];
-    sa += fabs(t);
-    s2 = fma(t, t, s2);
+  constexpr int U = 8;
+  double sa[U], s2[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) sa[u] = s2[u] = 0.0;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+  if (ldT == I && (reinterpret_cast<uintptr_t>(T) & 15) == 0) {
+    const int64_t N = I * JK, N2 = N / 2;
+    const double2* T2 = reinterpret_cast<const double2*>(T);
+    int64_t q = tid;
+    for (; q + (U - 1) * stride < N2; q += U * stride) {
+      double2 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) v[u] = __ldg(T2 + q + u * stride);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        sa[u] += fabs(v[u].x) + fabs(v[u].y);
+        s2[u] = fma(v[u].y, v[u].y, fma(v[u].x, v[u].x, s2[u]));
+      }
+    }
+    for (; q < N2; q += stride) {
+      const double2 v = __ldg(T2 + q);
+      sa[0] += fabs(v.x) + fabs(v.y);
+      s2[0] = fma(v.y, v.y, fma(v.x, v.x, s2[0]));
+    }
+    if ((N & 1) && tid == 0) {
+      const double t = T[N - 1];
+      sa[1] += fabs(t);
+      s2[1] = fma(t, t, s2[1]);
+    }
+  } else {
+    for (int64_t jk = blockIdx.x; jk < JK; jk += gridDim.x)
+      for (int64_t i = threadIdx.x; i < I; i += blockDim.x) {
+        const double t = T[i + ldT * jk];
+        sa[0] += fabs(t);
+        s2[0] = fma(t, t, s2[0]);
+      }
   }
-  sa = warp_sum(sa);
-  s2 = warp_sum(s2);
+  double a = 0.0, b = 0.0;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    a += sa[u];
+    b += s2[u];
+  }
+  a = warp_sum(a);
+  b = warp_sum(b);
   const int w = threadIdx.x >> 5;
   if ((threadIdx.x & 31) == 0) {
-    red[0][w] = sa;
-    red[1][w] = s2;
+    red[0][w] = a;
+    red[1][w] = b;
   }
   __syncthreads();
   if (threadIdx.x < 2) {
