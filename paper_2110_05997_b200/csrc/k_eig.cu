@@ -178,38 +178,34 @@ __global__ void __launch_bounds__(1024) k_jacobi_eig(int P, const double* __rest
         pr[2 * k + 1] = q;
       }
       __syncthreads();
+      // thread (lane-column x0 = tid % 128, pair group kg = tid / 128): no integer division in the loops
+      const int x0 = tid & 127, kg = tid >> 7, ng = nt >> 7;
       // rows p, q  <-  J^T (rows)
-      for (int e = tid; e < half * Pp; e += nt) {
-        const int k = e / Pp, col = e % Pp;
-        const double c = cs[2 * k], s = cs[2 * k + 1];
-        if (s == 0.0) continue;
-        const int p = pr[2 * k], q = pr[2 * k + 1];
-        const double hp = hs[p + Pp * col], hq = hs[q + Pp * col];
-        hs[p + Pp * col] = c * hp - s * hq;
-        hs[q + Pp * col] = s * hp + c * hq;
-      }
-      __syncthreads();
-      // columns p, q  <-  (cols) J, and V <- V J
-      for (int e = tid; e < half * Pp; e += nt) {
-        const int k = e / Pp, row = e % Pp;
-        const double c = cs[2 * k], s = cs[2 * k + 1];
-        if (s == 0.0) continue;
-        const int p = pr[2 * k], q = pr[2 * k + 1];
-        const double hp = hs[row + Pp * p], hq = hs[row + Pp * q];
-        hs[row + Pp * p] = c * hp - s * hq;
-        hs[row + Pp * q] = s * hp + c * hq;
-        if (row < P) {
-          const double vp = Vw[row + (int64_t)P * p], vq = Vw[row + (int64_t)P * q];
-          Vw[row + (int64_t)P * p] = c * vp - s * vq;
-          Vw[row + (int64_t)P * q] = s * vp + c * vq;
+      for (int x = x0; x < Pp; x += 128) {
+        for (int k = kg; k < half; k += ng) {
+          const double c = cs[2 * k], s = cs[2 * k + 1];
+          if (s == 0.0) continue;
+          const int p = pr[2 * k], q = pr[2 * k + 1];
+          const double hp = hs[p + Pp * x], hq = hs[q + Pp * x];
+          hs[p + Pp * x] = c * hp - s * hq;
+          hs[q + Pp * x] = s * hp + c * hq;
         }
       }
       __syncthreads();
-      for (int k = tid; k < half; k += nt) {
-        if (cs[2 * k + 1] != 0.0) {
+      // columns p, q  <-  (cols) J, and V <- V J; the rotated pair's own off-diagonal entries are set to 0
+      for (int x = x0; x < Pp; x += 128) {
+        for (int k = kg; k < half; k += ng) {
+          const double c = cs[2 * k], s = cs[2 * k + 1];
+          if (s == 0.0) continue;
           const int p = pr[2 * k], q = pr[2 * k + 1];
-          hs[p + Pp * q] = 0.0;
-          hs[q + Pp * p] = 0.0;
+          const double hp = hs[x + Pp * p], hq = hs[x + Pp * q];
+          hs[x + Pp * p] = x == q ? 0.0 : c * hp - s * hq;
+          hs[x + Pp * q] = x == p ? 0.0 : s * hp + c * hq;
+          if (x < P) {
+            const double vp = Vw[x + (int64_t)P * p], vq = Vw[x + (int64_t)P * q];
+            Vw[x + (int64_t)P * p] = c * vp - s * vq;
+            Vw[x + (int64_t)P * q] = s * vp + c * vq;
+          }
         }
       }
       __syncthreads();
