@@ -5,6 +5,7 @@
 // convention of reading R23 — plus the rank choice of Alg. Compression and the
 // MLSVD-energy initialisation. All reductions run in a fixed order.
 #include <cfloat>
+#include <cstdio>
 
 #include "tf_device.cuh"
 #include "../../include/tf.h"
@@ -116,13 +117,18 @@ __global__ void __launch_bounds__(kQrThreads) k_house_qr(int64_t n, int P, doubl
 // Parallel cyclic Jacobi (round-robin pairing, Golub–Van Loan sym.schur2 rotations) on the symmetric
 // part of H, one CTA, H in shared memory; Vtmp accumulates the rotations; the output is sorted by
 // |theta| decreasing (the ordering of Lemma svd-transpose) with ties kept in index order.
+#ifdef TF_JACOBI_STATS
+__device__ int g_jac_sweeps[64];
+__device__ int g_jac_calls;
+#endif
 __global__ void __launch_bounds__(1024) k_jacobi_eig(int P, const double* __restrict__ H, int64_t ldh,
                                                      double* __restrict__ Vt, double* __restrict__ V,
                                                      double* __restrict__ theta, int vsm, int max_sweeps) {
   extern __shared__ double hs[];
   const int Pp = P + (P & 1);
   const int half = Pp / 2;
-  double* cs = hs + (size_t)Pp * Pp;        // [half][2]
+  const int LH = Pp + 1;                    // odd pitch: a row of H (stride LH) touches every bank
+  double* cs = hs + (size_t)LH * Pp;        // [half][2]
   int* pr = reinterpret_cast<int*>(cs + 2 * half);   // [half][2]
   // the rotation accumulator lives in shared memory when it fits (P <= 112), else in global memory
   double* Vw = vsm ? reinterpret_cast<double*>(pr + 2 * half + 2) : Vt;
@@ -132,13 +138,13 @@ __global__ void __launch_bounds__(1024) k_jacobi_eig(int P, const double* __rest
     const int r = e % Pp, c = e / Pp;
     double v = 0.0;
     if (r < P && c < P) v = 0.5 * (H[r + (int64_t)c * ldh] + H[c + (int64_t)r * ldh]);
-    hs[r + Pp * c] = v;
+    hs[r + LH * c] = v;
   }
   for (int e = tid; e < P * P; e += nt) Vw[e] = (e % P == e / P) ? 1.0 : 0.0;
   __shared__ double hmax_s;
   if (tid == 0) {
     double hm = 0.0;
-    for (int i = 0; i < P; ++i) hm = fmax(hm, fabs(hs[i + Pp * i]));
+    for (int i = 0; i < P; ++i) hm = fmax(hm, fabs(hs[i + LH * i]));
     hmax_s = hm;
   }
   __syncthreads();
@@ -160,8 +166,8 @@ __global__ void __launch_bounds__(1024) k_jacobi_eig(int P, const double* __rest
         }
         double c = 1.0, s = 0.0;
         if (q < P) {
-          const double apq = hs[p + Pp * q];
-          const double app = hs[p + Pp * p], aqq = hs[q + Pp * q];
+          const double apq = hs[p + LH * q];
+          const double app = hs[p + LH * p], aqq = hs[q + LH * q];
           if (fabs(apq) > abs_floor && fabs(apq) > DBL_EPSILON * 0.5 * sqrt(fabs(app)) * sqrt(fabs(aqq))) {
             const double tau = (aqq - app) / (2.0 * apq);
             double t;
@@ -186,9 +192,9 @@ __global__ void __launch_bounds__(1024) k_jacobi_eig(int P, const double* __rest
           const double c = cs[2 * k], s = cs[2 * k + 1];
           if (s == 0.0) continue;
           const int p = pr[2 * k], q = pr[2 * k + 1];
-          const double hp = hs[p + Pp * x], hq = hs[q + Pp * x];
-          hs[p + Pp * x] = c * hp - s * hq;
-          hs[q + Pp * x] = s * hp + c * hq;
+          const double hp = hs[p + LH * x], hq = hs[q + LH * x];
+          hs[p + LH * x] = c * hp - s * hq;
+          hs[q + LH * x] = s * hp + c * hq;
         }
       }
       __syncthreads();
@@ -198,9 +204,9 @@ __global__ void __launch_bounds__(1024) k_jacobi_eig(int P, const double* __rest
           const double c = cs[2 * k], s = cs[2 * k + 1];
           if (s == 0.0) continue;
           const int p = pr[2 * k], q = pr[2 * k + 1];
-          const double hp = hs[x + Pp * p], hq = hs[x + Pp * q];
-          hs[x + Pp * p] = x == q ? 0.0 : c * hp - s * hq;
-          hs[x + Pp * q] = x == p ? 0.0 : s * hp + c * hq;
+          const double hp = hs[x + LH * p], hq = hs[x + LH * q];
+          hs[x + LH * p] = x == q ? 0.0 : c * hp - s * hq;
+          hs[x + LH * q] = x == p ? 0.0 : s * hp + c * hq;
           if (x < P) {
             const double vp = Vw[x + (int64_t)P * p], vq = Vw[x + (int64_t)P * q];
             Vw[x + (int64_t)P * p] = c * vp - s * vq;
@@ -212,17 +218,23 @@ __global__ void __launch_bounds__(1024) k_jacobi_eig(int P, const double* __rest
     }
     const int any = rotated;
     __syncthreads();
+#ifdef TF_JACOBI_STATS
+    if (tid == 0) g_jac_sweeps[min(g_jac_calls, 63)] = sweep + 1;
+#endif
     if (!any) break;
   }
+#ifdef TF_JACOBI_STATS
+  if (tid == 0) g_jac_calls++;
+#endif
   // sort by |theta| decreasing, ties in index order: rank_i = #{j : |t_j| > |t_i| or (== and j < i)}
   for (int i = tid; i < P; i += nt) {
-    const double ti = fabs(hs[i + Pp * i]);
+    const double ti = fabs(hs[i + LH * i]);
     int rank = 0;
     for (int j = 0; j < P; ++j) {
-      const double tj = fabs(hs[j + Pp * j]);
+      const double tj = fabs(hs[j + LH * j]);
       rank += (tj > ti) || (tj == ti && j < i);
     }
-    theta[rank] = hs[i + Pp * i];
+    theta[rank] = hs[i + LH * i];
     for (int r = 0; r < P; ++r) V[r + (int64_t)P * rank] = Vw[r + (int64_t)P * i];
   }
 }
@@ -515,7 +527,7 @@ cudaError_t launch_house_qr(int64_t n, int P, double* Z, int64_t ldz, double* Q,
 cudaError_t launch_jacobi_eig(int P, const double* H, int64_t ldh, double* Vtmp, double* V, double* theta,
                               cudaStream_t st, int max_sweeps) {
   const int Pp = P + (P & 1);
-  size_t smem = (size_t)Pp * Pp * 8 + (size_t)Pp * 8 + (size_t)Pp * 4 + 16;
+  size_t smem = (size_t)(Pp + 1) * Pp * 8 + (size_t)Pp * 8 + (size_t)Pp * 4 + 16;
   const int vsm = smem + (size_t)P * P * 8 <= 220 * 1024;
   if (vsm) smem += (size_t)P * P * 8;
   cudaError_t e = cudaFuncSetAttribute(k_jacobi_eig, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -524,6 +536,19 @@ cudaError_t launch_jacobi_eig(int P, const double* H, int64_t ldh, double* Vtmp,
   return cudaGetLastError();
 }
 
+#ifdef TF_JACOBI_STATS
+}  // namespace tfk
+extern "C" void tf_jacobi_stats_dump() {
+  int h[64], n = 0;
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(&n, tfk::g_jac_calls, sizeof(int));
+  cudaMemcpyFromSymbol(h, tfk::g_jac_sweeps, sizeof(h));
+  printf("jacobi calls %d, sweeps:", n);
+  for (int i = 0; i < n && i < 64; ++i) printf(" %d", h[i]);
+  printf("\n");
+}
+namespace tfk {
+#endif
 cudaError_t launch_eig_residual(int64_t n, int P, const double* ZV, const double* U, int64_t ld, const double* theta,
                                 double* res, cudaStream_t st) {
   k_eig_residual<<<P, 256, 0, st>>>(n, ZV, U, ld, theta, res);
