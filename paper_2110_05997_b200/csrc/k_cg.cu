@@ -509,6 +509,151 @@ __global__ void __launch_bounds__(kCgThreads, 1) k_cg_persistent(CgArgs A) {
   }
 }
 
+// ---- small systems: the whole CG (or one matvec) in ONE CTA with every vector in shared memory. For
+// n = R (I + J + K) up to a few thousand the persistent grid kernel sits on a ~14 us per-iteration latency
+// floor (its stages talk through global memory and grid barriers); here a stage is a block barrier. Same
+// algorithm and formulas (Gram G_l = V_l^T W_l of V = D (r + beta p), S_l = sum Pi^(l,l') * G_l', Thm-Hv apply
+// z = D (V Pi^(l) + W S_l + lambda V), the CG recurrences), plain FP64 FMAs in a fixed per-thread order.
+constexpr int kCgSmallThreads = 1024;
+__host__ __device__ constexpr size_t cg_small_smem_doubles(int64_t n, int64_t R) {
+  return (size_t)6 * n + (size_t)12 * R * R + 64;
+}
+
+__device__ __forceinline__ double small_block_sum(double v, double* red) {
+  v = warp_sum(v);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
+  __syncthreads();
+  return t;
+}
+
+__global__ void __launch_bounds__(kCgSmallThreads, 1) k_cg_small(CgArgs A) {
+  extern __shared__ __align__(16) double sm[];
+  const Modes& m = A.m;
+  const int R = (int)m.R;
+  const int64_t RR = (int64_t)R * R;
+  const int64_t n = m.R * (m.n[0] + m.n[1] + m.n[2]);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double* sx = sm;
+  double* sr = sx + n;
+  double* sp = sr + n;          // current direction (raw)
+  double* sq = sp + n;          // new direction (raw) = r + beta p
+  double* sz = sq + n;
+  double* sW = sz + n;
+  double* sPi = sW + n;         // 6 R^2
+  double* sG = sPi + 6 * RR;    // 3 R^2
+  double* sS = sG + 3 * RR;     // 3 R^2
+  double* red = sS + 3 * RR;    // 64
+  auto dsc = [&](int64_t qi) -> double {   // Jacobi scale of element qi (1 without)
+    if (!A.dscale) return 1.0;
+    const int l = mode_of(m, qi);
+    return A.dscale[l * R + (qi - m.off[l]) / m.n[l]];
+  };
+  for (int64_t qi = tid; qi < n; qi += nt) {
+    const int l = mode_of(m, qi);
+    sW[qi] = m.W[l][qi - m.off[l]];
+  }
+  for (int64_t e = tid; e < 6 * RR; e += nt) sPi[e] = A.pi[e];
+  // z = D (V Pi + W S + lambda V) for V = D * sq (sq raw); returns this thread's share of <sq, z>
+  auto matvec = [&](bool scaled) -> double {
+    // Gram G_l[r + R s] = sum_a V[a, r] W[a, s]
+    for (int64_t e = tid; e < 3 * RR; e += nt) {
+      const int l = (int)(e / RR);
+      const int64_t rs = e % RR, r = rs % R, c = rs / R, nl = m.n[l], off = m.off[l];
+      const double dr = (scaled && A.dscale) ? A.dscale[l * R + r] : 1.0;
+      double acc = 0.0;
+      for (int64_t a = 0; a < nl; ++a) acc = fma(sq[off + a + nl * r], sW[off + a + nl * c], acc);
+      sG[e] = dr * acc;
+    }
+    __syncthreads();
+    for (int64_t qi = tid; qi < RR; qi += nt) {
+      const double p12 = sPi[3 * RR + qi], p13 = sPi[4 * RR + qi], p23 = sPi[5 * RR + qi];
+      const double g0 = sG[qi], g1 = sG[RR + qi], g2 = sG[2 * RR + qi];
+      sS[qi] = p12 * g1 + p13 * g2;
+      sS[RR + qi] = p12 * g0 + p23 * g2;
+      sS[2 * RR + qi] = p13 * g0 + p23 * g1;
+    }
+    __syncthreads();
+    double dsum = 0.0;
+    for (int64_t qi = tid; qi < n; qi += nt) {
+      const int l = mode_of(m, qi);
+      const int64_t nl = m.n[l], off = m.off[l], loc = qi - off, a = loc % nl, sc = loc / nl;
+      const double* P = sPi + l * RR;
+      const double* S = sS + l * RR;
+      const double* D = (scaled && A.dscale) ? A.dscale + l * R : nullptr;
+      double acc = 0.0;
+      for (int r = 0; r < R; ++r) {
+        const double vr = sq[off + a + nl * r] * (D ? D[r] : 1.0);
+        acc = fma(vr, P[r + (int64_t)R * sc], acc);
+      }
+      for (int r = 0; r < R; ++r) acc = fma(sW[off + a + nl * r], S[r + (int64_t)R * sc], acc);
+      const double pr = sq[qi];
+      const double ds = D ? D[sc] : 1.0;
+      const double lam = A.damp ? A.lambda * A.damp[l * R + sc] : A.lambda;
+      const double yv = ds * fma(lam, ds * pr, acc);
+      sz[qi] = yv;
+      dsum = fma(pr, yv, dsum);
+    }
+    __syncthreads();
+    return dsum;
+  };
+  if (A.mode == 1) {   // single matvec y = (J^T J + lambda I) v
+    for (int64_t qi = tid; qi < n; qi += nt) sq[qi] = A.v[qi];
+    __syncthreads();
+    matvec(false);
+    for (int64_t qi = tid; qi < n; qi += nt) A.x[qi] = sz[qi];
+    return;
+  }
+  double s0 = 0.0;
+  for (int64_t qi = tid; qi < n; qi += nt) {
+    const double v = A.rhs[qi] * dsc(qi);
+    sx[qi] = 0.0;
+    sr[qi] = v;
+    sp[qi] = 0.0;
+    s0 = fma(v, v, s0);
+  }
+  double rr = small_block_sum(s0, red);
+  double beta = 0.0;
+  int iters = 0, nonfinite = 0;
+  for (int it = 1; it <= A.maxiter; ++it) {
+    for (int64_t qi = tid; qi < n; qi += nt) sq[qi] = fma(beta, sp[qi], sr[qi]);
+    __syncthreads();
+    const double pz = small_block_sum(matvec(true), red);
+    const double alpha = rr / pz;
+    if (!isfinite(alpha)) {
+      nonfinite = it;
+      break;
+    }
+    double s2 = 0.0;
+    for (int64_t qi = tid; qi < n; qi += nt) {
+      sx[qi] = fma(alpha, sq[qi], sx[qi]);
+      const double rn = fma(-alpha, sz[qi], sr[qi]);
+      sr[qi] = rn;
+      sp[qi] = sq[qi];
+      s2 = fma(rn, rn, s2);
+    }
+    const double rr_new = small_block_sum(s2, red);
+    beta = rr_new / rr;
+    rr = rr_new;
+    iters = it;
+    if (!isfinite(beta)) {
+      nonfinite = it;
+      break;
+    }
+    if (rr_new < A.tol) break;
+  }
+  for (int64_t qi = tid; qi < n; qi += nt) A.x[qi] = sx[qi] * dsc(qi);
+  if (tid == 0) {
+    A.st->rr = rr;
+    A.st->iters = iters;
+    A.st->nonfinite = nonfinite;
+    A.st->done = 1;
+  }
+}
+
 template <int NT>
 static cudaError_t launch_persistent_nt(const CgArgs& a, int nsm, cudaStream_t st) {
   auto kern = k_cg_persistent<NT>;
@@ -551,6 +696,14 @@ cudaError_t launch_cg_persistent(const Modes& m, const double* pi, const double*
   a.part = part;
   a.st = st_dev;
   a.mode = mode;
+  const int64_t ntot = m.R * (m.n[0] + m.n[1] + m.n[2]);
+  const size_t small_smem = 8 * cg_small_smem_doubles(ntot, m.R);
+  if (ntot <= 4096 && small_smem <= 200 * 1024 && !cg_debug_tstamp()) {   // one CTA, vectors in shared memory
+    cudaError_t ea = cudaFuncSetAttribute(k_cg_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)small_smem);
+    if (ea != cudaSuccess) return ea;
+    k_cg_small<<<1, kCgSmallThreads, small_smem, st>>>(a);
+    return cudaGetLastError();
+  }
   const int NT = (int)((m.R + 7) / 8);
   switch (NT) {
 #define TF_CASE(k) \
