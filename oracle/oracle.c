@@ -433,6 +433,8 @@ int oracle_cg(int64_t I, int64_t J, int64_t K, int64_t R, const double *A, const
   ld rr = 0.0L;
   for (int64_t q = 0; q < n; ++q) { r[q] = minv[q] * (ld)rhs[q]; p[q] = r[q]; rr += r[q] * r[q]; }
   int it = 0;
+  /* reading R33: r^(0) = 0 (rhs = 0) is already solved by x^(0) = 0; the loop as printed would divide 0 by 0 */
+  if (rr == 0.0L) maxiter = 0;
   for (int i = 1; i <= maxiter; ++i) {
     /* z = B p in three steps */
     for (int64_t q = 0; q < n; ++q) tmp[q] = minv[q] * p[q];

@@ -431,7 +431,9 @@ __global__ void __launch_bounds__(kCgThreads, 1) k_cg_persistent(CgArgs A) {
   // current direction (the other column half of the same rows) never see a partially updated vector.
   double* pc = A.p;
   double* pn = A.p + n;
-  for (int it = 1; it <= A.maxiter; ++it) {
+  // reading R33: rhs = 0 is solved by x = 0 (the printed loop would compute alpha = 0 / 0)
+  const int maxit = rr == 0.0 ? 0 : A.maxiter;
+  for (int it = 1; it <= maxit; ++it) {
     VSrc V{A.r, pc, beta, A.dscale};
     const int sb = 8 * (it - 1);
     stamp(A, sb + 0);
@@ -618,7 +620,8 @@ __global__ void __launch_bounds__(kCgSmallThreads, 1) k_cg_small(CgArgs A) {
   double rr = small_block_sum(s0, red);
   double beta = 0.0;
   int iters = 0, nonfinite = 0;
-  for (int it = 1; it <= A.maxiter; ++it) {
+  const int maxit = rr == 0.0 ? 0 : A.maxiter;   // reading R33
+  for (int it = 1; it <= maxit; ++it) {
     for (int64_t qi = tid; qi < n; qi += nt) sq[qi] = fma(beta, sp[qi], sr[qi]);
     __syncthreads();
     const double pz = small_block_sum(matvec(true), red);

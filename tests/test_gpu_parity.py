@@ -640,3 +640,56 @@ def test_pi_form_shapes(ctx, dims):
     okf, ef, bf = within([fd.item()], [fr], f_floor(T_np, fr))
     okg, eg, bg = within(to_np(gd), gr, grad_floor(w_np, I, J, K, R))
     assert okf and okg, (dims, ef, bf, eg, bg)
+
+
+# ------------------------------------------------------------------------- degenerate points
+@pytest.mark.parametrize("form", ["residual", "pi"])
+@pytest.mark.parametrize("case", ["w_zero", "T_zero", "zero_columns", "rank_one_T"])
+def test_degenerate_points(ctx, form, case):
+    """Degenerate inputs in both algebraic forms against the oracle: all factors zero (F = 1/2 ||T||^2, grad = 0:
+    W Pi and the MTTKRPs both vanish), T = 0 (F = 1/2 ||[[W]]||^2, grad = W Pi), one zero column per factor
+    (singular Grams), and an exactly rank-one T evaluated at R = 4 with a perturbed copy of its factor."""
+    I, J, K, R = 33, 27, 19, 4
+    rng = np.random.default_rng(3)
+    T = rng.standard_normal((K, J, I))
+    w = rng.standard_normal(R * (I + J + K))
+    if case == "w_zero":
+        w[:] = 0.0
+    elif case == "T_zero":
+        T[:] = 0.0
+    elif case == "zero_columns":
+        for off, nl in ((0, I), (I * R, J), ((I + J) * R, K)):
+            w[off + nl * 2: off + nl * 3] = 0.0   # column r = 2 of every factor (w is [vec A | vec B | vec C])
+    elif case == "rank_one_T":
+        a, b, c = rng.standard_normal(I), rng.standard_normal(J), rng.standard_normal(K)
+        T = np.einsum("k,j,i->kji", c, b, a)
+        w = 0.1 * rng.standard_normal(R * (I + J + K))
+        w[0:I], w[I * R:I * R + J], w[(I + J) * R:(I + J) * R + K] = a, b, c
+    ctx.set_eval_form(form)
+    try:
+        check_eval(ctx, T.reshape(-1), w, I, J, K, R)
+    finally:
+        ctx.set_eval_form("auto")
+    if case == "w_zero":   # exact values, not only the oracle's
+        f, g = ctx.tf_cpd_eval(tf.Dims(I, J, K, R), torch.from_numpy(T.reshape(-1)).cuda(), torch.from_numpy(w).cuda())
+        assert abs(f.item() - 0.5 * float(np.sum(T * T))) <= 1e-13 * float(np.sum(T * T))
+        assert torch.count_nonzero(g).item() == 0
+
+
+@pytest.mark.parametrize("dims", [(6, 5, 4, 3), (60, 50, 40, 9)])   # the single-CTA and the grid CG kernels
+def test_cg_zero_rhs(ctx, dims):
+    """Reading R33: rhs = 0 returns x = 0 after zero iterations (no 0/0), like the oracle."""
+    I, J, K, R = dims
+    n = R * (I + J + K)
+    rng = np.random.default_rng(9)
+    w = torch.from_numpy(rng.standard_normal(n)).cuda()
+    d = tf.Dims(I, J, K, R)
+    grams = ctx.tf_grams(d, w)
+    x = torch.full((n,), 7.0, dtype=torch.float64, device="cuda")
+    for jacobi in (False, True):
+        _, iters, r2 = ctx.tf_cg_solve(d, grams, w, torch.zeros(n, dtype=torch.float64, device="cuda"), 1e-3, 10, 0.0,
+                                       jacobi, x)
+        assert iters == 0 and r2 == 0.0
+        assert torch.count_nonzero(x).item() == 0
+        ref = oracle.cg(to_np(w), np.zeros(n), 1e-3, 10, I, J, K, R, jacobi=jacobi)
+        assert ref["iters"] == 0 and ref["status"] == 0

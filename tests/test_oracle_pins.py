@@ -372,6 +372,17 @@ def test_cg_one_iteration_closed_form():
     np.testing.assert_allclose(outj["x"], m * ah * rh, rtol=1e-12)
 
 
+def test_cg_zero_rhs_is_solved_by_zero():
+    """Reading R33: r^(0) = 0 is solved by x^(0) = 0 = (J^T J + lam I)^{-1} 0 without iterating (the printed
+    loop would form alpha = 0/0), for the plain and the Jacobi system."""
+    I, J, K, R = 4, 3, 3, 2
+    w, H, rhs = _dense_system(I, J, K, R, 1e-3, seed=5)
+    for jacobi in (False, True):
+        out = oracle.cg(w, np.zeros_like(rhs), 1e-3, 5, I, J, K, R, jacobi=jacobi)
+        assert out["status"] == 0 and out["iters"] == 0
+        assert np.all(out["x"] == 0.0)
+
+
 def test_cg_residual_identity_and_monotone_energy():
     """ε = ‖r^(i)‖² equals ‖b − A x^(i)‖²; the A-norm error is monotone."""
     I, J, K, R = 4, 3, 3, 2
