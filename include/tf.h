@@ -113,7 +113,7 @@ tf_status tf_gn_matvec(tf_ctx *ctx, tf_dims d, const double *grams, const double
 
 /* a9: Alg. CG-dGN: solve (J^T J + lambda I) x = rhs with
  * x0 = 0, at most maxiter iterations, stopping when ||r||^2 < tol (tol = 0: run
- * exactly maxiter). jacobi != 0 preconditions with M = diag(J^T J) + lambda I as
+ * exactly maxiter; rhs = 0 returns x = 0 after zero iterations, reading R33). jacobi != 0 preconditions with M = diag(J^T J) + lambda I as
  * M^{-1/2} (.) M^{-1/2} and returns x in
  * w-coordinates (x = M^{-1/2} x_hat). The iteration runs on the device with no
  * host round trip; iters_done and res2 (host pointers, nullable) receive the
