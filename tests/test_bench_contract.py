@@ -24,3 +24,25 @@ def test_reference_arm_json_line():
     assert b["cpu_baseline"]["kind"] == "oracle" and b["cpu_baseline"]["cores"] >= 1
     assert b["e2e"]["h2d_bytes_per_step"] == 0 and b["e2e"]["d2h_bytes_per_step"] == 0
     assert b["config"]["workload"].startswith("c1")
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_our_arm_json_line():
+    """Our arm on a small config: the roofline, e2e, clocks and launch-count keys the driver checks."""
+    out = subprocess.run([sys.executable, "bench.py", "--config", "c2", "--steps", "3", "--warmup", "3",
+                          "--no-stages", "--no-cpu-baseline"], cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1
+    b = json.loads(lines[0])
+    assert b["value"] > 0 and b["n_gpus"] == 1 and b["warmup"] >= 3
+    r = b["roofline"]
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in r, k
+    assert 0 < r["frac"] <= 1.0 and r["bound"] in ("tensor", "hbm", "alu")
+    assert b["e2e"]["value"] > 0 and b["e2e"]["h2d_bytes_per_step"] > 0 and b["e2e"]["d2h_bytes_per_step"] > 0
+    assert b["gpu_launches"] > 0
+    assert "sm_mhz" in b["clocks"] and "reasons" in b["clocks"]
