@@ -82,6 +82,11 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src, bool v
                "r"(valid ? 8 : 0)
                : "memory");
 }
+// 16-byte copy with zero fill beyond src_bytes (0, 8 or 16)
+__device__ __forceinline__ void cp_async16(double* dst, const double* src, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
@@ -275,13 +280,29 @@ __device__ double stage_apply(const CgArgs& A, const VSrc& V, double* y, double*
     const double* va = V.a + off;
     const double* vb = V.b ? V.b + off : V.a + off;
     __syncthreads();   // previous item consumed the staging buffers
-    for (int idx = threadIdx.x; idx < YR * R4; idx += blockDim.x) {
-      const int a = idx % YR, kk = idx / YR;
-      const bool ok = kk < R && a0 + a < n;
-      const int64_t ix = ok ? a0 + a + n * kk : 0;
-      cp_async8(&sXr[kk * LDX + a], va + ix, ok);
-      cp_async8(&sXp[kk * LDX + a], vb + ix, ok && V.b != nullptr);
-      cp_async8(&sW[kk * LDX + a], W + ix, ok);
+    // 16-byte copies of row pairs when every column start is 16-byte aligned (n and the offsets even)
+    const bool pair16 = ((n | off | a0) & 1) == 0 && ((reinterpret_cast<uintptr_t>(V.a) | reinterpret_cast<uintptr_t>(W) |
+                                                      reinterpret_cast<uintptr_t>(V.b ? V.b : V.a)) & 15) == 0;
+    if (pair16) {
+      for (int idx = threadIdx.x; idx < (YR / 2) * R4; idx += blockDim.x) {
+        const int a = 2 * (idx % (YR / 2)), kk = idx / (YR / 2);
+        int64_t rem = n - (a0 + a);
+        rem = rem < 0 ? 0 : (rem > 2 ? 2 : rem);
+        const int valid = kk < R ? (int)rem : 0;   // rows of the pair in range
+        const int64_t ix = valid ? a0 + a + n * kk : 0;
+        cp_async16(&sXr[kk * LDX + a], va + ix, 8 * valid);
+        cp_async16(&sXp[kk * LDX + a], vb + ix, V.b != nullptr ? 8 * valid : 0);
+        cp_async16(&sW[kk * LDX + a], W + ix, 8 * valid);
+      }
+    } else {
+      for (int idx = threadIdx.x; idx < YR * R4; idx += blockDim.x) {
+        const int a = idx % YR, kk = idx / YR;
+        const bool ok = kk < R && a0 + a < n;
+        const int64_t ix = ok ? a0 + a + n * kk : 0;
+        cp_async8(&sXr[kk * LDX + a], va + ix, ok);
+        cp_async8(&sXp[kk * LDX + a], vb + ix, ok && V.b != nullptr);
+        cp_async8(&sW[kk * LDX + a], W + ix, ok);
+      }
     }
     // [Pi; S] columns: a warp copies 8 consecutive k x 4 columns (64-byte global runs; the shared-memory
     // rows kk*LDM, LDM = 4 mod 8, land on distinct banks)
