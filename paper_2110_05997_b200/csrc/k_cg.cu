@@ -119,15 +119,31 @@ __device__ void stage_gram(const CgArgs& A, const VSrc& V, double* smem) {
       dr[i] = (D && r < R) ? D[r] : 1.0;
     }
     double acc[MT][NT][2] = {};
+    const bool pair16 = ((n | off | zb) & 1) == 0 &&
+                        ((reinterpret_cast<uintptr_t>(V.a) | reinterpret_cast<uintptr_t>(W) |
+                          reinterpret_cast<uintptr_t>(hasP ? V.b : V.a)) & 15) == 0;
     for (int64_t c0 = zb; c0 < ze; c0 += kGRows) {
       __syncthreads();   // the previous chunk (or item) is consumed
-      for (int idx = threadIdx.x; idx < kGRows * R4; idx += blockDim.x) {
-        const int a = idx % kGRows, col = idx / kGRows;
-        const bool ok = col < R && c0 + a < ze;
-        const int64_t ix = ok ? c0 + a + n * col : 0;
-        cp_async8(&sR[col * kGLd + a], V.a + off + ix, ok);
-        if (hasP) cp_async8(&sP[col * kGLd + a], V.b + off + ix, ok);
-        cp_async8(&sW[col * kGLd + a], W + ix, ok);
+      if (pair16) {   // 16-byte row pairs (every column start aligned)
+        for (int idx = threadIdx.x; idx < (kGRows / 2) * R4; idx += blockDim.x) {
+          const int a = 2 * (idx % (kGRows / 2)), col = idx / (kGRows / 2);
+          int64_t rem = ze - (c0 + a);
+          rem = rem < 0 ? 0 : (rem > 2 ? 2 : rem);
+          const int valid = col < R ? (int)rem : 0;
+          const int64_t ix = valid ? c0 + a + n * col : 0;
+          cp_async16(&sR[col * kGLd + a], V.a + off + ix, 8 * valid);
+          if (hasP) cp_async16(&sP[col * kGLd + a], V.b + off + ix, 8 * valid);
+          cp_async16(&sW[col * kGLd + a], W + ix, 8 * valid);
+        }
+      } else {
+        for (int idx = threadIdx.x; idx < kGRows * R4; idx += blockDim.x) {
+          const int a = idx % kGRows, col = idx / kGRows;
+          const bool ok = col < R && c0 + a < ze;
+          const int64_t ix = ok ? c0 + a + n * col : 0;
+          cp_async8(&sR[col * kGLd + a], V.a + off + ix, ok);
+          if (hasP) cp_async8(&sP[col * kGLd + a], V.b + off + ix, ok);
+          cp_async8(&sW[col * kGLd + a], W + ix, ok);
+        }
       }
       cp_async_wait_all();
       __syncthreads();
