@@ -238,7 +238,7 @@ __host__ __device__ constexpr int apply_rows() { return NT > 13 ? 16 : 32; }
 
 template <int NT>
 __host__ __device__ constexpr size_t apply_smem_doubles(int R4) {
-  return (size_t)3 * R4 * (apply_rows<NT>() + 8) + (size_t)(2 * R4) * (8 * ((NT + 1) / 2) + 4);
+  return (size_t)3 * R4 * (apply_rows<NT>() + 8) + (size_t)(8 * ((NT + 1) / 2)) * (2 * R4 + 16);
 }
 
 template <int NT>
@@ -248,7 +248,6 @@ __device__ double stage_apply(const CgArgs& A, const VSrc& V, double* y, double*
   constexpr int WG = 8 / MT;                 // warps sharing one m-tile
   constexpr int NTH = (NT + 1) / 2;          // n-tiles per column half
   constexpr int NTW = (NTH + WG - 1) / WG;   // n-tiles per warp
-  constexpr int LDM = 8 * NTH + 4;
   const Modes& m = A.m;
   const int R = (int)m.R;
   const int64_t RR = (int64_t)R * R;
@@ -258,7 +257,10 @@ __device__ double stage_apply(const CgArgs& A, const VSrc& V, double* y, double*
   double* sXr = smem;                        // [R4][LDX]
   double* sXp = sXr + R4 * LDX;
   double* sW = sXp + R4 * LDX;
-  double* sM = sW + R4 * LDX;                // [2 R4][LDM]
+  // [Pi; S] columns of the half, transposed: sMT[c][k] (k < R4: Pi, R4 + k: S) with a pitch of 4 mod 16
+  // doubles: contiguous (16-byte) copies of Pi's columns, conflict-free B fragments (lane (g,q) -> 4g + q)
+  const int LDMT = 2 * R4 + ((4 - 2 * R4) % 16 + 16) % 16;
+  double* sMT = sW + R4 * LDX;                // [8 NTH][LDMT]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
   const int mt = warp % MT, tw = warp / MT;
   const int nh = NT > 1 ? 2 : 1;
@@ -320,20 +322,29 @@ __device__ double stage_apply(const CgArgs& A, const VSrc& V, double* y, double*
         cp_async8(&sW[kk * LDX + a], W + ix, ok);
       }
     }
-    // [Pi; S] columns: a warp copies 8 consecutive k x 4 columns (64-byte global runs; the shared-memory
-    // rows kk*LDM, LDM = 4 mod 8, land on distinct banks)
-    const int nkb = (R4 + 7) / 8;
+    // [Pi; S] columns of the half (restaged only when the mode or half changes): 16-byte k-pairs when R is even
     const bool restage = l != staged_l || h != staged_h;
     staged_l = l;
     staged_h = h;
-    for (int idx = threadIdx.x; restage && idx < nkb * 8 * 8 * NTH; idx += blockDim.x) {
-      const int ln = idx & 31, blk = idx >> 5;
-      const int kk = 8 * (blk % nkb) + (ln & 7), cc = 4 * (blk / nkb) + (ln >> 3);
-      if (kk >= R4) continue;
-      const bool ok = kk < R && s_lo + cc < R;
-      const int64_t ix = ok ? kk + (int64_t)R * (s_lo + cc) : 0;
-      cp_async8(&sM[kk * LDM + cc], P + ix, ok);
-      cp_async8(&sM[(R4 + kk) * LDM + cc], Sl + ix, ok);
+    if (restage) {
+      const bool kpair = (R & 1) == 0 && ((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(Sl)) & 15) == 0;
+      if (kpair) {
+        for (int idx = threadIdx.x; idx < (R4 / 2) * 8 * NTH; idx += blockDim.x) {
+          const int kk = 2 * (idx % (R4 / 2)), cc = idx / (R4 / 2);
+          const int valid = (s_lo + cc < R) ? (kk + 1 < R ? 16 : (kk < R ? 8 : 0)) : 0;
+          const int64_t ix = valid ? kk + (int64_t)R * (s_lo + cc) : 0;
+          cp_async16(&sMT[cc * LDMT + kk], P + ix, valid);
+          cp_async16(&sMT[cc * LDMT + R4 + kk], Sl + ix, valid);
+        }
+      } else {
+        for (int idx = threadIdx.x; idx < R4 * 8 * NTH; idx += blockDim.x) {
+          const int kk = idx % R4, cc = idx / R4;
+          const bool ok = kk < R && s_lo + cc < R;
+          const int64_t ix = ok ? kk + (int64_t)R * (s_lo + cc) : 0;
+          cp_async8(&sMT[cc * LDMT + kk], P + ix, ok);
+          cp_async8(&sMT[cc * LDMT + R4 + kk], Sl + ix, ok);
+        }
+      }
     }
     cp_async_wait_all();
     __syncthreads();
@@ -349,7 +360,7 @@ __device__ double stage_apply(const CgArgs& A, const VSrc& V, double* y, double*
 #pragma unroll
       for (int j = 0; j < NTW; ++j) {
         const int tl = tw + WG * j;
-        if (tl < NTH && t0 + tl < NT) dmma(acc[j], fa, sM[r * LDM + 8 * tl + g]);
+        if (tl < NTH && t0 + tl < NT) dmma(acc[j], fa, sMT[(8 * tl + g) * LDMT + r]);
       }
     }
     // W S_l
@@ -360,7 +371,7 @@ __device__ double stage_apply(const CgArgs& A, const VSrc& V, double* y, double*
 #pragma unroll
       for (int j = 0; j < NTW; ++j) {
         const int tl = tw + WG * j;
-        if (tl < NTH && t0 + tl < NT) dmma(acc[j], fa, sM[(R4 + r) * LDM + 8 * tl + g]);
+        if (tl < NTH && t0 + tl < NT) dmma(acc[j], fa, sMT[(8 * tl + g) * LDMT + R4 + r]);
       }
     }
     stamp(A, 42 + 4 * nit);
