@@ -279,7 +279,7 @@ def test_gn_matvec_against_plain_route(ctx):
 
 
 @pytest.mark.parametrize("jacobi", [False, True])
-@pytest.mark.parametrize("case", ["c1", "c3r", "r120"])
+@pytest.mark.parametrize("case", ["c1", "c3r", "r120", "even30", "even31"])
 def test_cg_per_iteration(ctx, case, jacobi):
     """Every CG iterate x^(i), i = 1..10, against Alg. CG-dGN in the oracle (rhs = -grad, lambda = 1e-3)."""
     if case == "c1":
@@ -290,9 +290,14 @@ def test_cg_per_iteration(ctx, case, jacobi):
         P = synth.make_problem("c3", "cpu", dims=(60, 50, 40, 20))
         I, J, K, R = 60, 50, 40, 20
         w = to_np(P.w("random"))
-    else:   # R > 104 exercises the 16-row apply tiles of the persistent CG kernel
+    elif case == "r120":   # R > 104 exercises the 16-row apply tiles of the persistent CG kernel
         P = synth.make_problem("c5", "cpu", dims=(37, 29, 23, 120))
         I, J, K, R = 37, 29, 23, 120
+        w = to_np(P.w("random"))
+    else:   # n > 4096 with even mode sizes: the grid kernel's 16-byte staging paths (R even: also [Pi; S] pairs)
+        I, J, K = 80, 64, 48
+        R = 30 if case == "even30" else 31
+        P = synth.make_problem("c3", "cpu", dims=(I, J, K, R))
         w = to_np(P.w("random"))
     T = to_np(P.T).reshape(-1)
     _, grad = oracle.cpd_eval(T, w, I, J, K, R)
