@@ -311,9 +311,23 @@ tf_status tf_als(tf_ctx *ctx, tf_dims d, const double *T, double *w, int sweeps,
  *     (three contractions, 6*I*J*K*R flops). The environment variable TF_EVAL_FORM=residual selects 1
  *     for new contexts. */
 tf_status tf_ctx_set_eval_form(tf_ctx *ctx, int form);
-/* Synchronizes and reports whether the last guarded Pi-form evaluation on this ctx fell back to the
- * residual form (1), did not (0), or no Pi-form evaluation has run (-1). */
+/* Synchronizes and reports whether the last evaluation on this ctx ran the guarded Pi form and fell back
+ * to the residual form (1), ran it without falling back (0), or did not run the Pi form at all (-1: no
+ * evaluation yet, or the last one was a residual-form evaluation). */
 tf_status tf_ctx_eval_fallback(tf_ctx *ctx, int *fell_back);
+/* Which load path the last tf_cpd_eval on this ctx ran (the library may fall back instead
+ * of failing on alignment, but must say which path it ran): *tma = 1 when the frontal-slice tiles were
+ * staged by TMA (cp.async.bulk.tensor; T 16-byte aligned and ldT even), 0 when T is not 16-byte aligned or
+ * ldT is odd and the kernel loaded the tiles with cooperative 8-byte loads, -1 before the first evaluation.
+ * Both paths compute the same values. */
+tf_status tf_ctx_eval_path(tf_ctx *ctx, int *tma);
+
+/* Test/diagnostic knob for the persistent CG and GN-matvec kernel (rows a8/a9): nblocks > 0 launches the
+ * grid kernel with min(nblocks, #SMs) blocks (and never the single-CTA kernel for small systems), so that
+ * every block processes several work items at small sizes, as it does at c5 on the full grid; 0 (default)
+ * restores the normal choice (all SMs; one CTA for n <= 4096). Same arithmetic and the same results to
+ * rounding; TF_ERR_ARG if nblocks < 0. */
+tf_status tf_ctx_set_cg_grid(tf_ctx *ctx, int nblocks);
 
 /* K-sharded dGN loop: every rank holds slices k_begin .. k_begin+K-1 of T (d.K local,
  * d.K_total global) and the full w; each evaluation's partial [grad | F] and the tensor sums are summed over

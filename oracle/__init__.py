@@ -65,6 +65,8 @@ def lib():
             L.oracle_jtj_diag.argtypes = [_i64] * 4 + [_d] * 4
             L.oracle_cg.argtypes = ([_i64] * 4 + [_d] * 4 + [ctypes.c_double, _d, ctypes.c_int, ctypes.c_double,
                                     ctypes.c_int] + [_d] * 5 + [ctypes.POINTER(ctypes.c_int)])
+            L.oracle_dgn_stop.argtypes = [ctypes.c_int, _d, ctypes.c_int] + [ctypes.c_double] * 4
+            L.oracle_dgn_stop.restype = ctypes.c_int
             L.oracle_dgn.argtypes = ([_i64] * 4 + [_d, _d, ctypes.c_int, ctypes.c_double, ctypes.c_double] +
                                      [ctypes.c_int] * 3 + [ctypes.POINTER(ctypes.c_int)] * 3 + [_d, _d, ctypes.c_int])
             _lib = L
@@ -225,3 +227,11 @@ def dgn(T, w0, I, J, K, R, cg_iters, maxiter=None, tol=1e-6, mu0=0.0, use_gamma=
                      cgi.ctypes.data_as(ctypes.POINTER(ctypes.c_int)), ctypes.byref(it), ctypes.byref(why),
                      ctypes.byref(f), _p(hist), nthreads)
     return {"w": w, "iters": it.value, "reason": why.value, "f": f.value, "hist": hist.reshape(-1, 5)[:it.value]}
+
+
+def dgn_stop(k, rel, maxiter, tol, step, ginf, normT2):
+    """The dGN stopping rule at iteration k: the first condition 1..7 that holds, or 0.
+    rel = relative errors after 0..k iterations (at least k + 1 values)."""
+    r = np.ascontiguousarray(np.asarray(rel, dtype=np.float64))
+    assert r.size >= k + 1 and k >= 1
+    return int(lib().oracle_dgn_stop(int(k), _p(r), int(maxiter), float(tol), float(step), float(ginf), float(normT2)))

@@ -502,6 +502,38 @@ static ld linearized_half_sq(int64_t I, int64_t J, int64_t K, int64_t R, const d
   return 0.5L * s;
 }
 
+/*
+ * The stopping conditions of the dGN loop, checked at iteration k >= 1 in the paper's
+ * order; returns the first that holds (1..7) or 0. rel[0..k] = ||S - S^(k)|| / ||S|| (relative errors after
+ * 0..k iterations), step = ||w^(k-1) - w^(k)|| (reading R20: the Gauss-Newton step x before balancing),
+ * ginf = ||grad F(w^(k))||_inf, nT2 = ||T||^2.
+ *   1 relative error          rel[k] < tol
+ *   2 step size               step < tol
+ *   3 rel. error improvement  |rel[k-1] - rel[k]| < tol
+ *   4 gradient norm           ginf < tol
+ *   5 average error           mean(rel over [k-2c, k-c)) - mean(rel over [k-c, k)) < tol
+ *   6 average improvement     (1/c) sum_{t in [k-c, k)} |rel[t] - rel[t+1]| < 1e-3 (1/c) sum_{t in [k-c, k)} rel[t]
+ *     (5 and 6 only when k > 2c and k = 0 mod c, c = 1 + ceil(maxiter / 10); reading R21)
+ *   7 divergence              rel[k] > max(1, ||T||^2) / (1e-16 + tol)
+ */
+int oracle_dgn_stop(int k, const double *rel, int maxiter, double tol, double step, double ginf, double nT2) {
+  const int c = 1 + (maxiter + 9) / 10;   /* c = 1 + ceil(maxiter / 10) */
+  if (rel[k] < tol) return 1;
+  if (step < tol) return 2;
+  if (fabs(rel[k - 1] - rel[k]) < tol) return 3;
+  if (ginf < tol) return 4;
+  if (k > 2 * c && k % c == 0) {
+    ld m1 = 0.0L, m2 = 0.0L, imp = 0.0L;
+    for (int t = k - 2 * c; t < k - c; ++t) m1 += rel[t];
+    for (int t = k - c; t < k; ++t) { m2 += rel[t]; imp += fabsl((ld)rel[t] - (ld)rel[t + 1]); }
+    m1 /= c; m2 /= c; imp /= c;
+    if (m1 - m2 < (ld)tol) return 5;
+    if (imp < 1e-3L * m2) return 6;
+  }
+  if ((ld)rel[k] > ((ld)nT2 > 1.0L ? (ld)nT2 : 1.0L) / (1e-16L + (ld)tol)) return 7;
+  return 0;
+}
+
 int oracle_dgn(int64_t I, int64_t J, int64_t K, int64_t R, const double *T, double *w, int maxiter, double tol,
                double mu0, int use_gamma, int jacobi, int balance, const int *cg_iters, int *iters, int *reason,
                double *f_out, double *hist, int nthreads) {
@@ -520,7 +552,6 @@ int oracle_dgn(int64_t I, int64_t J, int64_t K, int64_t R, const double *T, doub
   double *gA = grad, *gB = grad + I * R, *gC = grad + (I + J) * R;
   oracle_eval(I, J, K, R, T, w, w + I * R, w + (I + J) * R, &F, gA, gB, gC, nthreads);
   rel[0] = (double)(sqrtl(2.0L * (ld)F) / normT);
-  const int c = 1 + (maxiter + 9) / 10;   /* c = 1 + ceil(maxiter / 10) */
   int it = 0, why = 0;
   for (int k = 1; k <= maxiter; ++k) {
     const double *A = w, *B = w + I * R, *C = w + (I + J) * R;
@@ -575,20 +606,8 @@ int oracle_dgn(int64_t I, int64_t J, int64_t K, int64_t R, const double *T, doub
     if (!isfinite(F)) { why = 8; break; }
     ld ginf = 0.0L;
     for (int64_t q = 0; q < n; ++q) if (fabsl((ld)grad[q]) > ginf) ginf = fabsl((ld)grad[q]);
-    /* stopping conditions in the paper's order */
-    if (rel[k] < tol) { why = 1; break; }
-    if (sqrtl(step2) < (ld)tol) { why = 2; break; }
-    if (fabs(rel[k - 1] - rel[k]) < tol) { why = 3; break; }
-    if (ginf < (ld)tol) { why = 4; break; }
-    if (k > 2 * c && k % c == 0) {
-      ld m1 = 0.0L, m2 = 0.0L, imp = 0.0L;
-      for (int t = k - 2 * c; t < k - c; ++t) m1 += rel[t];
-      for (int t = k - c; t < k; ++t) { m2 += rel[t]; imp += fabsl((ld)rel[t] - (ld)rel[t + 1]); }
-      m1 /= c; m2 /= c; imp /= c;
-      if (m1 - m2 < (ld)tol) { why = 5; break; }
-      if (imp < 1e-3L * m2) { why = 6; break; }
-    }
-    if ((ld)rel[k] > (nT2 > 1.0L ? nT2 : 1.0L) / (1e-16L + (ld)tol)) { why = 7; break; }
+    why = oracle_dgn_stop(k, rel, maxiter, tol, (double)sqrtl(step2), (double)ginf, (double)nT2);
+    if (why) break;
   }
   if (iters) *iters = it;
   if (reason) *reason = why;

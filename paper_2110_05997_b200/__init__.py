@@ -69,6 +69,8 @@ _lib.tf_cpd_dgn.argtypes = [_vp, TfDims, _vp, _vp, ctypes.POINTER(TfDgnParams), 
                             ctypes.POINTER(ctypes.c_double)]
 _lib.tf_ctx_set_timing.argtypes = [_vp, ctypes.c_int]
 _lib.tf_ctx_set_eval_form.argtypes = [_vp, ctypes.c_int]
+_lib.tf_ctx_set_cg_grid.argtypes = [_vp, ctypes.c_int]
+_lib.tf_ctx_eval_path.argtypes = [_vp, ctypes.POINTER(ctypes.c_int)]
 _lib.tf_cpd_dgn_sharded.argtypes = [_vp, TfDims, _vp, _vp, ctypes.POINTER(TfDgnParams), ctypes.POINTER(TfDgnResult),
                                     ctypes.POINTER(ctypes.c_double), ALLREDUCE_FN, ctypes.c_void_p, _vp]
 _lib.tf_ctx_eval_fallback.argtypes = [_vp, ctypes.POINTER(ctypes.c_int)]
@@ -114,7 +116,7 @@ EXPORTED = ["tf_ctx_create", "tf_ctx_destroy", "tf_ctx_set_stream", "tf_status_s
             "tf_grams", "tf_hadamard", "tf_cpd_eval", "tf_cpd_eval_host", "tf_gn_matvec", "tf_cg_solve",
             "tf_reg_gamma", "tf_gn_matvec_damped", "tf_cg_solve_damped", "tf_cpd_dgn", "tf_ctx_set_timing",
             "tf_ctx_kernel_stats", "tf_unfolding_grams", "tf_sym_eig_top", "tf_multilinear_core", "tf_compress",
-            "tf_energy_init", "tf_uncompress", "tf_cpd", "tf_mttkrp", "tf_als", "tf_ctx_set_eval_form",
+            "tf_energy_init", "tf_uncompress", "tf_cpd", "tf_mttkrp", "tf_als", "tf_ctx_set_eval_form", "tf_ctx_set_cg_grid", "tf_ctx_eval_path",
             "tf_ctx_eval_fallback", "tf_cpd_dgn_sharded", "tf_compress_st",
             "tf_compress_st_sharded", "tf_cpd_sharded"]
 
@@ -600,8 +602,19 @@ class Context:
         size) or 'residual' (6IJKR flops) for tf_cpd_eval."""
         self._check(_lib.tf_ctx_set_eval_form(self._h, {"auto": 0, "residual": 1, "pi": 2}[form]))
 
+    def eval_used_tma(self) -> int:
+        """1 if the last evaluation staged T by TMA, 0 if by cooperative loads (unaligned T / odd ldT), -1 none."""
+        v = ctypes.c_int()
+        self._check(_lib.tf_ctx_eval_path(self._h, ctypes.byref(v)))
+        return v.value
+
+    def set_cg_grid(self, nblocks: int):
+        """Grid size of the persistent CG / matvec kernel (0 = default; > 0: that many blocks, grid kernel)."""
+        self._check(_lib.tf_ctx_set_cg_grid(self._h, int(nblocks)))
+
     def eval_fell_back(self) -> int:
-        """1 if the last guarded Pi-form evaluation reran the residual form, 0 if not, -1 if none ran."""
+        """1 if the last evaluation ran the guarded Pi form and reran the residual form, 0 if the Pi form held,
+        -1 if the last evaluation did not run the Pi form."""
         v = ctypes.c_int()
         self._check(_lib.tf_ctx_eval_fallback(self._h, ctypes.byref(v)))
         return v.value

@@ -726,7 +726,7 @@ cudaError_t launch_cg_persistent(const Modes& m, const double* pi, const double*
                                  double lambda, double tol,
                                  int maxiter, const double* rhs, const double* v, double* x, double* r, double* p,
                                  double* z, double* G, double* S, double* part, CgState* st_dev, int mode, int nsm,
-                                 cudaStream_t st) {
+                                 bool allow_small, cudaStream_t st) {
   CgArgs a;
   a.S = S;
   a.tstamp = cg_debug_tstamp();
@@ -749,7 +749,7 @@ cudaError_t launch_cg_persistent(const Modes& m, const double* pi, const double*
   a.mode = mode;
   const int64_t ntot = m.R * (m.n[0] + m.n[1] + m.n[2]);
   const size_t small_smem = 8 * cg_small_smem_doubles(ntot, m.R);
-  if (ntot <= 4096 && small_smem <= 200 * 1024 && !cg_debug_tstamp()) {   // one CTA, vectors in shared memory
+  if (allow_small && ntot <= 4096 && small_smem <= 200 * 1024 && !cg_debug_tstamp()) {   // one CTA, vectors in shared memory
     cudaError_t ea = cudaFuncSetAttribute(k_cg_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)small_smem);
     if (ea != cudaSuccess) return ea;
     k_cg_small<<<1, kCgSmallThreads, small_smem, st>>>(a);

@@ -337,14 +337,18 @@ __global__ void __launch_bounds__(256) k_partial_final(int nblk, int ncomp, int 
   }
 }
 
-__global__ void k_axpy_inplace(int64_t n, const double* __restrict__ x, double* __restrict__ w) {
+// gate (nullable): the CG state of the step; a CG that met a non-finite alpha/beta leaves w untouched (the dGN
+// loop then stops with reason 8 at w^(k-1), as the oracle does)
+__global__ void k_axpy_inplace(int64_t n, const double* __restrict__ x, double* __restrict__ w, const CgState* gate) {
+  if (gate && gate->nonfinite) return;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
     w[q] += x[q];
 }
 
 // Norm balancing: column r of every mode gets the norm (prod_l ||w_r^(l)||)^(1/3); column
 // norms from the Grams' diagonals. Columns of a rank-one term with a zero factor are left unchanged.
-__global__ void k_balance(Modes m, const double* __restrict__ grams, double* __restrict__ w) {
+__global__ void k_balance(Modes m, const double* __restrict__ grams, double* __restrict__ w, const CgState* gate) {
+  if (gate && gate->nonfinite) return;
   const int64_t R = m.R, RR = R * R;
   const int64_t n = R * (m.n[0] + m.n[1] + m.n[2]);
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
@@ -382,14 +386,14 @@ cudaError_t launch_scale_copy(int64_t n, double alpha, const double* x, double* 
   return cudaGetLastError();
 }
 
-cudaError_t launch_axpy_inplace(int64_t n, const double* x, double* w, cudaStream_t st) {
-  k_axpy_inplace<<<vec_blocks(n), 256, 0, st>>>(n, x, w);
+cudaError_t launch_axpy_inplace(int64_t n, const double* x, double* w, const CgState* gate, cudaStream_t st) {
+  k_axpy_inplace<<<vec_blocks(n), 256, 0, st>>>(n, x, w, gate);
   return cudaGetLastError();
 }
 
-cudaError_t launch_balance(const Modes& m, const double* grams, double* w, cudaStream_t st) {
+cudaError_t launch_balance(const Modes& m, const double* grams, double* w, const CgState* gate, cudaStream_t st) {
   const int64_t n = m.R * (m.n[0] + m.n[1] + m.n[2]);
-  k_balance<<<vec_blocks(n), 256, 0, st>>>(m, grams, w);
+  k_balance<<<vec_blocks(n), 256, 0, st>>>(m, grams, w, gate);
   return cudaGetLastError();
 }
 

@@ -41,7 +41,10 @@ tf_status ensure(tf_ctx* c, DevBuf& b, size_t bytes) {
   if (bytes == 0) bytes = 8;
   if (b.cap >= bytes) return TF_OK;
   if (b.p) {
+    // the buffer may still be read or written by work on either library stream (the host-staged path copies
+    // on copy_stream): both must be idle before it is freed
     cudaStreamSynchronize(c->stream);
+    if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
     cudaFree(b.p);
     b.p = nullptr;
     b.cap = 0;
@@ -230,6 +233,7 @@ tf_status eval_impl(tf_ctx* c, const tf_dims& d, const double* T, const double* 
   // (small problems are launch-bound: the Pi form's extra launches — Grams, guard, conditional fallback —
   // would cost more than the reconstruction flops it saves, hence the 5e9-flop threshold above)
   c->last_eval_pi = pi_form;
+  c->last_eval_tma = tma ? 1 : 0;
   if (!pi_form) {
     TF_CUDA(c, launch_eval(&map, T, p, NT, tma, BT, c->stream));
     if (c->timing) TF_CUDA(c, cudaEventRecord(e1, c->stream));
@@ -389,10 +393,23 @@ tf_status tf_ctx_set_eval_form(tf_ctx* c, int form) {
   return TF_OK;
 }
 
+tf_status tf_ctx_eval_path(tf_ctx* c, int* tma) {
+  if (!c || !tma) return TF_ERR_ARG;
+  *tma = c->last_eval_tma;
+  return TF_OK;
+}
+
+tf_status tf_ctx_set_cg_grid(tf_ctx* c, int nblocks) {
+  if (!c) return TF_ERR_ARG;
+  if (nblocks < 0) return set_err(c, TF_ERR_ARG, "nblocks must be >= 0");
+  c->cg_grid = nblocks;
+  return TF_OK;
+}
+
 tf_status tf_ctx_eval_fallback(tf_ctx* c, int* fell_back) {
   if (!c || !fell_back) return TF_ERR_ARG;
   *fell_back = -1;
-  if (!c->evPart.p) return TF_OK;
+  if (!c->evPart.p || !c->last_eval_pi) return TF_OK;   // -1: the last evaluation did not run the Pi form
   cudaSetDevice(c->device);
   const int nblk = eval_pi_blocks(c->nsm);
   int v = -1;
@@ -569,7 +586,7 @@ tf_status tf_gn_matvec_damped(tf_ctx* c, tf_dims d, const double* grams, const d
   if ((s = matvec_ws(c, d, m, ws))) return s;
   TF_CUDA(c, launch_hadamard(d.R, grams, ws.pi, c->stream));
   TF_CUDA(c, launch_cg_persistent(m, ws.pi, nullptr, damp, lambda, 0.0, 0, nullptr, v, y, nullptr, nullptr, nullptr,
-                                  ws.G, ws.S, ws.partial, nullptr, 1, c->nsm, c->stream));
+                                  ws.G, ws.S, ws.partial, nullptr, 1, cg_grid(c), c->cg_grid == 0, c->stream));
   c->total_launches += 2;
   return TF_OK;
 }
@@ -597,7 +614,7 @@ static tf_status cg_impl(tf_ctx* c, const tf_dims& d, const double* grams, const
   if (jacobi) TF_CUDA(c, launch_jacobi_scale(m, ws.pi, lambda, damp, ws.dscale, c->stream));
   TF_CUDA(c, launch_cg_persistent(m, ws.pi, jacobi ? ws.dscale : nullptr, damp, lambda, tol, maxiter, rhs, nullptr, x,
                                   (double*)c->cgR.p, (double*)c->cgP.p, (double*)c->cgZ.p, ws.G, ws.S, ws.partial, st,
-                                  0, c->nsm, c->stream));
+                                  0, cg_grid(c), c->cg_grid == 0, c->stream));
   c->total_launches += 2 + (jacobi ? 1 : 0);
   return TF_OK;
 }
@@ -717,13 +734,16 @@ tf_status dgn_impl(tf_ctx* c, tf_dims d, const double* T, double* w, const tf_dg
       if ((s = matvec_ws(c, d, m, ws))) return s;
       TF_CUDA(c, launch_hadamard(d.R, grams, ws.pi, c->stream));
       TF_CUDA(c, launch_cg_persistent(m, ws.pi, nullptr, nullptr, 0.0, 0.0, 0, nullptr, x, y, nullptr, nullptr,
-                                      nullptr, ws.G, ws.S, ws.partial, nullptr, 1, c->nsm, c->stream));
+                                      nullptr, ws.G, ws.S, ws.partial, nullptr, 1, cg_grid(c), c->cg_grid == 0, c->stream));
     }
     TF_CUDA(c, launch_dots(n, grad, x, y, part, scal + 4, c->stream));   // {g.x, x.JtJx, x.x, max|g_old|}
-    TF_CUDA(c, launch_axpy_inplace(n, x, w, c->stream));                 // w^(k) = w^(k-1) + x
+    // w^(k) = w^(k-1) + x; the step and the balancing are skipped on the device when the CG met a non-finite
+    // alpha/beta (reason 8 below leaves w = w^(k-1), as Alg. CG-dGN's caller in the oracle does)
+    const CgState* gate = (const CgState*)c->cgState.p;
+    TF_CUDA(c, launch_axpy_inplace(n, x, w, gate, c->stream));
     if (prm->balance) {
       if ((s = grams_impl(c, d, w, grams))) return s;
-      TF_CUDA(c, launch_balance(m, grams, w, c->stream));
+      TF_CUDA(c, launch_balance(m, grams, w, gate, c->stream));
     }
     if ((s = eval_global())) return s;                                   // F, grad at w^(k)
     if ((s = grams_impl(c, d, w, grams))) return s;

@@ -11,6 +11,9 @@ struct DevBuf {
   size_t cap = 0;
 };
 
+struct tf_ctx;
+inline int cg_grid(const tf_ctx* c);
+
 struct tf_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -28,7 +31,9 @@ struct tf_ctx {
   DevBuf cpdU, cpdSig, cpdS, cpdW, cpdGrad, cpdScal;   // tf_cpd pipeline
   DevBuf alsKR, alsM, alsSmall, alsF;                 // CP-ALS
   DevBuf evGrams, evPart;                             // Pi-form evaluation: local Grams, guard partials
+  int cg_grid = 0;                                    // 0: default CG launch; > 0: grid kernel with that many blocks
   int eval_form = 0;                                  // 0 auto, 1 residual form, 2 guarded Pi form
+  int last_eval_tma = -1;                             // the last evaluation's slice loads: 1 TMA, 0 cooperative
   bool last_eval_pi = false;                          // the last evaluation ran the guarded Pi form
   bool force_residual = false;                        // dGN loop: the guard fell back, stay residual
   bool eval_f_only = false;                           // the caller needs F only (guard ignores grad)              // compression: Grams, U, core intermediates
@@ -70,3 +75,6 @@ tf_status eval_f_only(tf_ctx* c, tf_dims d, const double* T, const double* w, do
     cudaError_t e_ = (expr);                                      \
     if (e_ != cudaSuccess) return tfh::cuda_err((c), e_, #expr);  \
   } while (0)
+
+// blocks of the persistent CG / matvec launch: every SM, or the test cap of tf_ctx_set_cg_grid
+inline int cg_grid(const tf_ctx* c) { return c->cg_grid > 0 && c->cg_grid < c->nsm ? c->cg_grid : c->nsm; }

@@ -81,8 +81,8 @@ struct CgState {
 cudaError_t launch_cg_persistent(const Modes& m, const double* pi, const double* dscale, const double* damp,
                                  double lambda, double tol,
                                  int maxiter, const double* rhs, const double* v, double* x, double* r, double* p,
-                                 double* z, double* G, double* S, double* part, CgState* st_dev, int mode, int nsm,
-                                 cudaStream_t st);
+                                 double* z, double* G, double* S, double* part, CgState* st_dev, int mode, int grid,
+                                 bool allow_small, cudaStream_t st);
 size_t cg_gram_partial_doubles(int64_t R);
 
 // dGN outer-loop helpers (k_small.cu)
@@ -90,9 +90,9 @@ cudaError_t launch_dots(int64_t n, const double* g, const double* x, const doubl
                         cudaStream_t st);   // out = {g.x, x.y, x.x, max|g|}; partial: red_blocks()*4
 cudaError_t launch_tsums(int64_t I, int64_t J, int64_t K, int64_t ldT, const double* T, double* partial, double* out,
                          cudaStream_t st);  // out = {sum|t|, sum t^2}; partial: red_blocks()*2
-cudaError_t launch_axpy_inplace(int64_t n, const double* x, double* w, cudaStream_t st);
+cudaError_t launch_axpy_inplace(int64_t n, const double* x, double* w, const CgState* gate, cudaStream_t st);
 cudaError_t launch_scale_copy(int64_t n, double alpha, const double* x, double* y, cudaStream_t st);
-cudaError_t launch_balance(const Modes& m, const double* grams, double* w, cudaStream_t st);
+cudaError_t launch_balance(const Modes& m, const double* grams, double* w, const CgState* gate, cudaStream_t st);
 int red_blocks();
 
 // y += x (n doubles), used by the host-streamed evaluation

@@ -56,6 +56,7 @@ class ShardedEvaluator:
             from types import SimpleNamespace
             self._Dims = lambda **kw: SimpleNamespace(**kw)
         self.eval_fn = eval_fn
+        self.ctx = ctx
         self.device = device
         self.buf = None
 
@@ -79,7 +80,14 @@ class ShardedEvaluator:
         else:
             self.eval_fn(self.local_dims, T_local, w, f, grad)
         if allreduce and self.world > 1:
-            dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group)
+            stream = getattr(self.ctx, "stream", None) if buf.is_cuda else None
+            if stream is not None:
+                # the evaluation was enqueued on the library's stream; NCCL orders after torch's current stream,
+                # so run the collective on the evaluation stream itself (no read of buf before the kernels end)
+                with torch.cuda.stream(stream):
+                    dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group)
+            else:
+                dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group)
         return f, grad
 
 

@@ -152,19 +152,24 @@ class Problem:
 
 
 def make_problem(name: str, device="cpu", seed: int = 0, k_range=None, slab: int = 16,
-                 dims=None) -> Problem:
+                 dims=None, noise_value=None) -> Problem:
     """Build the seeded workload `name` on `device`.
 
     k_range=(k0, k1) keeps only slices k0..k1-1 of T (K-sharding); everything
     that depends on all of T (SNR / σ_T scaling) is still computed from every
     slice, so a shard is bit-identical to the same slices of the full tensor.
-    dims=(I,J,K,R) overrides the shape (tests use the recipes at reduced size).
+    dims=(I,J,K,R) overrides the shape (tests use the recipes at reduced size); noise_value overrides the
+    recipe's noise level in its own unit (sigma, SNR in dB, or fraction of sigma_T) — the tests of the
+    cancellation guard (reading R31) use c3's recipe at other SNRs.
     """
     cfg = CONFIGS[name]
     if dims is not None:
         I, J, K, R = dims
         cfg = Config(cfg.name, I, J, K, R, cfg.factors, cfg.noise, cfg.noise_value, cfg.points,
                      cfg.lam, cfg.cg_iters, cfg.desc + f" (reduced to {I}x{J}x{K} R={R})")
+    if noise_value is not None:
+        cfg = Config(cfg.name, cfg.I, cfg.J, cfg.K, cfg.R, cfg.factors, cfg.noise, float(noise_value), cfg.points,
+                     cfg.lam, cfg.cg_iters, cfg.desc + f" (noise {cfg.noise} = {noise_value})")
     I, J, K, R = cfg.I, cfg.J, cfg.K, cfg.R
     k0, k1 = (0, K) if k_range is None else k_range
     dev = torch.device(device)

@@ -57,3 +57,50 @@ def to_np(x) -> np.ndarray:
     if isinstance(x, torch.Tensor):
         return x.detach().cpu().numpy().astype(np.float64)
     return np.asarray(x, dtype=np.float64)
+
+
+def w_blocks(I, J, K, R):
+    """(name, slice) of the three factor blocks of a packed w-layout vector [vec A | vec B | vec C]."""
+    return [("A", slice(0, I * R)), ("B", slice(I * R, (I + J) * R)), ("C", slice((I + J) * R, (I + J + K) * R))]
+
+
+def block_floors(w, I, J, K, R):
+    """Per-block forward-error floors u·‖W_ℓ Π^(ℓ)‖_F of an fp64 gradient (reading R14, split by block)."""
+    w = np.asarray(w, dtype=np.float64).reshape(-1)
+    A = w[:I * R].reshape(R, I).T
+    B = w[I * R:(I + J) * R].reshape(R, J).T
+    C = w[(I + J) * R:].reshape(R, K).T
+    gA, gB, gC = A.T @ A, B.T @ B, C.T @ C
+    return [U * np.linalg.norm(A @ (gB * gC)), U * np.linalg.norm(B @ (gA * gC)), U * np.linalg.norm(C @ (gA * gB))]
+
+
+def check_elementwise(got, ref, blocks, floors=None, tol: float = TOL):
+    """Per-block and per-element parity next to the whole-vector norm check.
+
+    For every block b (e.g. dF/dA, dF/dB, dF/dC):
+      ‖Δ_b‖₂ ≤ tol·‖ref_b‖₂ + κ·floor_b                                    (a small block cannot hide)
+      |Δ_e| ≤ tol·(|ref_e| + rms(ref_b)) + κ·floor_b   for every element e   (nor a single entry)
+    rms(ref_b) = ‖ref_b‖₂/√n_b is the block's own scale: an entry far below it (cancellation in its
+    contraction) is held to 1e-10 of the block scale, every other entry to 1e-10 of itself.
+    Returns a dict of the worst ratios err/bound (≤ 1 passes) per block; raises AssertionError on failure."""
+    got = np.asarray(got, dtype=np.float64).reshape(-1)
+    ref = np.asarray(ref, dtype=np.float64).reshape(-1)
+    out = {}
+    for bi, (name, sl) in enumerate(blocks):
+        g, r = got[sl], ref[sl]
+        if r.size == 0:
+            continue
+        fl = KAPPA * (floors[bi] if floors is not None else 0.0)
+        d = np.abs(g - r)
+        nb = float(np.linalg.norm(r))
+        blk_bound = tol * nb + fl
+        blk_err = float(np.linalg.norm(g - r))
+        rms = nb / math.sqrt(r.size)
+        el_bound = tol * (np.abs(r) + rms) + fl
+        el_ratio = d / np.where(el_bound > 0, el_bound, np.inf)
+        worst = int(np.argmax(el_ratio)) if el_ratio.size else 0
+        out[name] = {"block_err": blk_err / max(nb, 1e-300), "block_ratio": blk_err / blk_bound if blk_bound > 0 else
+                     (0.0 if blk_err == 0 else np.inf), "elem_ratio": float(el_ratio[worst]), "elem_index": worst}
+        assert blk_err <= blk_bound, (name, "block", blk_err, blk_bound)
+        assert np.all(d <= el_bound), (name, "element", worst, float(g[worst]), float(r[worst]), float(el_bound[worst]))
+    return out

@@ -107,6 +107,7 @@ def _padded_ld(ctx):
         Tp[:, :, I:] = 1e300   # padding must never be read
         Tt = torch.from_numpy(Tp.reshape(-1)).cuda()
         f, g = ctx.tf_cpd_eval(tf.Dims(I, J, K, R, ldT=ldT), Tt, torch.from_numpy(w).cuda())
+        assert ctx.eval_used_tma() == (1 if ldT % 2 == 0 else 0)   # the library reports the load path it ran
         assert rel_err([f.item()], [fr]) <= TOL
         assert rel_err(to_np(g), gr) <= TOL
 
@@ -278,10 +279,21 @@ def test_gn_matvec_against_plain_route(ctx):
     assert rel_err(to_np(y), oracle.gn_matvec_plain(w, v, 1e-3, c.I, c.J, c.K, c.R)) <= TOL
 
 
+@pytest.mark.parametrize("grid", [0, 5])
 @pytest.mark.parametrize("jacobi", [False, True])
 @pytest.mark.parametrize("case", ["c1", "c3r", "r120", "even30", "even31"])
-def test_cg_per_iteration(ctx, case, jacobi):
-    """Every CG iterate x^(i), i = 1..10, against Alg. CG-dGN in the oracle (rhs = -grad, lambda = 1e-3)."""
+def test_cg_per_iteration(ctx, case, jacobi, grid):
+    """Every CG iterate x^(i), i = 1..10, against Alg. CG-dGN in the oracle (rhs = -grad, lambda = 1e-3). grid = 5
+    runs the persistent grid kernel on 5 blocks (tf_ctx_set_cg_grid), so every block processes several Gram and
+    apply items, as on the full grid at c5."""
+    ctx.set_cg_grid(grid)
+    try:
+        _cg_per_iteration(ctx, case, jacobi)
+    finally:
+        ctx.set_cg_grid(0)
+
+
+def _cg_per_iteration(ctx, case, jacobi):
     if case == "c1":
         P = synth.make_problem("c1", "cpu")
         I, J, K, R = 20, 20, 20, 3
@@ -698,3 +710,52 @@ def test_cg_zero_rhs(ctx, dims):
         assert torch.count_nonzero(x).item() == 0
         ref = oracle.cg(to_np(w), np.zeros(n), 1e-3, 10, I, J, K, R, jacobi=jacobi)
         assert ref["iters"] == 0 and ref["status"] == 0
+
+
+@pytest.mark.parametrize("jacobi", [False, True])
+def test_dgn_cg_breakdown_leaves_w(ctx, jacobi):
+    """Stop reason 8 (non-finite CG alpha/beta): a NaN entry in T makes F, grad F and mu^(0) = mean|T| NaN, so
+    Alg. CG-dGN meets alpha = NaN at its first iteration. Like the oracle, the loop stops at w^(k-1): w is
+    returned bitwise unchanged (no step, no balancing), 0 iterations done, reason 8."""
+    I, J, K, R = 14, 11, 9, 3
+    T, w0 = _exact_plus_noise(I, J, K, R, 8, 1e-2)
+    T[17] = np.nan
+    cgi = synth.cg_budget(5, seed=2)
+    ref = oracle.dgn(T, w0, I, J, K, R, cgi, maxiter=5, tol=1e-6, jacobi=jacobi)
+    assert ref["reason"] == 8 and ref["iters"] == 0 and np.array_equal(ref["w"], w0)
+    wt = torch.from_numpy(w0.copy()).cuda()
+    out, _ = ctx.tf_cpd_dgn(tf.Dims(I, J, K, R), torch.from_numpy(T).cuda(), wt, cgi, maxiter=5, tol=1e-6,
+                            jacobi=jacobi)
+    assert out["reason"] == 8 and out["iters"] == 0, out
+    assert np.array_equal(to_np(wt), w0)
+
+
+@pytest.mark.parametrize("case", ["step", "gradient", "divergence"])
+def test_dgn_stop_conditions_match_oracle(ctx, case):
+    """The dGN loop on the device stops with the same condition at the same iteration as the oracle in the
+    constructed runs of tests/test_oracle_pins.py::test_dgn_stops_in_runs (conditions 2, 4 and 7 at k = 1;
+    PAPER.md:2756-2773), and returns the same w."""
+    I, J, K, R = 5, 4, 3, 2
+    rng = np.random.default_rng(31)
+    A, B, C = (rng.standard_normal((n, R)) for n in (I, J, K))
+    t = np.einsum("ir,jr,kr->ijk", A, B, C) + 0.1 * rng.standard_normal((I, J, K))
+    T = np.ascontiguousarray(t.transpose(2, 1, 0)).reshape(-1)
+    nT = float(np.linalg.norm(T))
+    cgi = np.full(5, 4, dtype=np.int32)
+    kw = {}
+    if case == "step":
+        w0, tol, kw = np.zeros(R * (I + J + K)), 1e-8, {"use_gamma": False, "jacobi": False}
+        want = 2
+    elif case == "gradient":
+        s = 1e-9
+        T = T * s
+        w0, tol, want = rng.standard_normal(R * (I + J + K)) * s ** (1 / 3), 1e-4, 4
+    else:
+        T = T / (2 * nT)
+        w0, tol, want = 30.0 * rng.standard_normal(R * (I + J + K)), 1.0, 7
+    ref = oracle.dgn(T, w0, I, J, K, R, cgi, maxiter=5, tol=tol, **kw)
+    assert ref["reason"] == want and ref["iters"] == 1
+    wt = torch.from_numpy(w0.copy()).cuda()
+    out, _ = ctx.tf_cpd_dgn(tf.Dims(I, J, K, R), torch.from_numpy(T).cuda(), wt, cgi, maxiter=5, tol=tol, **kw)
+    assert out["reason"] == want and out["iters"] == 1, out
+    assert rel_err(to_np(wt), ref["w"]) <= 1e-9

@@ -250,3 +250,40 @@ def test_st_mlsvd_error_identity_and_special_cases(golden_dir):
     cw = M.mlsvd(Tw, 6, 5, 4, 3)
     assert sw["ranks"] == (3, 3, 3)
     assert np.allclose(np.abs(sw["S"]), np.abs(cw["S"]), atol=1e-10)
+
+
+
+@pytest.mark.parametrize("mlsvd_tol,ranks", [(3e-2, (3, 3, 3)), (6e-2, (2, 2, 2)), (1e-3, (4, 4, 3))])
+def test_st_mlsvd_per_step_threshold(mlsvd_tol, ranks):
+    """Alg. ST-MLSVD's per-step truncation (PAPER.md:1430-1439 with Alg. Compression's rule, 2566-2583, reading
+    R32): each step keeps the smallest i with tail/total < mlsvd_tol / L, L = 3, of THAT step's singular values.
+    The tensor is (Q1, Q2, Q3)·S for random orthogonal Q_l and a core of four rank-one terms s_t e_a⊗e_b⊗e_c,
+    (a,b,c; s²) = (0,0,0; 1), (1,1,1; 0.6), (2,2,2; 0.02), (3,3,1; 0.005), whose mode-l unfolding rows share no
+    columns: the mode-l singular values are exactly the square roots of the row sums of s², so the ranks are
+    derived by hand (P_l = min(5, R = 5) = 5):
+      mode 1: σ² = 1, 0.6, 0.02, 0.005, 0 (total 1.625); tail after i = 2: 0.025/1.625 = 0.01538, after i = 3:
+              0.005/1.625 = 0.003077, after i = 4: 0.
+      tol 3e-2 -> threshold 1e-2 -> R~1 = 3; step 1 drops term 4, so step 2 sees σ² = 1, 0.6, 0.02 (tail after
+              2: 0.02/1.62 = 0.0123 >= 1e-2) -> 3, step 3 the same -> (3, 3, 3).
+      tol 6e-2 -> threshold 2e-2 -> R~1 = 2; steps 2 and 3 see 1, 0.6 (tail after 1: 0.375) -> (2, 2, 2).
+      tol 1e-3 -> threshold 3.33e-4 -> R~1 = 4 (tail after 3 = 0.003077); step 2 sees 1, 0.6, 0.02, 0.005 -> 4;
+              step 3's rows are 1, 0.605 (terms 2 and 4 share c = 1), 0.02 -> tail after 2 = 0.0123, after 3 = 0
+              -> 3: (4, 4, 3).
+    A threshold of mlsvd_tol (no 1/L) or 3·mlsvd_tol gives R~1 = 2 in the first case; mlsvd_tol / 9 gives 4 in
+    the second. The truncation error equals the dropped energy (ST-HOSVD identity), below mlsvd_tol."""
+    n, R = 5, 5
+    terms = [((0, 0, 0), 1.0), ((1, 1, 1), 0.6), ((2, 2, 2), 0.02), ((3, 3, 1), 0.005)]
+    S = np.zeros((n, n, n))
+    for (a, b, c), s2 in terms:
+        S[a, b, c] = math.sqrt(s2)
+    rng = np.random.default_rng(17)
+    Q = [np.linalg.qr(rng.standard_normal((n, n)))[0] for _ in range(3)]
+    t = np.einsum("ia,jb,kc,abc->ijk", Q[0], Q[1], Q[2], S)
+    st = M.st_mlsvd(jac.storage_from_tensor(t), n, n, n, R, mlsvd_tol)
+    assert st["ranks"] == ranks
+    # step 1's singular values are the hand-derived ones
+    assert np.allclose(st["sigma"][0] ** 2, [1.0, 0.6, 0.02, 0.005, 0.0], atol=1e-14)
+    rec = np.einsum("ia,jb,kc,abc->ijk", *st["U"], st["S"])
+    dropped = {(3, 3, 3): 0.005, (2, 2, 2): 0.025, (4, 4, 3): 0.0}[ranks]
+    assert abs(np.linalg.norm(t - rec) ** 2 - dropped) <= 1e-13
+    assert dropped / 1.625 < mlsvd_tol

@@ -549,3 +549,170 @@ def test_dgn_damping_rule_and_balancing():
     na, nb_, nc = (np.linalg.norm(M, axis=0) for M in (A, B, C))
     np.testing.assert_allclose(na, nb_, rtol=1e-13)
     np.testing.assert_allclose(na, nc, rtol=1e-13)
+
+
+# --------------------------------------------------------------------------- gamma: the per-mode pairing
+def _tight_factors(norms, I, J, K, seed):
+    """Columns nearly parallel to e_0 (1e-3 perturbation) with prescribed norms norms[l][r]: every Cauchy-Schwarz
+    bound behind gamma is then attained to 1e-3, so the dominance rows are tight."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for l, n in enumerate((I, J, K)):
+        cols = []
+        for r in range(len(norms[l])):
+            v = np.zeros(n)
+            v[0] = 1.0
+            v += 1e-3 * rng.standard_normal(n)
+            cols.append(norms[l][r] * v / np.linalg.norm(v))
+        out.append(np.stack(cols, axis=1))
+    return out
+
+
+def _dominant(H, d):
+    off = np.abs(H - np.diag(np.diag(H))).max(axis=1)
+    return bool(np.all(np.diag(H) + d >= off * (1 - 1e-12)))
+
+
+def test_reg_gamma_pairing_is_the_one_that_dominates():
+    """gamma_X^(r) = ||Y_r|| ||Z_r|| M, gamma_Y^(r) = ||X_r|| ||Z_r|| M, gamma_Z^(r) = ||X_r|| ||Y_r|| M with
+    M = max over r' of all three products. On factors whose columns are nearly parallel
+    (the off-diagonal entries of J^T J attain their Cauchy-Schwarz bounds) with column r of mode r much
+    shorter than the rest, every row of J^T J + D dominates each of its off-diagonal entries with the oracle's
+    gamma. The test also shows it discriminates: every other pairing of the three products to the modes, and
+    M taken over a single product, break dominance on at least one of the three cyclic variants."""
+    import itertools
+    I, J, K, R = 3, 4, 3, 3
+    base = np.array([[0.05, 2.0, 3.0], [1.5, 0.04, 2.5], [2.2, 1.7, 0.06]])
+    configs = [np.roll(base, s, axis=0) for s in range(3)]   # which product attains M rotates too
+    wrong_pairings = set(p for p in itertools.permutations(("YZ", "XZ", "XY")) if p != ("YZ", "XZ", "XY"))
+    broken_pairings, broken_partial_max = set(), set()
+    for ci, nm in enumerate(configs):
+        X, Y, Z = _tight_factors(nm, I, J, K, seed=ci)
+        w = w_of(X, Y, Z)
+        Jm = jac.jacobian_entrywise(w, I, J, K, R)
+        H = Jm.T @ Jm
+        gam = oracle.reg_gamma(w, I, J, K, R)
+        assert _dominant(H, _expand_damp(gam, I, J, K, R)), ci
+        # negative controls (mutations of the rule, written here only to show the pin discriminates)
+        nx, ny, nz = (np.linalg.norm(F, axis=0) for F in (X, Y, Z))
+        prods = {"YZ": ny * nz, "XZ": nx * nz, "XY": nx * ny}
+        Mx = max(p.max() for p in prods.values())
+        for perm in wrong_pairings:
+            if not _dominant(H, _expand_damp(np.concatenate([prods[p] * Mx for p in perm]), I, J, K, R)):
+                broken_pairings.add(perm)
+        for key in prods:
+            g1 = np.concatenate([prods[p] * prods[key].max() for p in ("YZ", "XZ", "XY")])
+            if not _dominant(H, _expand_damp(g1, I, J, K, R)):
+                broken_partial_max.add(key)
+    assert broken_pairings == wrong_pairings
+    assert broken_partial_max == {"YZ", "XZ", "XY"}
+
+
+# --------------------------------------------------------------------------- dGN: stopping rule and gain ratio
+def test_dgn_stop_rule_constructed_histories():
+    """The stopping conditions of PAPER.md:2756-2773 on constructed histories, each made to hold while every
+    earlier condition fails (readings R20, R21): the rule returns that condition, and moving the history just
+    across its threshold (10% either side) turns it off. maxiter = 15 -> c = 1 + ceil(15/10) = 3, so 5 and 6
+    are checked at k = 9, 12, ... (k > 2c, k = 0 mod c) over the windows [k-6, k-3) and [k-3, k)."""
+    S = oracle.dgn_stop
+    tol, nT2, mx = 1e-4, 4.0, 15
+    big = 1.0
+    lo, hi = 0.9 * tol, 1.1 * tol
+    # 1: relative error below tol
+    assert S(1, [0.5, lo], mx, tol, big, big, nT2) == 1
+    assert S(1, [0.5, hi], mx, tol, big, big, nT2) == 0
+    # 2: step below tol (the error did not change either: 2 is checked before 3)
+    assert S(1, [0.5, 0.5], mx, tol, lo, big, nT2) == 2
+    assert S(1, [0.5, 0.3], mx, tol, hi, big, nT2) == 0
+    # 3: improvement of the relative error below tol
+    assert S(1, [0.5, 0.5 - lo], mx, tol, big, big, nT2) == 3
+    assert S(1, [0.5, 0.5 - hi], mx, tol, big, big, nT2) == 0
+    # 4: infinity norm of the gradient below tol
+    assert S(1, [0.5, 0.3], mx, tol, big, lo, nT2) == 4
+    assert S(1, [0.5, 0.3], mx, tol, big, hi, nT2) == 0
+    # 5: mean of rel over [3, 6) minus mean over [6, 9) below tol (oscillation without decrease), at k = 9:
+    #    rel[3..5] = 0.6, 0.7, 0.6 and rel[6..8] = 0.7, 0.6, 0.6 + 3 lo: m1 - m2 = -lo < tol; rel[9] = 0.65
+    rel5 = [1.0, 0.9, 0.8, 0.6, 0.7, 0.6, 0.7, 0.6, 0.6 + 3 * lo, 0.65]
+    assert S(9, rel5, mx, tol, big, big, nT2) == 5
+    assert S(8, rel5, mx, tol, big, big, nT2) == 0            # only checked at k = 0 mod c
+    assert S(6, rel5[:7], mx, tol, big, big, nT2) == 0        # ... and k > 2c
+    rel5b = list(rel5)
+    rel5b[8] = 0.6 - 3 * hi                                   # m1 - m2 = 1.1 tol
+    assert S(9, rel5b, mx, tol, big, big, nT2) == 0
+    # 6: mean improvement over [6, 9) below 1e-3 of the mean error (decreasing, so 5 fails): steps of d with
+    #    3 d = ... rel[6..9] = 0.5, 0.5 - d, 0.5 - 2d, 0.5 - 3d; imp = d vs 1e-3 m2 = 1e-3 (0.5 - d)
+    def rel6(d):
+        return [1.0, 0.9, 0.8, 0.7, 0.6, 0.55, 0.5, 0.5 - d, 0.5 - 2 * d, 0.5 - 3 * d]
+    thr = 1e-3 * 0.5 / (1 + 1e-3)                           # d = 1e-3 (0.5 - d)
+    assert S(9, rel6(0.9 * thr), mx, tol, big, big, nT2) == 6
+    assert S(9, rel6(1.1 * thr), mx, tol, big, big, nT2) == 0
+    # 7: divergence: rel > max(1, ||T||^2) / (1e-16 + tol) = 4 / 1e-4 = 4e4
+    assert S(1, [3e4, 1.1 * 4e4], mx, tol, big, big, nT2) == 7
+    assert S(1, [3e4, 0.9 * 4e4], mx, tol, big, big, nT2) == 0
+    assert S(1, [0.5, 2.2], mx, 0.5, big, big, 0.25) == 7      # max(1, ||T||^2) = 1: threshold 1 / 0.5 = 2
+    assert S(1, [0.5, 1.8], mx, 0.5, big, big, 0.25) == 0
+
+
+def _small_problem(I, J, K, R, seed, sigma, scale=1.0):
+    rng = np.random.default_rng(seed)
+    A, B, C = (rng.standard_normal((n, R)) for n in (I, J, K))
+    t = scale * (build_T(A, B, C) + sigma * rng.standard_normal((I, J, K)))
+    return dense_T(t), rng
+
+
+def test_dgn_stops_in_runs():
+    """Runs of the oracle's dGN loop that must stop with a given condition at k = 1:
+    * 2 (step): w0 = 0 is a stationary point (every MTTKRP and W Pi vanish), so -grad F = 0 and CG returns x = 0
+      (reading R33): ||x|| = 0 < tol while the relative error is 1 (3 holds too, but 2 comes first).
+    * 4 (gradient): T and w0 scaled by s and s^(1/3) (s = 1e-9): the relative error and its first improvement
+      are scale-free (large), the step scales as s^(1/3) = 1e-3 > tol, the gradient as s^(5/3) < tol.
+    * 7 (divergence): ||T|| < 1 and w0 huge: after one Gauss-Newton step the model is still far worse than
+      0, rel > 1 / (1e-16 + tol) with tol = 1 (and the step, improvement and gradient are all > 1).
+    Each is checked on the oracle's own history and on the final w with the pinned evaluation."""
+    I, J, K, R = 5, 4, 3, 2
+    T, rng = _small_problem(I, J, K, R, 31, 0.1)
+    nT = float(np.linalg.norm(T))
+    cgi = np.full(5, 4, dtype=np.int32)
+    # 2
+    out = oracle.dgn(T, np.zeros(R * (I + J + K)), I, J, K, R, cgi, maxiter=5, tol=1e-8, use_gamma=False,
+                     jacobi=False)
+    assert out["reason"] == 2 and out["iters"] == 1, out
+    assert out["hist"][0, 4] == 0.0 and abs(out["hist"][0, 1] - 1.0) < 1e-15
+    # 4
+    s = 1e-9
+    Ts = T * s
+    w0 = rng.standard_normal(R * (I + J + K)) * s ** (1 / 3)
+    out = oracle.dgn(Ts, w0, I, J, K, R, cgi, maxiter=5, tol=1e-4)
+    assert out["reason"] == 4 and out["iters"] == 1, out
+    f0, _ = oracle.cpd_eval(Ts, w0, I, J, K, R)
+    f1, g1 = oracle.cpd_eval(Ts, out["w"], I, J, K, R)
+    rel0, rel1 = math.sqrt(2 * f0) / (nT * s), math.sqrt(2 * f1) / (nT * s)
+    assert rel1 >= 1e-4 and abs(rel0 - rel1) >= 1e-4 and out["hist"][0, 4] >= 1e-4
+    assert np.abs(g1).max() < 1e-4
+    # 7
+    Tt = T / (2 * nT)                       # ||T|| = 1/2
+    w0 = 30.0 * rng.standard_normal(R * (I + J + K))
+    out = oracle.dgn(Tt, w0, I, J, K, R, cgi, maxiter=5, tol=1.0)
+    assert out["reason"] == 7 and out["iters"] == 1, out
+    f1, g1 = oracle.cpd_eval(Tt, out["w"], I, J, K, R)
+    assert math.sqrt(2 * f1) / 0.5 > 1.0 and np.abs(g1).max() >= 1.0 and out["hist"][0, 4] >= 1.0
+
+
+def test_dgn_gain_ratio_against_explicit_jacobian():
+    """The gain ratio of one dGN step (reading R19): g = (F(w0) - F(w1)) /
+    (F(w0) - 1/2 ||f(w0) + J_f(w0) x||^2) with x = w1 - w0 (no balancing), recomputed with the explicit
+    Jacobian of Lemma partialf and the pinned evaluation, equals the oracle's recorded g."""
+    I, J, K, R = 4, 3, 3, 2
+    T, rng = _small_problem(I, J, K, R, 41, 0.3)
+    w0 = rng.standard_normal(R * (I + J + K))
+    for jacobi in (False, True):
+        out = oracle.dgn(T, w0, I, J, K, R, np.array([3], dtype=np.int32), maxiter=1, tol=0.0, balance=False,
+                         jacobi=jacobi)
+        x = out["w"] - w0
+        f0, _ = oracle.cpd_eval(T, w0, I, J, K, R)
+        f1, _ = oracle.cpd_eval(T, out["w"], I, J, K, R)
+        Jm = jac.jacobian_entrywise(w0, I, J, K, R)
+        r0 = jac.residual(T, w0, I, J, K, R)
+        g = (f0 - f1) / (f0 - 0.5 * np.sum((r0 + Jm @ x) ** 2))
+        assert abs(out["hist"][0, 3] - g) <= 1e-10 * abs(g), (out["hist"][0, 3], g)
+        assert abs(out["hist"][0, 0] - f1) <= 1e-14 * f1
