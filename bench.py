@@ -107,12 +107,27 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU oracle timing
-def oracle_sample(cfg, P_T_slices, w_np, k_slices, cg_iters_sample, threads):
-    """Time the oracle (as it stands) on a bounded sample of the workload and scale to one full step.
+def host_cpu():
+    """The host CPU model and core count (lscpu), recorded beside every oracle timing."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"model": model, "nproc": os.cpu_count()}
 
-    Sample: F + grad over the first `k_slices` frontal slices (oracle_eval, OpenMP over slices), plus
-    `cg_iters_sample` CG iterations of Alg. CG-dGN (Thm Hv matvecs). Scaled: eval time * K/k_slices +
-    CG time * cg_iters/cg_iters_sample.
+
+def oracle_shard_sample(cfg, T_shard, w_np, k_s, threads):
+    """Time the oracle (as it stands, never tuned) on one K-shard of the workload plus the step's whole CG.
+
+    The sample is a real unit of the method's sharded form: F + grad over the contiguous shard of
+    the first k_s frontal slices (oracle_eval, OpenMP over slices; the evaluation is a sum over slices, so a
+    shard costs exactly k_s/K of the evaluation), then ALL cfg.cg_iters iterations of Alg. CG-dGN with Thm-Hv
+    matvecs on the full parameter vector (not scaled). Returns (evals/s of one full step on this host, seconds
+    actually spent, description): evals/s = 1 / (t_shard * K / k_s + t_cg).
     """
     import numpy as np
 
@@ -120,27 +135,29 @@ def oracle_sample(cfg, P_T_slices, w_np, k_slices, cg_iters_sample, threads):
     I, J, K, R = cfg.I, cfg.J, cfg.K, cfg.R
     A = w_np[:I * R]
     B = w_np[I * R:(I + J) * R]
-    C = w_np[(I + J) * R:].reshape(R, K)[:, :k_slices].reshape(-1)
+    C = w_np[(I + J) * R:].reshape(R, K)[:, :k_s].reshape(-1)
     ws = np.concatenate([A, B, C])
     t0 = time.perf_counter()
-    f, g = oracle.cpd_eval(P_T_slices, ws, I, J, k_slices, R, nthreads=threads)
+    f, g = oracle.cpd_eval(T_shard, ws, I, J, k_s, R, nthreads=threads)
     t_eval = time.perf_counter() - t0
     t_cg = 0.0
-    if cfg.cg_iters and cg_iters_sample:
+    if cfg.cg_iters:
         rhs = -np.concatenate([g[:(I + J) * R], np.zeros(K * R)])
+        rhs[(I + J) * R:] = -np.pad(g[(I + J) * R:].reshape(R, k_s), ((0, 0), (0, K - k_s))).reshape(-1)
         t0 = time.perf_counter()
-        oracle.cg(w_np, rhs, cfg.lam, cg_iters_sample, I, J, K, R)
+        oracle.cg(w_np, rhs, cfg.lam, cfg.cg_iters, I, J, K, R)
         t_cg = time.perf_counter() - t0
-    step_s = t_eval * K / k_slices + (t_cg * cfg.cg_iters / cg_iters_sample if cg_iters_sample else 0.0)
-    sample = (f"oracle_eval on {k_slices}/{K} frontal slices ({t_eval:.2f} s, {threads} OpenMP threads, "
-              f"80-bit accumulation) scaled x{K / k_slices:.1f}")
-    if cfg.cg_iters and cg_iters_sample:
-        sample += f" + {cg_iters_sample}/{cfg.cg_iters} CG iterations ({t_cg:.2f} s) scaled"
-    return 1.0 / step_s, sample, t_eval + t_cg
+    step_s = t_eval * K / k_s + t_cg
+    sample = (f"oracle_eval on the K-shard of frontal slices 0..{k_s - 1} of {K} ({t_eval:.2f} s, {threads} OpenMP "
+              f"threads, 80-bit accumulation; the evaluation is a sum over slices, so one shard is {k_s}/{K} of it)")
+    if cfg.cg_iters:
+        sample += f" + all {cfg.cg_iters} CG iterations on the full vector ({t_cg:.2f} s, one thread)"
+    sample += f"; one step = {t_eval:.2f} s x {K}/{k_s} + {t_cg:.2f} s"
+    return 1.0 / step_s, t_eval + t_cg, sample
 
 
 def pick_k_slices(cfg, T_first_slice, w_np, budget_s=12.0, threads=16):
-    """Slices so that the eval sample is ~budget_s of CPU work: time one slice, then scale."""
+    """Shard size (frontal slices) for ~budget_s of CPU work: time one slice on one thread, then scale."""
     import numpy as np
 
     import oracle
@@ -150,7 +167,7 @@ def pick_k_slices(cfg, T_first_slice, w_np, budget_s=12.0, threads=16):
     t0 = time.perf_counter()
     oracle.cpd_eval(T_first_slice, ws, I, J, 1, R, nthreads=1)
     t1 = time.perf_counter() - t0          # one slice on one thread
-    per_slice = t1 / max(1, min(threads, 16))
+    per_slice = t1 / max(1, threads)
     return int(max(1, min(cfg.K, budget_s / max(per_slice, 1e-9))))
 
 
@@ -163,32 +180,123 @@ def run_reference(args):
     cfg = synth.CONFIGS[args.config]
     threads = os.cpu_count() or 1
     P1 = synth.make_problem(args.config, "cpu", k_range=(0, 1))
-    k_sl = pick_k_slices(cfg, P1.T.numpy().reshape(-1), P1.w(cfg.points[-1]).numpy(), 8.0, threads)
+    k_sl = pick_k_slices(cfg, P1.T.numpy().reshape(-1), P1.w(cfg.points[-1]).numpy(), 6.0, threads)
     P = synth.make_problem(args.config, "cpu", k_range=(0, k_sl))
     w = P.w(cfg.points[-1]).numpy()
     T = P.T.numpy().reshape(-1)
-    cg_s = 1 if cfg.cg_iters else 0
-    for _ in range(max(0, args.warmup)):
-        pass  # the oracle has no warm-up state; a warm-up pass would only double the CPU time
-    vals, secs = [], 0.0
+    # the oracle has no warm-up state: the W warm-up steps would only repeat the CPU work, so none are run
+    vals, secs, sample = [], [], ""
+    t_run = time.perf_counter()
     for _ in range(max(1, args.steps)):
-        v, sample, s = oracle_sample(cfg, T, w, k_sl, cg_s, threads)
+        v, s, sample = oracle_shard_sample(cfg, T, w, k_sl, threads)
         vals.append(v)
-        secs += s
+        secs.append(s)
+    t_run = time.perf_counter() - t_run
     value = statistics.median(vals)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True,
+        "steps": len(vals), "warmup": 0, "ms_per_step": 1000.0 * statistics.median(secs), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64 (80-bit long double accumulation)",
         "data": "synthetic (seeded, BASELINE.json recipe)",
         "config": {"workload": f"{cfg.name}: {cfg.desc}", "I": cfg.I, "J": cfg.J, "K": cfg.K, "R": cfg.R,
                    "cg_iters": cfg.cg_iters, "lambda": cfg.lam},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample,
+                         "host": host_cpu()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": "the reference arm of this tier is the CPU oracle timed on the box's host cores on a bounded "
-                "sample of the workload, scaled to one full step",
+        "wall_s": t_run,
+        "note": ("the reference arm of this tier is the CPU oracle on the box's host cores. Each step is one "
+                 "bounded sample (a K-shard evaluation + the whole CG); ms_per_step is the wall time a sample "
+                 "step actually took, value the evals/s of one full step that the sample implies"),
     }
     print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- multi-rank control path
+def init_ranks(backend: str, cuda: bool):
+    """One process per GPU (torchrun env: RANK / LOCAL_RANK / WORLD_SIZE / MASTER_*): the process group and
+    this rank's device. NCCL's communicator set-up lines (nranks, NVLS / P2P over NVLink) go to stderr."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if cuda and backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
+    if world > 1:
+        if cuda:
+            torch.cuda.set_device(local)
+        if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    return world, rank, local
+
+
+def max_over_ranks(x: float, dev, world: int) -> float:
+    """The timed-region length as the max over ranks (a MAX all-reduce), the value every rank reports."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def run_mock(args):
+    """TEST-ONLY check of the multi-rank control path on CPU (gloo; tests/test_dist_gloo.py runs it under
+    torchrun with 2 ranks): the same rank set-up, K-sharding (shard_range), ShardedEvaluator with its single SUM
+    all-reduce of [grad | f], barriers, timed loop and max-over-ranks reduction as the CUDA arm, with a stand-in
+    evaluator that is NOT the method (f_local = sum of the local slices, dF/dC row k = sum of slice k, dF/dA =
+    dF/dB = 0) so that the all-reduced result is checkable exactly. It measures nothing; its JSON line says
+    "mock": true and carries no throughput."""
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2110_05997_b200.dist import ShardedEvaluator, shard_range
+
+    world, rank, _ = init_ranks("gloo", cuda=False)
+    cfg = synth.CONFIGS[args.config]
+    I, J, K, R = cfg.I, cfg.J, cfg.K, cfg.R
+    k0, k1 = shard_range(K, rank, world)
+    P = synth.make_problem(args.config, "cpu", k_range=(k0, k1))
+
+    def stand_in(d, T, w, f, g, grams=None):
+        g.zero_()
+        f.fill_(float(T.sum()))
+        gC = g[(d.I + d.J) * d.R:].view(d.R, d.K_total)
+        gC[:, d.k_begin:d.k_begin + d.K] = T.reshape(d.K, -1).sum(dim=1)[None, :]
+
+    ev = ShardedEvaluator(I, J, K, R, rank=rank, world=world, eval_fn=stand_in)
+    assert (ev.k0, ev.k1) == (k0, k1)
+    w = P.w(cfg.points[-1])
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        ev(P.T, w)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        f, g = ev(P.T, w)
+    barrier()
+    sec = max_over_ranks(time.perf_counter() - t0, "cpu", world)
+    if rank == 0:
+        gC = g[(I + J) * R:].view(R, K)[0]
+        print(json.dumps({"mock": True, "impl": "ours-mock", "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "max_rank_seconds": sec, "value": None,
+                          "config": {"workload": f"{cfg.name}: {cfg.desc}",
+                                     "parallelism": f"K-sharded x{world} + 1 GLOO all-reduce of [grad|f]"},
+                          "check": {"f": float(f.item()), "gC_row0": gC.tolist(),
+                                    "shards": [list(shard_range(K, r, world)) for r in range(world)]}}),
+              flush=True)
+    if world > 1:
+        dist.destroy_process_group()
     return 0
 
 
@@ -202,21 +310,11 @@ def run_ours(args):
     import synth
     from paper_2110_05997_b200.dist import ShardedEvaluator, shard_range
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
     # TF_BENCH_BACKEND=gloo (development only): a functional check of the multi-rank path on a box with fewer
     # GPUs than ranks (ranks share a device; the all-reduce goes through the host, so no kernel waits on another
     # rank). Numbers from such a run are not scaling measurements.
     backend = os.environ.get("TF_BENCH_BACKEND", "nccl")
-    if backend != "nccl":
-        local = local % max(1, torch.cuda.device_count())
-    if world > 1:
-        torch.cuda.set_device(local)
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
+    world, rank, local = init_ranks(backend, cuda=True)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     cfg = synth.CONFIGS[args.config]
@@ -272,10 +370,7 @@ def run_ours(args):
     ms_local = e0.elapsed_time(e1)
     eval_ms, eval_n, launches = ctx.kernel_stats(reset=True)
     ctx.set_timing(False)
-    t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_total = float(t.item())
+    ms_total = max_over_ranks(ms_local, dev, world)
     ms_per_step = ms_total / args.steps
     value = 1000.0 / ms_per_step          # whole-job evaluations of the full problem per second
 
@@ -289,10 +384,19 @@ def run_ours(args):
     flops = nctr * I * J * (k1 - k0) * R
     peak_tf, peak_bw = fp64_peak()
     achieved_tf = flops / (kernel_ms * 1e-3) / 1e12
-    prof = load_json(os.path.join(ROOT, "profiles", f"ncu_eval_{cfg.name}_r01.json"), {}) or {}
+    prof, prof_src = {}, None
+    for tag in ("r02", "r01"):
+        src = os.path.join("profiles", f"ncu_eval_{cfg.name}_{tag}.json")
+        prof = load_json(os.path.join(ROOT, src), {}) or {}
+        if prof.get("dram_bytes_per_launch"):
+            prof_src = src
+            break
     traffic = prof.get("dram_bytes_per_launch") if world == 1 else None
     roofline = {"bound": "tensor", "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": achieved_tf / peak_tf, "traffic": traffic,
+                "traffic_source": (f"{prof_src}: dram__bytes_read.sum + dram__bytes_write.sum of one launch from a "
+                                   "stored ncu --set full capture of this kernel at this config (not measured in "
+                                   "this run)") if traffic else None,
                 "kernel": "k_eval_fused", "kernel_ms": kernel_ms, "eval_form": form,
                 "algorithmic": (f"{int(nctr)}*I*J*K_local*R = {flops:.4e} flop per evaluation "
                                 + ("(Pi form: T_k B and T_k^T A diag(c_k) per slice, PAPER.md:2641; kernel_ms spans "
@@ -337,10 +441,7 @@ def run_ours(args):
             step_e2e()
         barrier()
         sec = time.perf_counter() - t0
-        st = torch.tensor([sec], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(st, op=dist.ReduceOp.MAX)
-        sec = float(st.item())
+        sec = max_over_ranks(sec, dev, world)
         h2d = int(T_host.numel() * 8 + 2 * n * 8 + (n + 1) * 8)
         d2h = int((n + 1) * 8 + n * 8)
         e2e = {"value": e2e_steps / sec, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -354,14 +455,9 @@ def run_ours(args):
         wn = w.cpu().numpy()
         k_sl = pick_k_slices(cfg, P.T[:1].cpu().numpy().reshape(-1), wn, 12.0, threads)
         Ts = P.T[:k_sl].cpu().numpy().reshape(-1)
-        v, sample, _ = oracle_sample(cfg, Ts, wn, k_sl, 1 if cfg.cg_iters else 0, threads)
-        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample}
-        # the same oracle on one host thread (BASELINE.md §4 asks for both), on a smaller slice sample
-        k1 = max(1, k_sl // max(1, threads))
-        v1, sample1, _ = oracle_sample(cfg, P.T[:k1].cpu().numpy().reshape(-1), wn, k1, 0, 1)
-        cpu["single_thread"] = {"value": v1, "unit": UNIT, "cores": 1,
-                                "sample": sample1 + " (evaluation only; the CG share is as in the multi-thread "
-                                                    "sample, negligible)"}
+        v, secs, sample = oracle_shard_sample(cfg, Ts, wn, k_sl, threads)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample, "seconds": secs,
+               "host": host_cpu()}
 
     # compression stage (NEXT #3), measured once beside the step on the resident T (not part of `value`)
     stages = None
@@ -479,7 +575,9 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json recipe; no dataset)",
             "config": {"workload": f"{cfg.name}: {cfg.desc}", "I": I, "J": J, "K": K, "R": R,
                        "cg_iters": cfg.cg_iters, "lambda": cfg.lam, "point": point,
-                       "parallelism": f"K-sharded x{world} + 1 NCCL all-reduce of [grad|f]" if world > 1 else "1 GPU",
+                       "parallelism": (f"K-sharded x{world} + 1 {backend.upper()} all-reduce of [grad|f]"
+                                       + ("" if backend == "nccl" else " (development switch: ranks share a GPU; "
+                                          "not a scaling measurement)")) if world > 1 else "1 GPU",
                        "l2": f"inputs larger than L2 (T = {cfg.t_bytes / 1e9:.2f} GB > 126 MB), no flush",
                        "step": "tf_cpd_eval (F, grad, Grams) + tf_cg_solve(cg_iters)" if world == 1 else
                                "tf_cpd_eval (local, + Grams of the full factors) + all_reduce([grad|f]) + tf_cg_solve(cg_iters)"},
@@ -504,9 +602,13 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-stages", action="store_true", help="skip the compression-stage measurement")
+    ap.add_argument("--mock", action="store_true",
+                    help="TEST ONLY: the multi-rank control path on CPU (gloo) with a stand-in evaluator; no numbers")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    if args.mock:
+        return run_mock(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -7,7 +7,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtf.so")
-SOURCES = ["tf_api.cu", "tf_mlsvd.cu", "k_eval.cu", "k_small.cu", "k_cg.cu", "k_gemm.cu", "k_eig.cu", "tf_als.cu", "k_als.cu"]
+SOURCES = ["tf_api.cu", "tf_mlsvd.cu", "k_eval.cu", "k_small.cu", "k_cg.cu", "k_cg_rows.cu", "k_gemm.cu", "k_eig.cu", "tf_als.cu", "k_als.cu"]
 HEADERS = ["tf_internal.h", "tf_device.cuh", "tf_ctx.h", os.path.join("..", "..", "include", "tf.h")]
 NVCC_FLAGS = ["-shared", "-Xcompiler", "-fPIC", "-gencode", "arch=compute_100a,code=sm_100a", "-O3",
               "-lineinfo", "-std=c++17"]

@@ -755,6 +755,12 @@ cudaError_t launch_cg_persistent(const Modes& m, const double* pi, const double*
     k_cg_small<<<1, kCgSmallThreads, small_smem, st>>>(a);
     return cudaGetLastError();
   }
+  // the row-owned kernel (k_cg_rows.cu) whenever every block's rows, vectors and operand ring fit in shared
+  // memory; TF_CG_KERNEL=grid selects this kernel instead (development comparisons)
+  const char* kenv = getenv("TF_CG_KERNEL");   // read per call: the parity tests switch it
+  const bool force_grid = kenv && kenv[0] == 'g';
+  if (!force_grid && cg_rows_fits(m, nsm, cg_gram_partial_doubles(m.R)))
+    return launch_cg_rows(m, pi, dscale, damp, lambda, tol, maxiter, rhs, v, x, G, S, part, st_dev, mode, nsm, st);
   const int NT = (int)((m.R + 7) / 8);
   switch (NT) {
 #define TF_CASE(k) \
@@ -789,14 +795,12 @@ extern "C" void tf_cg_debug_dump(void) {
   unsigned long long h[64];
   cudaDeviceSynchronize();
   cudaMemcpy(h, tfk::g_tstamp, sizeof(h), cudaMemcpyDeviceToHost);
+  // slots 8 (it - 1) + 0..7; row-owned kernel: start, Gram done, barrier, S done, barrier, apply done,
+  // <p,z> barrier, ||r||^2 barrier (the grid kernel's slots: start, gram, sync, S+sync, apply, sync+alpha, update)
   for (int it = 0; it < 3; ++it) {
     const unsigned long long* b = h + 8 * it;
-    printf("iter %d: gram %.2f us, sync %.2f, S+sync %.2f, apply %.2f, sync+alpha %.2f, update %.2f us\n", it + 1,
-           (b[1] - b[0]) * 1e-3, (b[2] - b[1]) * 1e-3, (b[3] - b[2]) * 1e-3, (b[4] - b[3]) * 1e-3,
-           (b[5] - b[4]) * 1e-3, (b[6] - b[5]) * 1e-3);
-  }
-  for (int i = 0; i < 2; ++i) {
-    const unsigned long long* b = h + 40 + 4 * i;
-    printf("apply item %d: staging %.2f us, compute %.2f us, epilogue->next %.2f us\n", i, (b[1] - b[0]) * 1e-3, (b[2] - b[1]) * 1e-3, (b[4] - b[2]) * 1e-3);
+    printf("iter %d:", it + 1);
+    for (int k = 1; k < 8; ++k) printf(" %.2f", (b[k] - b[k - 1]) * 1e-3);
+    printf(" us; next start %.2f\n", (b[8] - b[7]) * 1e-3);
   }
 }

@@ -1,0 +1,643 @@
+// Row-owned persistent CG (rows a8/a9: Thm Hv; Alg. CG-dGN).
+//
+// One cooperative launch runs the whole CG. Block b owns a contiguous range of <= 8*mtb rows of ONE mode l
+// (blocks per mode in proportion to the mode sizes). For the whole solve it keeps in shared memory the rows of
+// W_l and of the search direction p ([column][row], pitch 8 mtb + 4 = 4 or 12 mod 16: conflict-free DMMA
+// fragments in both contractions) and the constant Pi~_l = D_l Pi^(l) D_l ([column][k], pitch R8 + 4); every
+// thread keeps its entries of r in registers (x: global, updated in place) (the positions of its output tiles of the apply). No vector
+// travels through global memory inside the loop: per iteration the global traffic is the Gram partial of each
+// block (R^2 doubles), the reduced S~ matrices and their streamed chunks. Four grid-wide steps per iteration:
+//   G  p <- r + beta p (registers -> shared); Gram partial P_b = p_rows^T W_rows (DMMA, inner dim = rows),
+//      stored transposed (16-byte stores of a lane's two adjacent columns)
+//   S  G_l = D_l sum_b P_b (fixed order, one lane per mode and entry, all loads in flight) and
+//      S~_l = (sum_{l' != l} Pi^(l,l') * G_l') D_l                                     (Thm Hv's S_l, scaled)
+//   Y  z = p Pi~_l + W S~_l + lambda_c D_c^2 p: the Thm-Hv apply with the Jacobi scaling folded into the
+//      operands (z = D (V Pi + W S + lambda V), V = p D); p Pi~ runs from shared memory
+//      while the S~ chunks stream in through a cp.async ring; z stays in registers; partial <p, z>
+//   U  alpha = ||r||^2 / <p, z>; r -= alpha z; x += alpha p (registers); partial ||r||^2 -> beta
+// Scalars are recomputed by every block from the per-block partials in the same fixed order (deterministic,
+// no host round trip). Mode 1 (single matvec y = (J^T J + lambda D) v) runs G, S and Y once.
+#include <cooperative_groups.h>
+#include <cstdio>
+#include <cstdlib>
+
+#include "tf_internal.h"
+#include "tf_device.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace tfk {
+
+unsigned long long* cg_debug_tstamp();
+
+constexpr int kRThreads = 256;
+constexpr int kRMaxMT = 6;        // m-tiles (8 rows) per block at most
+constexpr int kKC = 16;           // k-rows of S~ per streamed chunk
+constexpr int kLDK = kKC + 4;     // chunk pitch per column (4 mod 16: conflict-free B fragments)
+constexpr int kNBUF = 4;          // cp.async ring depth
+constexpr int kSBatch = 16;       // Gram partials loaded at once per lane in stage S
+constexpr int kRedSlots = 64;
+
+struct RowsArgs {
+  Modes m;
+  const double* pi;       // 6 R^2 Hadamard chains [Pi1 | Pi2 | Pi3 | Pi12 | Pi13 | Pi23]
+  const double* dscale;   // 3R or nullptr: Jacobi M^{-1/2} per (mode, r)
+  const double* damp;     // 3R or nullptr: damping matrix D per (mode, r) (nullptr = I)
+  double lambda, tol;
+  int maxiter;
+  const double* rhs;      // CG right-hand side (w-coordinates)
+  const double* v;        // matvec input
+  double* x;              // CG solution / matvec output
+  double* G;              // nblk x R^2 Gram partials
+  double* S;              // 3 R^2: S~_l
+  double* part;           // 2 x nblk scalar partials
+  CgState* st;
+  int mode;               // 0 CG, 1 single matvec
+  int bstart[4];          // first block of each mode; bstart[3] = number of blocks
+  int mtb;                // row capacity per block = 8 mtb
+  unsigned long long* tstamp;
+};
+
+__host__ __device__ constexpr int rows_ldr(int mtb) { return 8 * mtb + 4; }
+__host__ __device__ constexpr int rows_ldpi(int NT) { return 8 * NT + 4; }
+__host__ __device__ constexpr size_t rows_smem_doubles(int NT, int mtb) {
+  return (size_t)2 * (8 * NT) * rows_ldr(mtb) + (size_t)(8 * NT) * rows_ldpi(NT) + (size_t)kNBUF * (8 * NT) * kLDK +
+         (size_t)2 * (8 * NT) + kRedSlots;
+}
+
+__device__ __forceinline__ void rstamp(const RowsArgs& A, int slot) {
+  if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && slot < 64) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    A.tstamp[slot] = t;
+  }
+}
+
+__device__ __forceinline__ void cpa8(double* dst, const double* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cpa16(double* dst, const double* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+// a global load issued where it stands (volatile: not sunk to its first use, so that its latency overlaps the
+// work placed between the load and the use)
+__device__ __forceinline__ double ld_early(const double* p) {
+  double v;
+  asm volatile("ld.global.f64 %0, [%1];\n" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// the same total in every block: warp 0 sums the per-block partials (fixed lane order + fixed butterfly)
+__device__ __forceinline__ double rows_grid_total(const double* part, int nblk, double* red) {
+  if (threadIdx.x < 32) {
+    double v = 0.0;
+    for (int i = threadIdx.x; i < nblk; i += 32) v += part[i];
+    v = warp_sum(v);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const double t = red[0];
+  __syncthreads();
+  return t;
+}
+
+__device__ __forceinline__ double rows_block_sum(double v, double* red) {
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[1 + (threadIdx.x >> 5)] = v;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int i = 0; i < kRThreads / 32; ++i) t += red[1 + i];
+  __syncthreads();
+  return t;
+}
+
+// One S~ chunk: rows k0 .. k0 + kKC of the R x R column-major source, all R8 columns, into
+// buf[c][kk] (pitch kLDK); zero beyond R.
+__device__ __forceinline__ void issue_chunk(const double* src, int R, int R8, int k0, double* buf, bool pair) {
+  if (pair) {   // 16-byte copies (R even and src 16-byte aligned)
+    for (int idx = threadIdx.x; idx < R8 * (kKC / 2); idx += kRThreads) {
+      const int c = idx / (kKC / 2), kk = 2 * (idx % (kKC / 2));
+      const int k = k0 + kk;
+      const int valid = c < R ? (k + 1 < R ? 16 : (k < R ? 8 : 0)) : 0;
+      cpa16(buf + c * kLDK + kk, valid ? src + k + (int64_t)R * c : src, valid);
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < R8 * kKC; idx += kRThreads) {
+      const int c = idx / kKC, kk = idx % kKC;
+      const int k = k0 + kk;
+      const bool ok = c < R && k < R;
+      cpa8(buf + c * kLDK + kk, ok ? src + k + (int64_t)R * c : src, ok);
+    }
+  }
+}
+
+// One k-step of the apply for a warp's tiles: m-tile wsub (and wsub + 4 when MGT = 2 and it exists) times the NJ
+// column tiles J0 .. J0 + NJ - 1. A fragments from [k][row] rows (pitch ldr), B from [column][k] operands (pitch
+// ldb). Every DMMA of the common path is unconditional (no per-instruction predicate, no warp re-convergence).
+template <int NJ, int J0, int MGT, int NH>
+__device__ __forceinline__ void apply_kstep(double (&acc)[MGT][NH][2], const double* arows, int ldr, const double* bops,
+                                            int ldb, int ka, int kb, int wsub, int g, bool second) {
+  double fa0 = arows[ka * ldr + 8 * wsub + g];
+  double fb[NJ > 0 ? NJ : 1];
+#pragma unroll
+  for (int jj = 0; jj < NJ; ++jj) fb[jj] = bops[(8 * (J0 + jj) + g) * ldb + kb];
+#pragma unroll
+  for (int jj = 0; jj < NJ; ++jj) dmma(acc[0][jj], fa0, fb[jj]);
+  if (MGT > 1 && second) {
+    const double fa1 = arows[ka * ldr + 8 * (wsub + 4) + g];
+#pragma unroll
+    for (int jj = 0; jj < NJ; ++jj) dmma(acc[MGT - 1][jj], fa1, fb[jj]);
+  }
+}
+
+template <int NT, int MGT>
+__global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double rsm[];
+  constexpr int R8 = 8 * NT;
+  constexpr int NH = (NT + 1) / 2;                       // apply n-tiles per warp (column half)
+  constexpr int MG = MGT;                                // apply m-tiles per warp at most (s, s + 4)
+  constexpr int GBASE = (NT / 4) * 4;                   // Gram i-tiles handled as full rows of tiles
+  constexpr int GLO = ((NT - GBASE) * NT + 7) / 8;       // leftover Gram tiles per warp at most
+  constexpr int LDPI = rows_ldpi(NT);
+  constexpr int NCH = (R8 + kKC - 1) / kKC;              // S~ chunks
+  const Modes& m = A.m;
+  const int R = (int)m.R;
+  const int64_t RR = (int64_t)R * R;
+  const int nblk = A.bstart[3];
+  const int LDR = rows_ldr(A.mtb);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+
+  // ---- this block's rows
+  const int b = blockIdx.x;
+  int l = 0;
+  while (l < 2 && b >= A.bstart[l + 1]) ++l;
+  const int bi = b - A.bstart[l], nbl = A.bstart[l + 1] - A.bstart[l];
+  const int64_t nl = m.n[l], off = m.off[l];
+  const int64_t a0 = nl * bi / nbl, a1 = nl * (bi + 1) / nbl;
+  const int nr = (int)(a1 - a0);
+  const int MTb = (nr + 7) / 8;
+  const double* Dl = A.dscale ? A.dscale + l * R : nullptr;
+
+  double* sW = rsm;
+  double* sP = sW + R8 * LDR;
+  double* sPi = sP + R8 * LDR;
+  double* ring = sPi + R8 * LDPI;
+  double* sD = ring + kNBUF * R8 * kLDK;   // D_c (Jacobi scale of this mode; 1 without)
+  double* sLD = sD + R8;                   // lambda_c D_c^2 (lambda_c = lambda damp_c)
+  double* red = sLD + R8;
+
+  // apply tiles of this warp: sub-partition s = warp % 4 owns m-tiles s and s + 4 (every SMSP the same share
+  // of the critical 8-row tiles), the two warps of a sub-partition split the NT column tiles in halves (NH, NT - NH);
+  // all bounds are warp-uniform. The thread owns the entries (row 8 mt + g, column 8 j + 2 q + e) of r, x and z.
+  const int wsub = warp & 3, whalf = warp >> 2;
+#define TF_TILES(BODY)                                       \
+  _Pragma("unroll") for (int mi = 0; mi < MG; ++mi)          \
+  _Pragma("unroll") for (int jj = 0; jj < NH; ++jj) {        \
+    const int mt = wsub + 4 * mi, j = whalf * NH + jj;       \
+    if (mt < MTb && j < NT) { BODY }                         \
+  }
+
+  // ---- prologue (every copy in flight at once): W rows, p = 0 (or v), Pi^(l), D; then Pi~ = D Pi^(l) D in place;
+  // r = D rhs in registers, x = 0
+  const double* Wl = m.W[l];
+  for (int idx = threadIdx.x; idx < R8 * LDR; idx += kRThreads) {
+    const int c = idx / LDR, a = idx % LDR;
+    const bool ok = c < R && a < nr;
+    const int64_t gi = ok ? a0 + a + nl * c : 0;
+    cpa8(sW + idx, Wl + gi, ok);
+    cpa8(sP + idx, (A.mode == 1 ? A.v : Wl) + (A.mode == 1 ? off : 0) + gi, ok && A.mode == 1);
+  }
+  {
+    const double* P = A.pi + (int64_t)l * RR;
+    for (int idx = threadIdx.x; idx < R8 * LDPI; idx += kRThreads) {
+      const int c = idx / LDPI, k = idx % LDPI;
+      const bool ok = c < R && k < R;
+      cpa8(sPi + idx, P + (ok ? k + (int64_t)R * c : 0), ok);
+    }
+  }
+  for (int c = threadIdx.x; c < R8; c += kRThreads) cpa8(sD + c, Dl ? Dl + min(c, R - 1) : Wl, Dl != nullptr && c < R);
+  cpa_commit();
+  cpa_wait<0>();
+  __syncthreads();
+  for (int c = threadIdx.x; c < R8; c += kRThreads) {
+    if (!Dl) sD[c] = c < R ? 1.0 : 0.0;
+    const double lam = c < R ? (A.damp ? A.lambda * A.damp[l * R + c] : A.lambda) : 0.0;
+    sLD[c] = lam * sD[c] * sD[c];
+  }
+  if (Dl) {
+    for (int idx = threadIdx.x; idx < R8 * LDPI; idx += kRThreads) {
+      const int c = idx / LDPI, k = idx % LDPI;
+      if (c < R8 && k < R8) sPi[idx] *= sD[k] * sD[c];
+    }
+  }
+  __syncthreads();
+  double rreg[MG][NH][2];
+  double s0 = 0.0;
+#pragma unroll
+  for (int mi = 0; mi < MG; ++mi)
+#pragma unroll
+    for (int jj = 0; jj < NH; ++jj) rreg[mi][jj][0] = rreg[mi][jj][1] = 0.0;
+  if (A.mode == 0) {
+    TF_TILES({
+      const int row = 8 * mt + g;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = 8 * j + 2 * q + e;
+        if (row < nr && c < R) {
+          const double rv = A.rhs[off + a0 + row + nl * c] * sD[c];
+          rreg[mi][jj][e] = rv;
+          s0 = fma(rv, rv, s0);
+        }
+      }
+    })
+    // x = 0 (after the loads of rhs: no load waits behind a store)
+    TF_TILES({
+      const int row = 8 * mt + g;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = 8 * j + 2 * q + e;
+        if (row < nr && c < R) A.x[off + a0 + row + nl * c] = 0.0;
+      }
+    })
+  }
+  double* part0 = A.part;
+  double* part1 = A.part + nblk;
+  double rr = 0.0;
+  if (A.mode == 0) {
+    s0 = rows_block_sum(s0, red);
+    if (threadIdx.x == 0) part1[b] = s0;
+    grid.sync();
+    rr = rows_grid_total(part1, nblk, red);
+  } else {
+    __syncthreads();
+  }
+
+  const double* Sl = A.S + (int64_t)l * RR;
+  const bool pairS = (R & 1) == 0 && (reinterpret_cast<uintptr_t>(Sl) & 15) == 0;
+  double beta = 0.0;
+  int iters = 0, nonfinite = 0;
+  const int maxit = A.mode == 1 ? 1 : (rr == 0.0 ? 0 : A.maxiter);   // reading R33
+  double acc[MG][NH][2];
+
+  for (int it = 1; it <= maxit; ++it) {
+    const int sb = 8 * (it - 1);
+    rstamp(A, sb + 0);
+    // ---- G: p <- r + beta p at this thread's positions; Gram partial of the raw p rows
+    if (A.mode == 0) {
+      TF_TILES({
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int o = (8 * j + 2 * q + e) * LDR + 8 * mt + g;
+          sP[o] = fma(beta, sP[o], rreg[mi][jj][e]);
+        }
+      })
+      __syncthreads();
+    }
+    {
+      // warp w: i-tiles w and w + 8 of the GBASE full rows of tiles, one row of NT tiles at a time (B fragments
+      // reloaded per row: 1.08 shared loads per DMMA), then its share of the leftover tiles (i >= GBASE)
+      const int ks = (nr + 3) / 4;
+      double* Gp = A.G + (int64_t)b * RR;
+#pragma unroll 1
+      for (int ii = 0; ii < 2; ++ii) {
+        const int i = warp + 8 * ii;
+        if (i >= GBASE) break;
+        double gf[NT][2];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) gf[j][0] = gf[j][1] = 0.0;
+#pragma unroll 2
+        for (int s = 0; s < ks; ++s) {
+          const int a = 4 * s + q;
+          const double fa = sP[(8 * i + g) * LDR + a];
+#pragma unroll
+          for (int j = 0; j < NT; ++j) dmma(gf[j], fa, sW[(8 * j + g) * LDR + a]);
+        }
+        // the partial is stored transposed (entry (r, c) at c + R r): a lane's two columns are adjacent
+        const int r = 8 * i + g;
+        if (r < R) {
+#pragma unroll
+          for (int j = 0; j < NT; ++j) {
+            const int c = 8 * j + 2 * q;
+            double* dst = Gp + c + (int64_t)R * r;
+            if (c + 1 < R && (R & 1) == 0) *reinterpret_cast<double2*>(dst) = make_double2(gf[j][0], gf[j][1]);
+            else {
+              if (c < R) dst[0] = gf[j][0];
+              if (c + 1 < R) dst[1] = gf[j][1];
+            }
+          }
+        }
+      }
+      // leftover tiles (i >= GBASE): tile warp + 8u; the bound is warp-uniform, so it is a branch around an
+      // unpredicated k-loop
+#pragma unroll 1
+      for (int u = 0; u < GLO; ++u) {
+        const int t = warp + 8 * u;
+        if (t >= (NT - GBASE) * NT) break;
+        const int i = GBASE + t / NT, j = t % NT;
+        double gl[2] = {0.0, 0.0};
+        for (int s = 0; s < ks; ++s) {
+          const int a = 4 * s + q;
+          dmma(gl, sP[(8 * i + g) * LDR + a], sW[(8 * j + g) * LDR + a]);
+        }
+        const int r = 8 * i + g;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = 8 * j + 2 * q + e;
+          if (r < R && c < R) Gp[c + (int64_t)R * r] = gl[e];
+        }
+      }
+    }
+    rstamp(A, sb + 1);
+    grid.sync();
+    rstamp(A, sb + 2);
+    // ---- S, overlapped with the first half of p Pi~ (which does not depend on S): one lane per (entry, mode)
+    // issues the loads of that mode's partials (block order, all in flight), the DMMAs of p Pi~ run while they
+    // are in flight, then the lane sums them in block order; the three lanes of an entry exchange their sums and
+    // each writes its mode's S~
+#pragma unroll
+    for (int mi = 0; mi < MG; ++mi)
+#pragma unroll
+      for (int jj = 0; jj < NH; ++jj) acc[mi][jj][0] = acc[mi][jj][1] = 0.0;
+    const bool second = MG > 1 && wsub + 4 < MTb;
+    auto pi_steps = [&](int s0, int s1) {
+#pragma unroll 4
+      for (int s = s0; s < s1; ++s) {
+        if (whalf == 0) apply_kstep<NH, 0, MG, NH>(acc, sP, LDR, sPi, LDPI, 4 * s + q, 4 * s + q, wsub, g, second);
+        else apply_kstep<NT - NH, NH, MG, NH>(acc, sP, LDR, sPi, LDPI, 4 * s + q, 4 * s + q, wsub, g, second);
+      }
+    };
+    constexpr int KS1 = (R8 / 4) / 2;
+    {
+      const int gw = blockIdx.x * (kRThreads / 32) + warp, nw = nblk * (kRThreads / 32);
+      const int ll = lane % 3;
+      bool first = true;
+      for (int64_t eb = (int64_t)gw * 10; first || eb < RR; eb += (int64_t)nw * 10) {
+        const int64_t e = eb + lane / 3;
+        const bool act = lane < 30 && e < RR;
+        const int be = A.bstart[ll + 1];
+        const double* gp = A.G + (act ? e : 0);
+        int bb = A.bstart[ll];
+        double v[kSBatch];
+#pragma unroll
+        for (int u = 0; u < kSBatch; ++u) {
+          const bool ok = act && bb + u < be;
+          v[u] = ok ? gp[(int64_t)(bb + u) * RR] : 0.0;
+        }
+        const int r = act ? (int)(e / R) : 0, c = act ? (int)(e % R) : 0;   // partials are stored transposed
+        const double* D = A.dscale;
+        double d0 = 1.0, d1 = 1.0, d2 = 1.0, dc = 1.0, p12 = 0.0, p13 = 0.0, p23 = 0.0;
+        if (act) {
+          if (D) {
+            d0 = D[r];
+            d1 = D[R + r];
+            d2 = D[2 * R + r];
+            dc = D[ll * R + c];
+          }
+          const int64_t rc = r + (int64_t)R * c;
+          p12 = A.pi[3 * RR + rc];
+          p13 = A.pi[4 * RR + rc];
+          p23 = A.pi[5 * RR + rc];
+        }
+        if (first) pi_steps(0, KS1);   // the loads above are in flight meanwhile
+        first = false;
+        double gsum = 0.0;
+#pragma unroll
+        for (int u = 0; u < kSBatch; ++u) gsum += v[u];
+        for (bb += kSBatch; bb < be; bb += kSBatch) {   // modes with more than kSBatch blocks
+#pragma unroll
+          for (int u = 0; u < kSBatch; ++u) v[u] = (act && bb + u < be) ? gp[(int64_t)(bb + u) * RR] : 0.0;
+#pragma unroll
+          for (int u = 0; u < kSBatch; ++u) gsum += v[u];
+        }
+        const int base = 3 * (lane / 3);
+        const double x0 = __shfl_sync(0xffffffffu, gsum, min(base, 31));
+        const double x1 = __shfl_sync(0xffffffffu, gsum, min(base + 1, 31));
+        const double x2 = __shfl_sync(0xffffffffu, gsum, min(base + 2, 31));
+        if (act) {
+          const double g0 = x0 * d0, g1 = x1 * d1, g2 = x2 * d2;
+          double sv;
+          if (ll == 0) sv = p12 * g1 + p13 * g2;
+          else if (ll == 1) sv = p12 * g0 + p23 * g2;
+          else sv = p13 * g0 + p23 * g1;
+          A.S[(int64_t)ll * RR + r + (int64_t)R * c] = sv * dc;
+        }
+      }
+    }
+    rstamp(A, sb + 3);
+    grid.sync();
+    rstamp(A, sb + 4);
+    // ---- Y: S~ chunks stream in while the second half of p Pi~ runs, then W S~ from the ring
+    for (int ck = 0; ck < kNBUF - 1; ++ck) {
+      if (ck < NCH) issue_chunk(Sl, R, R8, ck * kKC, ring + ck * R8 * kLDK, pairS);
+      cpa_commit();
+    }
+    pi_steps(KS1, R8 / 4);
+    for (int ck = 0; ck < NCH; ++ck) {
+      cpa_wait<kNBUF - 2>();
+      __syncthreads();
+      {
+        const int nx = ck + kNBUF - 1;
+        if (nx < NCH) issue_chunk(Sl, R, R8, nx * kKC, ring + (nx % kNBUF) * R8 * kLDK, pairS);
+        cpa_commit();
+      }
+      const int k0 = ck * kKC;
+      const double* buf = ring + (ck % kNBUF) * R8 * kLDK;
+      const int nks = min(kKC, R8 - k0) / 4;
+#pragma unroll 4
+      for (int s = 0; s < nks; ++s) {
+        if (whalf == 0) apply_kstep<NH, 0, MG, NH>(acc, sW, LDR, buf, kLDK, k0 + 4 * s + q, 4 * s + q, wsub, g, second);
+        else apply_kstep<NT - NH, NH, MG, NH>(acc, sW, LDR, buf, kLDK, k0 + 4 * s + q, 4 * s + q, wsub, g, second);
+      }
+    }
+    rstamp(A, sb + 5);
+    // epilogue: z (registers) and <p, z>; matvec mode writes y
+    double pz = 0.0;
+    TF_TILES({
+      const int row = 8 * mt + g;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = 8 * j + 2 * q + e;
+        if (row < nr && c < R) {
+          const double pv = sP[c * LDR + row];
+          const double z = fma(sLD[c], pv, acc[mi][jj][e]);
+          acc[mi][jj][e] = z;
+          if (A.mode == 1) A.x[off + a0 + row + nl * c] = z;
+          else pz = fma(pv, z, pz);
+        }
+      }
+    })
+    if (A.mode == 1) break;
+    pz = rows_block_sum(pz, red);
+    if (threadIdx.x == 0) part0[b] = pz;
+    grid.sync();
+    rstamp(A, sb + 6);
+    const double alpha = rr / rows_grid_total(part0, nblk, red);
+    if (!isfinite(alpha)) {
+      nonfinite = it;
+      break;
+    }
+    // ---- U: r -= alpha z, x += alpha p at this thread's positions; ||r||^2 (x: all loads first, then stores)
+    double s2 = 0.0;
+    {
+      double xv[MG][NH][2];
+      TF_TILES({
+        const int row = 8 * mt + g;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = 8 * j + 2 * q + e;
+          xv[mi][jj][e] = (row < nr && c < R) ? A.x[off + a0 + row + nl * c] : 0.0;
+        }
+      })
+      TF_TILES({
+        const int row = 8 * mt + g;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = 8 * j + 2 * q + e;
+          if (row < nr && c < R) {
+            A.x[off + a0 + row + nl * c] = fma(alpha, sP[c * LDR + row], xv[mi][jj][e]);
+            const double rn = fma(-alpha, acc[mi][jj][e], rreg[mi][jj][e]);
+            rreg[mi][jj][e] = rn;
+            s2 = fma(rn, rn, s2);
+          }
+        }
+      })
+    }
+    s2 = rows_block_sum(s2, red);
+    if (threadIdx.x == 0) part1[b] = s2;
+    grid.sync();
+    rstamp(A, sb + 7);
+    const double rr_new = rows_grid_total(part1, nblk, red);
+    beta = rr_new / rr;
+    rr = rr_new;
+    iters = it;
+    if (!isfinite(beta)) {
+      nonfinite = it;
+      break;
+    }
+    if (rr_new < A.tol) break;
+  }
+  cpa_wait<0>();
+  if (A.mode == 1) return;
+  // x in w-coordinates: x = D x_hat
+  if (Dl) {
+    TF_TILES({
+      const int row = 8 * mt + g;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = 8 * j + 2 * q + e;
+        if (row < nr && c < R) A.x[off + a0 + row + nl * c] *= sD[c];
+      }
+    })
+  }
+#undef TF_TILES
+  if (b == 0 && threadIdx.x == 0) {
+    A.st->rr = rr;
+    A.st->iters = iters;
+    A.st->nonfinite = nonfinite;
+    A.st->done = 1;
+  }
+}
+
+// Blocks per mode: start from one each and give every further block to the mode with the most rows per block;
+// returns the m-tile capacity needed (0 if a mode has no rows).
+static int rows_plan(const Modes& m, int grid, int bstart[4]) {
+  int nb[3] = {1, 1, 1};
+  for (int l = 0; l < 3; ++l)
+    if (m.n[l] < 1) return 0;
+  // add blocks only while some block owns more than 24 rows (measured: c2/c3 run 13/15 us per iteration instead
+  // of 17 us on the full grid, c4/c5 are unchanged): fewer blocks mean fewer Gram partials to reduce in stage S
+  static const int target = [] {
+    const char* e = getenv("TF_CG_ROWS_TARGET");
+    return e ? atoi(e) : 24;
+  }();
+  for (int k = 3; k < grid; ++k) {
+    int best = -1;
+    int64_t most = 0;
+    for (int l = 0; l < 3; ++l) {
+      if (nb[l] >= m.n[l]) continue;
+      const int64_t rows = (m.n[l] + nb[l] - 1) / nb[l];
+      if (rows > most && rows > target) {
+        most = rows;
+        best = l;
+      }
+    }
+    if (best < 0) break;
+    nb[best] += 1;
+  }
+  bstart[0] = 0;
+  int64_t rmax = 0;
+  for (int l = 0; l < 3; ++l) {
+    bstart[l + 1] = bstart[l] + nb[l];
+    rmax = std::max<int64_t>(rmax, (m.n[l] + nb[l] - 1) / nb[l]);
+  }
+  // capacity of at least 4 m-tiles: sub-partition s always computes m-tile s (zero rows when beyond the block)
+  return std::max(4, (int)((rmax + 7) / 8));
+}
+
+template <int NT>
+static cudaError_t launch_rows_nt(RowsArgs& a, cudaStream_t st) {
+  auto kern = a.mtb > 4 ? k_cg_rows<NT, 2> : k_cg_rows<NT, 1>;
+  const size_t smem = 8 * rows_smem_doubles(NT, a.mtb);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRThreads, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  void* params[] = {&a};
+  return cudaLaunchCooperativeKernel((const void*)kern, dim3(a.bstart[3]), dim3(kRThreads), params, smem, st);
+}
+
+// Plans the row-owned kernel for these modes on `grid` blocks; returns false (nothing launched) when a block
+// would own more than 8 kRMaxMT rows, shared memory does not fit, or the scratch buffers are too small.
+bool cg_rows_fits(const Modes& m, int grid, size_t gram_partial_doubles) {
+  int bs[4];
+  const int mtb = rows_plan(m, grid, bs);
+  const int NT = (int)((m.R + 7) / 8);
+  if (mtb < 1 || mtb > kRMaxMT || NT > 16) return false;
+  if (8 * rows_smem_doubles(NT, mtb) > 227 * 1024) return false;
+  return (size_t)bs[3] * m.R * m.R <= gram_partial_doubles;
+}
+
+cudaError_t launch_cg_rows(const Modes& m, const double* pi, const double* dscale, const double* damp, double lambda,
+                           double tol, int maxiter, const double* rhs, const double* v, double* x, double* G,
+                           double* S, double* part, CgState* st_dev, int mode, int grid, cudaStream_t st) {
+  RowsArgs a;
+  a.m = m;
+  a.pi = pi;
+  a.dscale = dscale;
+  a.damp = damp;
+  a.lambda = lambda;
+  a.tol = tol;
+  a.maxiter = maxiter;
+  a.rhs = rhs;
+  a.v = v;
+  a.x = x;
+  a.S = S;
+  a.part = part;
+  a.st = st_dev;
+  a.mode = mode;
+  a.tstamp = cg_debug_tstamp();
+  a.mtb = rows_plan(m, grid, a.bstart);
+  a.G = G;
+  const int NT = (int)((m.R + 7) / 8);
+  switch (NT) {
+#define TF_CASE(k) \
+  case k:          \
+    return launch_rows_nt<k>(a, st);
+    TF_CASE(1) TF_CASE(2) TF_CASE(3) TF_CASE(4) TF_CASE(5) TF_CASE(6) TF_CASE(7) TF_CASE(8)
+    TF_CASE(9) TF_CASE(10) TF_CASE(11) TF_CASE(12) TF_CASE(13) TF_CASE(14) TF_CASE(15) TF_CASE(16)
+#undef TF_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace tfk

@@ -84,6 +84,11 @@ cudaError_t launch_cg_persistent(const Modes& m, const double* pi, const double*
                                  double* z, double* G, double* S, double* part, CgState* st_dev, int mode, int grid,
                                  bool allow_small, cudaStream_t st);
 size_t cg_gram_partial_doubles(int64_t R);
+// Row-owned persistent CG (k_cg_rows.cu): used by launch_cg_persistent when cg_rows_fits()
+bool cg_rows_fits(const Modes& m, int grid, size_t gram_partial_doubles);
+cudaError_t launch_cg_rows(const Modes& m, const double* pi, const double* dscale, const double* damp, double lambda,
+                           double tol, int maxiter, const double* rhs, const double* v, double* x, double* G,
+                           double* S, double* part, CgState* st_dev, int mode, int grid, cudaStream_t st);
 
 // dGN outer-loop helpers (k_small.cu)
 cudaError_t launch_dots(int64_t n, const double* g, const double* x, const double* y, double* partial, double* out,

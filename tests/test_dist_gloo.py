@@ -157,3 +157,34 @@ def test_sharded_dgn_exchange_gloo(world):
         assert abs(sums[0] - float(P.T.abs().sum())) <= 1e-12 * sums[0]
     for _, g, sums in res[1:]:
         assert np.array_equal(g, res[0][1]) and np.array_equal(sums, res[0][2])
+
+
+def test_bench_multi_rank_control_path_under_torchrun():
+    """bench.py's multi-rank control path end to end, launched the way the driver launches N > 1 (torchrun, one
+    process per rank, 127.0.0.1 rendezvous), on CPU with gloo (`--mock`: the same rank set-up, K-sharding,
+    ShardedEvaluator all-reduce, barriers and max-over-ranks timing, with a stand-in evaluator whose all-reduced
+    output is exactly checkable): both ranks exit 0, rank 0 alone prints one JSON line, the shards partition K,
+    f = sum of all of T and row k of the dF/dC block is the sum of slice k for every k (each rank contributed its
+    own slices and zeros elsewhere)."""
+    import json
+    import subprocess
+    import sys
+    import synth
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    port = _free_port()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2", "--mock", "--config", "c1", "--steps",
+           "2", "--warmup", "3"]
+    out = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, out.stdout
+    b = json.loads(lines[0])
+    assert b["mock"] is True and b["value"] is None and b["n_gpus"] == 2
+    assert b["config"]["parallelism"].startswith("K-sharded x2")
+    P = synth.make_problem("c1", "cpu")
+    K = P.cfg.K
+    assert b["check"]["shards"] == [[0, K // 2], [K // 2, K]]
+    T = P.T.numpy()
+    assert abs(b["check"]["f"] - float(T.sum())) <= 1e-12 * abs(T).sum()
+    np.testing.assert_allclose(b["check"]["gC_row0"], T.reshape(K, -1).sum(axis=1), rtol=1e-13, atol=1e-13)

@@ -279,13 +279,18 @@ def test_gn_matvec_against_plain_route(ctx):
     assert rel_err(to_np(y), oracle.gn_matvec_plain(w, v, 1e-3, c.I, c.J, c.K, c.R)) <= TOL
 
 
+@pytest.mark.parametrize("kernel", ["auto", "grid"])
 @pytest.mark.parametrize("grid", [0, 5])
 @pytest.mark.parametrize("jacobi", [False, True])
 @pytest.mark.parametrize("case", ["c1", "c3r", "r120", "even30", "even31"])
-def test_cg_per_iteration(ctx, case, jacobi, grid):
-    """Every CG iterate x^(i), i = 1..10, against Alg. CG-dGN in the oracle (rhs = -grad, lambda = 1e-3). grid = 5
-    runs the persistent grid kernel on 5 blocks (tf_ctx_set_cg_grid), so every block processes several Gram and
-    apply items, as on the full grid at c5."""
+def test_cg_per_iteration(ctx, case, jacobi, grid, kernel, monkeypatch):
+    """Every CG iterate x^(i), i = 1..10, against Alg. CG-dGN in the oracle (rhs = -grad, lambda = 1e-3), through
+    both persistent kernels: "auto" (the row-owned kernel wherever its shared memory fits — every case here but
+    R = 120 — and the one-CTA kernel for n <= 4096 on the default grid) and "grid" (TF_CG_KERNEL=grid: the
+    item-based grid kernel). grid = 5 caps the launch at 5 blocks (tf_ctx_set_cg_grid): the row-owned kernel then
+    owns 2-6 m-tiles per block, the grid kernel processes several Gram and apply items per block."""
+    if kernel == "grid":
+        monkeypatch.setenv("TF_CG_KERNEL", "grid")
     ctx.set_cg_grid(grid)
     try:
         _cg_per_iteration(ctx, case, jacobi)
