@@ -51,6 +51,7 @@ struct RowsArgs {
   double* G;              // nblk x R^2 Gram partials
   double* S;              // 3 R^2: S~_l
   double* part;           // 2 x nblk scalar partials
+  unsigned int* bar;      // grid-barrier arrival counter (zeroed before the launch)
   CgState* st;
   int mode;               // 0 CG, 1 single matvec
   int bstart[4];          // first block of each mode; bstart[3] = number of blocks
@@ -71,6 +72,23 @@ __device__ __forceinline__ void rstamp(const RowsArgs& A, int slot) {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     A.tstamp[slot] = t;
   }
+}
+
+// Grid-wide barrier of the cooperative launch: every block's thread 0 adds one arrival with release semantics
+// (after a block barrier, so the block's earlier writes are ordered before it) and spins with acquire loads until
+// all blocks of this phase have arrived; the counter only grows (phase e waits for e * nblk arrivals).
+__device__ __forceinline__ void rows_grid_sync(unsigned int* bar, unsigned int& phase, int nblk) {
+  __syncthreads();
+  ++phase;
+  if (threadIdx.x == 0) {
+    const unsigned int target = phase * (unsigned int)nblk;
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(bar) : "memory");
+    unsigned int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
 }
 
 __device__ __forceinline__ void cpa8(double* dst, const double* src, bool valid) {
@@ -158,7 +176,7 @@ __device__ __forceinline__ void apply_kstep(double (&acc)[MGT][NH][2], const dou
 
 template <int NT, int MGT>
 __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
-  cg::grid_group grid = cg::this_grid();
+  unsigned int bar_phase = 0;
   extern __shared__ __align__(16) double rsm[];
   constexpr int R8 = 8 * NT;
   constexpr int NH = (NT + 1) / 2;                       // apply n-tiles per warp (column half)
@@ -273,7 +291,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
   if (A.mode == 0) {
     s0 = rows_block_sum(s0, red);
     if (threadIdx.x == 0) part1[b] = s0;
-    grid.sync();
+    rows_grid_sync(A.bar, bar_phase, nblk);
     rr = rows_grid_total(part1, nblk, red);
   } else {
     __syncthreads();
@@ -355,7 +373,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
       }
     }
     rstamp(A, sb + 1);
-    grid.sync();
+    rows_grid_sync(A.bar, bar_phase, nblk);
     rstamp(A, sb + 2);
     // ---- S, overlapped with the first half of p Pi~ (which does not depend on S): one lane per (entry, mode)
     // issues the loads of that mode's partials (block order, all in flight), the DMMAs of p Pi~ run while they
@@ -431,7 +449,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
       }
     }
     rstamp(A, sb + 3);
-    grid.sync();
+    rows_grid_sync(A.bar, bar_phase, nblk);
     rstamp(A, sb + 4);
     // ---- Y: S~ chunks stream in while the second half of p Pi~ runs, then W S~ from the ring
     for (int ck = 0; ck < kNBUF - 1; ++ck) {
@@ -476,7 +494,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
     if (A.mode == 1) break;
     pz = rows_block_sum(pz, red);
     if (threadIdx.x == 0) part0[b] = pz;
-    grid.sync();
+    rows_grid_sync(A.bar, bar_phase, nblk);
     rstamp(A, sb + 6);
     const double alpha = rr / rows_grid_total(part0, nblk, red);
     if (!isfinite(alpha)) {
@@ -511,7 +529,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
     }
     s2 = rows_block_sum(s2, red);
     if (threadIdx.x == 0) part1[b] = s2;
-    grid.sync();
+    rows_grid_sync(A.bar, bar_phase, nblk);
     rstamp(A, sb + 7);
     const double rr_new = rows_grid_total(part1, nblk, red);
     beta = rr_new / rr;
@@ -622,6 +640,10 @@ cudaError_t launch_cg_rows(const Modes& m, const double* pi, const double* dscal
   a.x = x;
   a.S = S;
   a.part = part;
+  // the last 16 doubles of the partial-sum workspace hold the grid-barrier counter
+  a.bar = reinterpret_cast<unsigned int*>(part + 2 * (size_t)grid);
+  cudaError_t ez = cudaMemsetAsync(a.bar, 0, 8, st);
+  if (ez != cudaSuccess) return ez;
   a.st = st_dev;
   a.mode = mode;
   a.tstamp = cg_debug_tstamp();
