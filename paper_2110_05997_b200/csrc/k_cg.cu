@@ -803,4 +803,8 @@ extern "C" void tf_cg_debug_dump(void) {
     for (int k = 1; k < 8; ++k) printf(" %.2f", (b[k] - b[k - 1]) * 1e-3);
     printf(" us; next start %.2f\n", (b[8] - b[7]) * 1e-3);
   }
+  if (h[59] > h[56] && h[56])
+    printf("prologue: operands %.2f us, W -> tensor memory %.2f us, rhs + first barrier %.2f us; first iteration "
+           "starts %.2f us after it\n", (h[57] - h[56]) * 1e-3, (h[58] - h[57]) * 1e-3, (h[59] - h[58]) * 1e-3,
+           (h[0] - h[59]) * 1e-3);
 }

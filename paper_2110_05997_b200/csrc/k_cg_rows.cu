@@ -1,9 +1,10 @@
 // Row-owned persistent CG (rows a8/a9: Thm Hv; Alg. CG-dGN).
 //
 // One cooperative launch runs the whole CG. Block b owns a contiguous range of <= 8*mtb rows of ONE mode l
-// (blocks per mode in proportion to the mode sizes). For the whole solve it keeps in shared memory the rows of
-// W_l and of the search direction p ([column][row], pitch 8 mtb + 4 = 4 or 12 mod 16: conflict-free DMMA
-// fragments in both contractions) and the constant Pi~_l = D_l Pi^(l) D_l ([column][k], pitch R8 + 4); every
+// (blocks per mode in proportion to the mode sizes). For the whole solve it keeps the rows of W_l in tensor memory
+// (tcgen05.st once, as the DMMA fragments of both contractions), and in shared memory the rows of the search
+// direction p ([column][row], pitch 8 mtb + 4 = 4 or 12 mod 16: conflict-free DMMA fragments in both contractions)
+// and the constant Pi~_l = D_l Pi^(l) D_l ([column][k], pitch R8 + 4); every
 // thread keeps its entries of r in registers (x: global, updated in place) (the positions of its output tiles of the apply). No vector
 // travels through global memory inside the loop: per iteration the global traffic is the Gram partial of each
 // block (R^2 doubles), the reduced S~ matrices and their streamed chunks. Four grid-wide steps per iteration:
@@ -12,8 +13,9 @@
 //   S  G_l = D_l sum_b P_b (fixed order, one lane per mode and entry, all loads in flight) and
 //      S~_l = (sum_{l' != l} Pi^(l,l') * G_l') D_l                                     (Thm Hv's S_l, scaled)
 //   Y  z = p Pi~_l + W S~_l + lambda_c D_c^2 p: the Thm-Hv apply with the Jacobi scaling folded into the
-//      operands (z = D (V Pi + W S + lambda V), V = p D); p Pi~ runs from shared memory
-//      while the S~ chunks stream in through a cp.async ring; z stays in registers; partial <p, z>
+//      operands (z = D (V Pi + W S + lambda V), V = p D); the second half of p Pi~ runs
+//      from shared memory while all of S~_l is staged by cp.async; W's fragments come from tensor memory;
+//      z stays in registers; partial <p, z>
 //   U  alpha = ||r||^2 / <p, z>; r -= alpha z; x += alpha p (registers); partial ||r||^2 -> beta
 // Scalars are recomputed by every block from the per-block partials in the same fixed order (deterministic,
 // no host round trip). Mode 1 (single matvec y = (J^T J + lambda D) v) runs G, S and Y once.
@@ -32,9 +34,6 @@ unsigned long long* cg_debug_tstamp();
 
 constexpr int kRThreads = 256;
 constexpr int kRMaxMT = 6;        // m-tiles (8 rows) per block at most
-constexpr int kKC = 16;           // k-rows of S~ per streamed chunk
-constexpr int kLDK = kKC + 4;     // chunk pitch per column (4 mod 16: conflict-free B fragments)
-constexpr int kNBUF = 4;          // cp.async ring depth
 constexpr int kSBatch = 16;       // Gram partials loaded at once per lane in stage S
 constexpr int kRedSlots = 64;
 
@@ -62,12 +61,18 @@ struct RowsArgs {
 __host__ __device__ constexpr int rows_ldr(int mtb) { return 8 * mtb + 4; }
 __host__ __device__ constexpr int rows_ldpi(int NT) { return 8 * NT + 4; }
 __host__ __device__ constexpr size_t rows_smem_doubles(int NT, int mtb) {
-  return (size_t)2 * (8 * NT) * rows_ldr(mtb) + (size_t)(8 * NT) * rows_ldpi(NT) + (size_t)kNBUF * (8 * NT) * kLDK +
-         (size_t)2 * (8 * NT) + kRedSlots;
+  // p rows [R8][LDR], Pi~ and S~ [R8][LDPI] (S~ doubles as the staging buffer of the W rows in the prologue),
+  // D, lambda D^2, reduction scratch; W itself lives in tensor memory
+  return (size_t)(8 * NT) * rows_ldr(mtb) + (size_t)(8 * NT) * rows_ldpi(NT) +
+         (size_t)(8 * NT) * (rows_ldpi(NT) > rows_ldr(mtb) ? rows_ldpi(NT) : rows_ldr(mtb)) + (size_t)2 * (8 * NT) +
+         kRedSlots;
 }
+// tensor-memory columns per lane quadrant: the Gram's B fragments W[4s+q][8j+g] (2 mtb k-steps x NT doubles) and the
+// apply's A fragments W[8 mt + g][4s+q] (MG m-tiles x R8/4 k-steps), 2 columns per double
+__host__ __device__ constexpr int rows_tmem_cols(int NT, int mtb, int MG) { return 2 * (2 * mtb * NT + MG * 2 * NT); }
 
 __device__ __forceinline__ void rstamp(const RowsArgs& A, int slot) {
-  if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && slot < 64) {
+  if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && slot < 48) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     A.tstamp[slot] = t;
@@ -89,6 +94,15 @@ __device__ __forceinline__ void rows_grid_sync(unsigned int* bar, unsigned int& 
     } while (v < target);
   }
   __syncthreads();
+}
+
+// prologue stamps (slots 56..59: entry, operands staged, W parked in tensor memory, first barrier passed)
+__device__ __forceinline__ void pstamp(const RowsArgs& A, int k) {
+  if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    A.tstamp[56 + k] = t;
+  }
 }
 
 __device__ __forceinline__ void cpa8(double* dst, const double* src, bool valid) {
@@ -135,26 +149,6 @@ __device__ __forceinline__ double rows_block_sum(double v, double* red) {
   return t;
 }
 
-// One S~ chunk: rows k0 .. k0 + kKC of the R x R column-major source, all R8 columns, into
-// buf[c][kk] (pitch kLDK); zero beyond R.
-__device__ __forceinline__ void issue_chunk(const double* src, int R, int R8, int k0, double* buf, bool pair) {
-  if (pair) {   // 16-byte copies (R even and src 16-byte aligned)
-    for (int idx = threadIdx.x; idx < R8 * (kKC / 2); idx += kRThreads) {
-      const int c = idx / (kKC / 2), kk = 2 * (idx % (kKC / 2));
-      const int k = k0 + kk;
-      const int valid = c < R ? (k + 1 < R ? 16 : (k < R ? 8 : 0)) : 0;
-      cpa16(buf + c * kLDK + kk, valid ? src + k + (int64_t)R * c : src, valid);
-    }
-  } else {
-    for (int idx = threadIdx.x; idx < R8 * kKC; idx += kRThreads) {
-      const int c = idx / kKC, kk = idx % kKC;
-      const int k = k0 + kk;
-      const bool ok = c < R && k < R;
-      cpa8(buf + c * kLDK + kk, ok ? src + k + (int64_t)R * c : src, ok);
-    }
-  }
-}
-
 // One k-step of the apply for a warp's tiles: m-tile wsub (and wsub + 4 when MGT = 2 and it exists) times the NJ
 // column tiles J0 .. J0 + NJ - 1. A fragments from [k][row] rows (pitch ldr), B from [column][k] operands (pitch
 // ldb). Every DMMA of the common path is unconditional (no per-instruction predicate, no warp re-convergence).
@@ -174,6 +168,39 @@ __device__ __forceinline__ void apply_kstep(double (&acc)[MGT][NH][2], const dou
   }
 }
 
+// The same with the A fragments given (tensor memory).
+template <int NJ, int J0, int MGT, int NH>
+__device__ __forceinline__ void apply_kstep_v(double (&acc)[MGT][NH][2], double fa0, double fa1, const double* bops,
+                                              int ldb, int kb, int g, bool second) {
+  double fb[NJ > 0 ? NJ : 1];
+#pragma unroll
+  for (int jj = 0; jj < NJ; ++jj) fb[jj] = bops[(8 * (J0 + jj) + g) * ldb + kb];
+#pragma unroll
+  for (int jj = 0; jj < NJ; ++jj) dmma(acc[0][jj], fa0, fb[jj]);
+  if (MGT > 1 && second) {
+#pragma unroll
+    for (int jj = 0; jj < NJ; ++jj) dmma(acc[MGT - 1][jj], fa1, fb[jj]);
+  }
+}
+
+// All of S~_l (R x R column-major) into sS[c][k] (pitch ldpi), zero for k, c >= R; cp.async, one commit group.
+__device__ __forceinline__ void stage_S(const double* src, int R, int R8, int ldpi, double* sS, bool pair) {
+  if (pair) {
+    for (int idx = threadIdx.x; idx < R8 * (R8 / 2); idx += kRThreads) {
+      const int c = idx / (R8 / 2), k = 2 * (idx % (R8 / 2));
+      const int valid = c < R ? (k + 1 < R ? 16 : (k < R ? 8 : 0)) : 0;
+      cpa16(sS + c * ldpi + k, valid ? src + k + (int64_t)R * c : src, valid);
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < R8 * R8; idx += kRThreads) {
+      const int c = idx / R8, k = idx % R8;
+      const bool ok = c < R && k < R;
+      cpa8(sS + c * ldpi + k, ok ? src + k + (int64_t)R * c : src, ok);
+    }
+  }
+  cpa_commit();
+}
+
 template <int NT, int MGT>
 __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
   unsigned int bar_phase = 0;
@@ -184,7 +211,6 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
   constexpr int GBASE = (NT / 4) * 4;                   // Gram i-tiles handled as full rows of tiles
   constexpr int GLO = ((NT - GBASE) * NT + 7) / 8;       // leftover Gram tiles per warp at most
   constexpr int LDPI = rows_ldpi(NT);
-  constexpr int NCH = (R8 + kKC - 1) / kKC;              // S~ chunks
   const Modes& m = A.m;
   const int R = (int)m.R;
   const int64_t RR = (int64_t)R * R;
@@ -203,13 +229,14 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
   const int MTb = (nr + 7) / 8;
   const double* Dl = A.dscale ? A.dscale + l * R : nullptr;
 
-  double* sW = rsm;
-  double* sP = sW + R8 * LDR;
+  double* sP = rsm;
   double* sPi = sP + R8 * LDR;
-  double* ring = sPi + R8 * LDPI;
-  double* sD = ring + kNBUF * R8 * kLDK;   // D_c (Jacobi scale of this mode; 1 without)
+  double* sS = sPi + R8 * LDPI;            // S~ [c][k]; in the prologue the staging buffer of the W rows
+  double* sW = sS;
+  double* sD = sS + R8 * max(LDPI, LDR);   // D_c (Jacobi scale of this mode; 1 without)
   double* sLD = sD + R8;                   // lambda_c D_c^2 (lambda_c = lambda damp_c)
   double* red = sLD + R8;
+  __shared__ uint32_t tmem_base_s;
 
   // apply tiles of this warp: sub-partition s = warp % 4 owns m-tiles s and s + 4 (every SMSP the same share
   // of the critical 8-row tiles), the two warps of a sub-partition split the NT column tiles in halves (NH, NT - NH);
@@ -224,6 +251,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
 
   // ---- prologue (every copy in flight at once): W rows, p = 0 (or v), Pi^(l), D; then Pi~ = D Pi^(l) D in place;
   // r = D rhs in registers, x = 0
+  pstamp(A, 0);
   const double* Wl = m.W[l];
   for (int idx = threadIdx.x; idx < R8 * LDR; idx += kRThreads) {
     const int c = idx / LDR, a = idx % LDR;
@@ -255,7 +283,56 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
       if (c < R8 && k < R8) sPi[idx] *= sD[k] * sD[c];
     }
   }
+  // W in tensor memory (512 columns; a warp touches its lane quadrant warp % 4): per lane, the Gram's B fragments
+  // W[4s + q][8j + g] at columns 2 (s NT + j) and, after them, the apply's A fragments W[8 (wsub + 4 mi) + g][4s + q]
+  // at 2 (KG NT + mi R8/4 + s) — both are the same for the two warps of a quadrant, so warps 0-3 write them once
+  pstamp(A, 1);
+  const int KG = 2 * A.mtb;                // Gram k-steps at most (rows padded to 8 mtb)
+  if (warp == 0) tmem_alloc(&tmem_base_s, 512);
+  tmem_fence_before_sync();
   __syncthreads();
+  tmem_fence_after_sync();
+  const uint32_t ta = tmem_base_s + ((uint32_t)(32 * wsub) << 16);
+  const uint32_t taA = ta + 2 * KG * NT;
+  if (warp < 4) {
+#pragma unroll 1
+    for (int s = 0; s < KG; ++s) {
+#pragma unroll
+      for (int j0 = 0; j0 < NT; j0 += 4) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = (j0 + u < NT) ? sW[(8 * (j0 + u) + g) * LDR + 4 * s + q] : 0.0;
+        if (j0 + 4 <= NT) tmem_st4(ta + 2 * (s * NT + j0), v);
+        else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (j0 + u < NT) tmem_st1(ta + 2 * (s * NT + j0 + u), v[u]);
+        }
+      }
+    }
+#pragma unroll 1
+    for (int mi = 0; mi < MG; ++mi) {
+      const int mt = wsub + 4 * mi;
+#pragma unroll 1
+      for (int s = 0; s < R8 / 4; s += 4) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          v[u] = (mt < A.mtb && s + u < R8 / 4) ? sW[(4 * (s + u) + q) * LDR + 8 * mt + g] : 0.0;
+        if (s + 4 <= R8 / 4) tmem_st4(taA + 2 * (mi * (R8 / 4) + s), v);
+        else {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (s + u < R8 / 4) tmem_st1(taA + 2 * (mi * (R8 / 4) + s + u), v[u]);
+        }
+      }
+    }
+    tmem_wait_st();
+  }
+  tmem_fence_before_sync();
+  __syncthreads();
+  tmem_fence_after_sync();
+  pstamp(A, 2);
   double rreg[MG][NH][2];
   double s0 = 0.0;
 #pragma unroll
@@ -293,6 +370,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
     if (threadIdx.x == 0) part1[b] = s0;
     rows_grid_sync(A.bar, bar_phase, nblk);
     rr = rows_grid_total(part1, nblk, red);
+    pstamp(A, 3);
   } else {
     __syncthreads();
   }
@@ -330,12 +408,14 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
         double gf[NT][2];
 #pragma unroll
         for (int j = 0; j < NT; ++j) gf[j][0] = gf[j][1] = 0.0;
-#pragma unroll 2
         for (int s = 0; s < ks; ++s) {
           const int a = 4 * s + q;
           const double fa = sP[(8 * i + g) * LDR + a];
+          double fb[NT];
+          tmem_ld_doubles<NT>(ta + 2 * s * NT, fb);
+          tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < NT; ++j) dmma(gf[j], fa, sW[(8 * j + g) * LDR + a]);
+          for (int j = 0; j < NT; ++j) dmma(gf[j], fa, fb[j]);
         }
         // the partial is stored transposed (entry (r, c) at c + R r): a lane's two columns are adjacent
         const int r = 8 * i + g;
@@ -361,8 +441,10 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
         const int i = GBASE + t / NT, j = t % NT;
         double gl[2] = {0.0, 0.0};
         for (int s = 0; s < ks; ++s) {
-          const int a = 4 * s + q;
-          dmma(gl, sP[(8 * i + g) * LDR + a], sW[(8 * j + g) * LDR + a]);
+          double fb;
+          tmem_ld_d1(ta + 2 * (s * NT + j), &fb);
+          tmem_wait_ld();
+          dmma(gl, sP[(8 * i + g) * LDR + 4 * s + q], fb);
         }
         const int r = 8 * i + g;
 #pragma unroll
@@ -451,27 +533,23 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
     rstamp(A, sb + 3);
     rows_grid_sync(A.bar, bar_phase, nblk);
     rstamp(A, sb + 4);
-    // ---- Y: S~ chunks stream in while the second half of p Pi~ runs, then W S~ from the ring
-    for (int ck = 0; ck < kNBUF - 1; ++ck) {
-      if (ck < NCH) issue_chunk(Sl, R, R8, ck * kKC, ring + ck * R8 * kLDK, pairS);
-      cpa_commit();
-    }
+    // ---- Y: all of S~_l is staged while the second half of p Pi~ runs, then W S~ with W from tensor memory
+    stage_S(Sl, R, R8, LDPI, sS, pairS);
     pi_steps(KS1, R8 / 4);
-    for (int ck = 0; ck < NCH; ++ck) {
-      cpa_wait<kNBUF - 2>();
-      __syncthreads();
-      {
-        const int nx = ck + kNBUF - 1;
-        if (nx < NCH) issue_chunk(Sl, R, R8, nx * kKC, ring + (nx % kNBUF) * R8 * kLDK, pairS);
-        cpa_commit();
-      }
-      const int k0 = ck * kKC;
-      const double* buf = ring + (ck % kNBUF) * R8 * kLDK;
-      const int nks = min(kKC, R8 - k0) / 4;
-#pragma unroll 4
-      for (int s = 0; s < nks; ++s) {
-        if (whalf == 0) apply_kstep<NH, 0, MG, NH>(acc, sW, LDR, buf, kLDK, k0 + 4 * s + q, 4 * s + q, wsub, g, second);
-        else apply_kstep<NT - NH, NH, MG, NH>(acc, sW, LDR, buf, kLDK, k0 + 4 * s + q, 4 * s + q, wsub, g, second);
+    cpa_wait<0>();
+    __syncthreads();
+#pragma unroll 1
+    for (int hk = 0; hk < 2; ++hk) {   // the R8/4 = 2 NT k-steps in two batches of NT A fragments
+      double wa[MG][NT];
+      tmem_ld_doubles<NT>(taA + 2 * hk * NT, wa[0]);
+      if (MG > 1 && second) tmem_ld_doubles<NT>(taA + 2 * (R8 / 4 + hk * NT), wa[MG - 1]);
+      tmem_wait_ld();
+#pragma unroll
+      for (int u = 0; u < NT; ++u) {
+        const int kb = 4 * (hk * NT + u) + q;
+        const double fa1 = MG > 1 ? wa[MG - 1][u] : 0.0;
+        if (whalf == 0) apply_kstep_v<NH, 0, MG, NH>(acc, wa[0][u], fa1, sS, LDPI, kb, g, second);
+        else apply_kstep_v<NT - NH, NH, MG, NH>(acc, wa[0][u], fa1, sS, LDPI, kb, g, second);
       }
     }
     rstamp(A, sb + 5);
@@ -542,6 +620,9 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
     if (rr_new < A.tol) break;
   }
   cpa_wait<0>();
+  tmem_fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem_base_s, 512);
   if (A.mode == 1) return;
   // x in w-coordinates: x = D x_hat
   if (Dl) {
@@ -602,7 +683,9 @@ static int rows_plan(const Modes& m, int grid, int bstart[4]) {
 template <int NT>
 static cudaError_t launch_rows_nt(RowsArgs& a, cudaStream_t st) {
   auto kern = a.mtb > 4 ? k_cg_rows<NT, 2> : k_cg_rows<NT, 1>;
-  const size_t smem = 8 * rows_smem_doubles(NT, a.mtb);
+  // at least 120 KB of shared memory: one block per SM, since every block allocates all 512 tensor-memory columns
+  // (a second block on the SM would wait in tcgen05.alloc while the first waits for it at a grid barrier)
+  const size_t smem = std::max<size_t>(8 * rows_smem_doubles(NT, a.mtb), 120 * 1024);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
@@ -616,11 +699,13 @@ static cudaError_t launch_rows_nt(RowsArgs& a, cudaStream_t st) {
 // Plans the row-owned kernel for these modes on `grid` blocks; returns false (nothing launched) when a block
 // would own more than 8 kRMaxMT rows, shared memory does not fit, or the scratch buffers are too small.
 bool cg_rows_fits(const Modes& m, int grid, size_t gram_partial_doubles) {
+  if (grid < 3) return false;   // one block per mode at least (a smaller cap goes to the grid kernel)
   int bs[4];
   const int mtb = rows_plan(m, grid, bs);
   const int NT = (int)((m.R + 7) / 8);
   if (mtb < 1 || mtb > kRMaxMT || NT > 16) return false;
   if (8 * rows_smem_doubles(NT, mtb) > 227 * 1024) return false;
+  if (rows_tmem_cols(NT, mtb, mtb > 4 ? 2 : 1) > 512) return false;
   return (size_t)bs[3] * m.R * m.R <= gram_partial_doubles;
 }
 

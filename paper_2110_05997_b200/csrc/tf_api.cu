@@ -119,7 +119,17 @@ Modes make_modes(const tf_dims& d, const double* w) {
 // Choose the number of k-chunks per (i-tile, j-tile): minimise waves * (slices per chunk + overhead),
 // where one CTA is resident per SM (the fused kernel uses ~190 KB of shared memory).
 int choose_ksplit(int64_t tiles, int64_t K, int nsm) {
-  const double overhead = 2.0;  // prologue + partial write-out, in slice-iterations
+  // development overrides: TF_EVAL_KSPLIT (fixed split) and TF_EVAL_KSPLIT_OVH (the overhead constant)
+  static const int force = [] {
+    const char* e = getenv("TF_EVAL_KSPLIT");
+    return e ? atoi(e) : 0;
+  }();
+  static const double ovh = [] {
+    const char* e = getenv("TF_EVAL_KSPLIT_OVH");
+    return e ? atof(e) : 2.0;
+  }();
+  if (force > 0) return (int)std::min<int64_t>(force, K);
+  const double overhead = ovh;  // prologue + partial write-out, in slice-iterations
   int best = 1;
   double best_cost = 1e300;
   const int64_t kmax = std::min<int64_t>(K, 4096);

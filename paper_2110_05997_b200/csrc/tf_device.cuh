@@ -95,6 +95,12 @@ __device__ __forceinline__ void tmem_st4(uint32_t taddr, const double (&v)[4]) {
                "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
                : "memory");
 }
+// 1 double (2 x 32-bit columns) per thread
+__device__ __forceinline__ void tmem_st1(uint32_t taddr, double v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(taddr), "r"(__double2loint(v)),
+               "r"(__double2hiint(v))
+               : "memory");
+}
 __device__ __forceinline__ void tmem_ld4(uint32_t taddr, double (&v)[4]) {
   uint32_t r[8];
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];\n"
