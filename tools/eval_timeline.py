@@ -16,4 +16,4 @@ for _ in range(2):
 torch.cuda.synchronize()
 ctypes.CDLL(tf.LIB_PATH).tf_eval_timeline_dump()
 lib = ctypes.CDLL(tf.LIB_PATH)
-lib.tf_eval_cta_dump(4096)
+lib.tf_eval_cta_dump(int(sys.argv[2]) if len(sys.argv) > 2 else 4096)
