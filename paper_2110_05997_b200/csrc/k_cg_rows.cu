@@ -2,21 +2,21 @@
 //
 // One cooperative launch runs the whole CG. Block b owns a contiguous range of <= 8*mtb rows of ONE mode l
 // (blocks per mode in proportion to the mode sizes). For the whole solve it keeps the rows of W_l in tensor memory
-// (tcgen05.st once, as the DMMA fragments of both contractions), and in shared memory the rows of the search
-// direction p ([column][row], pitch 8 mtb + 4 = 4 or 12 mod 16: conflict-free DMMA fragments in both contractions)
-// and the constant Pi~_l = D_l Pi^(l) D_l ([column][k], pitch R8 + 4); every
-// thread keeps its entries of r in registers (x: global, updated in place) (the positions of its output tiles of the apply). No vector
-// travels through global memory inside the loop: per iteration the global traffic is the Gram partial of each
-// block (R^2 doubles), the reduced S~ matrices and their streamed chunks. Four grid-wide steps per iteration:
+// (tcgen05.st once, as the DMMA fragments of both contractions); in shared memory the rows of the search direction
+// p ([column][row], pitch 8 mtb + 4 = 4 or 12 mod 16: conflict-free DMMA fragments in both contractions), the
+// constant Pi~_l = D_l Pi^(l) D_l and, per iteration, S~_l ([column][k], pitch R8 + 4); every thread keeps its
+// entries of r in registers (the positions of its output tiles of the apply) and updates its entries of x in
+// place in global memory. Apart from x, no vector travels through global memory inside the loop: per iteration
+// the global traffic is the Gram partial of each block (R^2 doubles) and the reduced S~. Four grid-wide steps:
 //   G  p <- r + beta p (registers -> shared); Gram partial P_b = p_rows^T W_rows (DMMA, inner dim = rows),
 //      stored transposed (16-byte stores of a lane's two adjacent columns)
-//   S  G_l = D_l sum_b P_b (fixed order, one lane per mode and entry, all loads in flight) and
-//      S~_l = (sum_{l' != l} Pi^(l,l') * G_l') D_l                                     (Thm Hv's S_l, scaled)
+//   S  G_l = D_l sum_b P_b (fixed order, one lane per mode and entry, the loads in flight while the first half
+//      of p Pi~ runs) and S~_l = (sum_{l' != l} Pi^(l,l') * G_l') D_l                 (Thm Hv's S_l, scaled)
 //   Y  z = p Pi~_l + W S~_l + lambda_c D_c^2 p: the Thm-Hv apply with the Jacobi scaling folded into the
 //      operands (z = D (V Pi + W S + lambda V), V = p D); the second half of p Pi~ runs
 //      from shared memory while all of S~_l is staged by cp.async; W's fragments come from tensor memory;
 //      z stays in registers; partial <p, z>
-//   U  alpha = ||r||^2 / <p, z>; r -= alpha z; x += alpha p (registers); partial ||r||^2 -> beta
+//   U  alpha = ||r||^2 / <p, z>; r -= alpha z (registers); x += alpha p (global); partial ||r||^2 -> beta
 // Scalars are recomputed by every block from the per-block partials in the same fixed order (deterministic,
 // no host round trip). Mode 1 (single matvec y = (J^T J + lambda D) v) runs G, S and Y once.
 #include <cooperative_groups.h>
@@ -34,7 +34,7 @@ unsigned long long* cg_debug_tstamp();
 
 constexpr int kRThreads = 256;
 constexpr int kRMaxMT = 6;        // m-tiles (8 rows) per block at most
-constexpr int kSBatch = 16;       // Gram partials loaded at once per lane in stage S
+constexpr int kSBatch = 32;       // Gram partials loaded at once per lane in stage S
 constexpr int kRedSlots = 64;
 
 struct RowsArgs {
