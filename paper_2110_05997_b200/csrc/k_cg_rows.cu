@@ -454,13 +454,8 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
         }
       }
     }
-    rstamp(A, sb + 1);
-    rows_grid_sync(A.bar, bar_phase, nblk);
-    rstamp(A, sb + 2);
-    // ---- S, overlapped with the first half of p Pi~ (which does not depend on S): one lane per (entry, mode)
-    // issues the loads of that mode's partials (block order, all in flight), the DMMAs of p Pi~ run while they
-    // are in flight, then the lane sums them in block order; the three lanes of an entry exchange their sums and
-    // each writes its mode's S~
+    // p Pi~ does not depend on S: a third of it runs while this block's partial stores drain (before the grid
+    // barrier), a third while stage S's loads are in flight and the rest while S~ is staged
 #pragma unroll
     for (int mi = 0; mi < MG; ++mi)
 #pragma unroll
@@ -473,7 +468,14 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
         else apply_kstep<NT - NH, NH, MG, NH>(acc, sP, LDR, sPi, LDPI, 4 * s + q, 4 * s + q, wsub, g, second);
       }
     };
-    constexpr int KS1 = (R8 / 4) / 2;
+    constexpr int KS0 = (R8 / 4) / 3, KS1 = 2 * (R8 / 4) / 3;
+    pi_steps(0, KS0);
+    rstamp(A, sb + 1);
+    rows_grid_sync(A.bar, bar_phase, nblk);
+    rstamp(A, sb + 2);
+    // ---- S: one lane per (entry, mode) issues the loads of that mode's partials (block order, all in flight),
+    // the DMMAs of p Pi~ run while they are in flight, then the lane sums them in block order; the three lanes
+    // of an entry exchange their sums and each writes its mode's S~
     {
       const int gw = blockIdx.x * (kRThreads / 32) + warp, nw = nblk * (kRThreads / 32);
       const int ll = lane % 3;
@@ -505,7 +507,7 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
           p13 = A.pi[4 * RR + rc];
           p23 = A.pi[5 * RR + rc];
         }
-        if (first) pi_steps(0, KS1);   // the loads above are in flight meanwhile
+        if (first) pi_steps(KS0, KS1);   // the loads above are in flight meanwhile
         first = false;
         double gsum = 0.0;
 #pragma unroll
