@@ -459,6 +459,10 @@ def run_ours(args):
         v, secs, sample = oracle_shard_sample(cfg, Ts, wn, k_sl, threads)
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample, "seconds": secs,
                "host": host_cpu()}
+        # the same oracle on ONE host thread (SURVEY.md §8d asks for both runs): a smaller K-shard, same CG
+        ks1 = max(1, k_sl // max(1, 2 * threads))
+        v1, secs1, sample1 = oracle_shard_sample(cfg, P.T[:ks1].cpu().numpy().reshape(-1), wn, ks1, 1)
+        cpu["single_thread"] = {"value": v1, "unit": UNIT, "cores": 1, "sample": sample1, "seconds": secs1}
 
     # compression stage (NEXT #3), measured once beside the step on the resident T (not part of `value`)
     stages = None
