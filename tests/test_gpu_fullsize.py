@@ -5,13 +5,16 @@
   (F and dF/dA, dF/dB are sums over frontal slices, dF/dC row k depends on slice k only: PAPER.md:1844-1851,
   1801-1805), which is exactly the definition's sum split in k.
 * Alg. CG-dGN in the launch configuration the bench times: c3 (n = 30 000, 10 iterations,
-  lambda = 1e-3, Jacobi on/off, the collinear true point and a random point) and c5 (n = 360 000, 20
-  iterations, the grid kernel with several apply items per block). Per iteration i: the GPU's x^(i) against
+  lambda = 1e-3, Jacobi on/off, the collinear true point and a random point; once more on a 37-block grid) and c5
+  (n = 360 000, 20 iterations, the row-owned persistent kernel on the full grid). Per iteration i: the GPU's x^(i)
+  against
   the oracle's (iterate drift, reported), ||r^(i)||^2, and the GN matvec (Thm Hv) of the
   search direction the oracle's CG formed at that iteration, at 1e-10 per block and per element.
 * The cancellation guard of the Pi form (reading R31) just above its thresholds: 2F/||T||^2 in {1.05e-3, 2e-3,
   1e-2} and ||grad F||/||W Pi|| = 1.1e-3, forced Pi form, against the oracle at 1e-10.
 * Bitwise determinism of both forms at c3 full size.
+* The K-sharded evaluation at c5 (2 and 8 shards): the shards' partial [grad | F] summed in rank order (the
+  all-reduce) against the single-device result (1e-12) and the oracle (1e-10 per block and element).
 
 Set TF_PARITY_REPORT=<dir> to write the per-iteration drift curves and error ratios as JSON.
 """
@@ -291,3 +294,33 @@ def test_c5_cg_per_iteration(ctx, c5):
     P, fr, gr = c5
     c = P.cfg
     _cg_parity(ctx, "c5/random/jacobi=0", to_np(P.w("random")), -gr, c.lam, 20, False, c.I, c.J, c.K, c.R, 1e-10)
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_c5_k_shards_sum_to_full_and_oracle(ctx, c5, world):
+    """What one rank of an N-GPU run computes at the benchmark's size: the partial [grad | F] of each
+    balanced K-shard (k_begin, K_total; dF/dC rows outside the shard exactly zero), summed over the N shards in rank
+    order — the all-reduce — equals the single-device evaluation to 1e-12 (only the reduction tree differs) and the
+    oracle to 1e-10 per block and element."""
+    P, fr, gr = c5
+    c = P.cfg
+    I, J, K, R = c.I, c.J, c.K, c.R
+    w = P.w("random")
+    f1, g1 = ctx.tf_cpd_eval(tf.Dims(I, J, K, R), P.T, w)
+    f1, g1 = float(f1.item()), to_np(g1)
+    fs, gs = 0.0, np.zeros_like(g1)
+    for rank in range(world):
+        k0, k1 = synth.shard_range(K, rank, world)
+        f, g = ctx.tf_cpd_eval(tf.Dims(I, J, k1 - k0, R, K_total=K, k_begin=k0), P.T[k0:k1], w)
+        g = to_np(g)
+        gC = g[(I + J) * R:].reshape(R, K)
+        assert not gC[:, :k0].any() and not gC[:, k1:].any()
+        fs += float(f.item())
+        gs += g
+    assert abs(fs - f1) <= 1e-12 * abs(f1)
+    assert rel_err(gs, g1) <= 1e-12
+    okf, ef, bf = within([fs], [fr])
+    assert okf, (ef, bf)
+    per = check_elementwise(gs, gr, w_blocks(I, J, K, R), block_floors(to_np(w), I, J, K, R))
+    _report(f"shards/c5/{world}", {"f_rel_vs_single": abs(fs - f1) / abs(f1), "grad_rel_vs_single": rel_err(gs, g1),
+                                   "grad_rel_vs_oracle": rel_err(gs, gr), "blocks": per})
