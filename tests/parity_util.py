@@ -104,3 +104,51 @@ def check_elementwise(got, ref, blocks, floors=None, tol: float = TOL):
         assert blk_err <= blk_bound, (name, "block", blk_err, blk_bound)
         assert np.all(d <= el_bound), (name, "element", worst, float(g[worst]), float(r[worst]), float(el_bound[worst]))
     return out
+
+
+def hv_abs_terms(w, v, lam, I, J, K, R):
+    """Per element, the sum of the absolute values of every term of (J^T J + lam I) v evaluated by Thm Hv
+    (PAPER.md:2352-2370): |V_l| |Pi^(l)| + |W_l| |S_l| + lam |V_l| with |Pi| and |S| built from the absolute Grams
+    |W|^T |W| and |V|^T |W|. Any fp64 evaluation order of the matvec (Grams over n_l rows, then 2R-term sums)
+    has a forward error of at most (n_max + 2R + 2) u times this per element (the standard dot-product bound), which
+    is the element floor where the result cancels (a Jacobi-scaled CG direction at c5: terms ~1e3, entries ~1e-4)."""
+    w = np.asarray(w, dtype=np.float64).reshape(-1)
+    v = np.asarray(v, dtype=np.float64).reshape(-1)
+    dims = (I, J, K)
+    offs = (0, I * R, (I + J) * R)
+    Wa = [np.abs(w[o:o + n * R].reshape(R, n).T) for o, n in zip(offs, dims)]
+    Va = [np.abs(v[o:o + n * R].reshape(R, n).T) for o, n in zip(offs, dims)]
+    ga = [X.T @ X for X in Wa]
+    gv = [Va[l].T @ Wa[l] for l in range(3)]
+    out = []
+    for l in range(3):
+        o1, o2 = [m for m in range(3) if m != l]
+        Pl = ga[o1] * ga[o2]
+        # Pi^(l,l') is the Gram of the remaining mode
+        Sl = ga[o2] * gv[o1] + ga[o1] * gv[o2]
+        out.append((Va[l] @ Pl + Wa[l] @ Sl + abs(lam) * Va[l]).T.reshape(-1))
+    return np.concatenate(out), max(dims) + 2 * R + 2
+
+
+def check_elementwise_floor(got, ref, blocks, elem_floor, tol: float = TOL):
+    """check_elementwise with a per-element floor array (e.g. the forward-error bound of hv_abs_terms) in place of
+    the per-block one: |Δ_e| ≤ tol·(|ref_e| + rms(ref_b)) + floor_e, and per block ‖Δ_b‖ ≤ tol‖ref_b‖ + ‖floor_b‖."""
+    got = np.asarray(got, dtype=np.float64).reshape(-1)
+    ref = np.asarray(ref, dtype=np.float64).reshape(-1)
+    fl = np.asarray(elem_floor, dtype=np.float64).reshape(-1)
+    out = {}
+    for name, sl in blocks:
+        g, r, f = got[sl], ref[sl], fl[sl]
+        if r.size == 0:
+            continue
+        d = np.abs(g - r)
+        nb = float(np.linalg.norm(r))
+        blk_bound = tol * nb + float(np.linalg.norm(f))
+        blk_err = float(np.linalg.norm(g - r))
+        el_bound = tol * (np.abs(r) + nb / math.sqrt(r.size)) + f
+        ratio = d / np.where(el_bound > 0, el_bound, np.inf)
+        worst = int(np.argmax(ratio))
+        out[name] = {"block_ratio": blk_err / blk_bound if blk_bound > 0 else 0.0, "elem_ratio": float(ratio[worst])}
+        assert blk_err <= blk_bound, (name, "block", blk_err, blk_bound)
+        assert np.all(d <= el_bound), (name, "element", worst, float(g[worst]), float(r[worst]), float(el_bound[worst]))
+    return out
