@@ -5,9 +5,10 @@
 // (tcgen05.st once, as the DMMA fragments of both contractions); in shared memory the rows of the search direction
 // p ([column][row], pitch 8 mtb + 4 = 4 or 12 mod 16: conflict-free DMMA fragments in both contractions), the
 // constant Pi~_l = D_l Pi^(l) D_l and, per iteration, S~_l ([column][k], pitch R8 + 4); every thread keeps its
-// entries of r in registers (the positions of its output tiles of the apply) and updates its entries of x in
-// place in global memory. Apart from x, no vector travels through global memory inside the loop: per iteration
-// the global traffic is the Gram partial of each block (R^2 doubles) and the reduced S~. Four grid-wide steps:
+// entries of r in registers (the positions of its output tiles of the apply) and its entries of x in tensor
+// memory (in global memory when a thread owns two m-tiles). No other vector travels through global memory inside
+// the loop: per iteration the global traffic is the Gram partial of each block (R^2 doubles) and the reduced S~.
+// Four grid-wide steps per iteration:
 //   G  p <- r + beta p (registers -> shared); Gram partial P_b = p_rows^T W_rows (DMMA, inner dim = rows),
 //      stored transposed (16-byte stores of a lane's two adjacent columns)
 //   S  G_l = D_l sum_b P_b (fixed order, one lane per mode and entry, the loads in flight while the first half
@@ -16,7 +17,7 @@
 //      operands (z = D (V Pi + W S + lambda V), V = p D); the second half of p Pi~ runs
 //      from shared memory while all of S~_l is staged by cp.async; W's fragments come from tensor memory;
 //      z stays in registers; partial <p, z>
-//   U  alpha = ||r||^2 / <p, z>; r -= alpha z (registers); x += alpha p (global); partial ||r||^2 -> beta
+//   U  alpha = ||r||^2 / <p, z>; r -= alpha z (registers); x += alpha p (tensor memory); partial ||r||^2 -> beta
 // Scalars are recomputed by every block from the per-block partials in the same fixed order (deterministic,
 // no host round trip). Mode 1 (single matvec y = (J^T J + lambda D) v) runs G, S and Y once.
 #include <cooperative_groups.h>
@@ -69,7 +70,9 @@ __host__ __device__ constexpr size_t rows_smem_doubles(int NT, int mtb) {
 }
 // tensor-memory columns per lane quadrant: the Gram's B fragments W[4s+q][8j+g] (2 mtb k-steps x NT doubles) and the
 // apply's A fragments W[8 mt + g][4s+q] (MG m-tiles x R8/4 k-steps), 2 columns per double
-__host__ __device__ constexpr int rows_tmem_cols(int NT, int mtb, int MG) { return 2 * (2 * mtb * NT + MG * 2 * NT); }
+__host__ __device__ constexpr int rows_tmem_cols(int NT, int mtb, int MG) {
+  return 2 * (2 * mtb * NT + MG * 2 * NT) + (MG == 1 ? 8 * ((NT + 1) / 2) : 0);   // + x (MG = 1)
+}
 
 __device__ __forceinline__ void rstamp(const RowsArgs& A, int slot) {
   if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && slot < 48) {
@@ -294,6 +297,10 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
   tmem_fence_after_sync();
   const uint32_t ta = tmem_base_s + ((uint32_t)(32 * wsub) << 16);
   const uint32_t taA = ta + 2 * KG * NT;
+  // MG = 1: this thread's entries of x (2 NH doubles) live in tensor memory too, after the A fragments, one
+  // region per column half (the two warps of a quadrant own different entries)
+  constexpr bool kXT = MG == 1;
+  const uint32_t taX = taA + 2 * MG * (R8 / 4) + whalf * 4 * NH;
   if (warp < 4) {
 #pragma unroll 1
     for (int s = 0; s < KG; ++s) {
@@ -353,14 +360,22 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
       }
     })
     // x = 0 (after the loads of rhs: no load waits behind a store)
-    TF_TILES({
-      const int row = 8 * mt + g;
+    if constexpr (kXT) {
+      double z0[2 * NH];
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int c = 8 * j + 2 * q + e;
-        if (row < nr && c < R) A.x[off + a0 + row + nl * c] = 0.0;
-      }
-    })
+      for (int i = 0; i < 2 * NH; ++i) z0[i] = 0.0;
+      tmem_st_doubles<2 * NH>(taX, z0);
+      tmem_wait_st();
+    } else {
+      TF_TILES({
+        const int row = 8 * mt + g;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = 8 * j + 2 * q + e;
+          if (row < nr && c < R) A.x[off + a0 + row + nl * c] = 0.0;
+        }
+      })
+    }
   }
   double* part0 = A.part;
   double* part1 = A.part + nblk;
@@ -583,7 +598,26 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
     }
     // ---- U: r -= alpha z, x += alpha p at this thread's positions; ||r||^2 (x: all loads first, then stores)
     double s2 = 0.0;
-    {
+    if constexpr (kXT) {   // x in tensor memory: load, update, store back
+      double xt[2 * NH];
+      tmem_ld_doubles<2 * NH>(taX, xt);
+      tmem_wait_ld();
+      TF_TILES({
+        const int row = 8 * mt + g;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int c = 8 * j + 2 * q + e;
+          if (row < nr && c < R) {
+            xt[2 * jj + e] = fma(alpha, sP[c * LDR + row], xt[2 * jj + e]);
+            const double rn = fma(-alpha, acc[mi][jj][e], rreg[mi][jj][e]);
+            rreg[mi][jj][e] = rn;
+            s2 = fma(rn, rn, s2);
+          }
+        }
+      })
+      tmem_st_doubles<2 * NH>(taX, xt);
+      tmem_wait_st();
+    } else {
       double xv[MG][NH][2];
       TF_TILES({
         const int row = 8 * mt + g;
@@ -622,12 +656,25 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
     if (rr_new < A.tol) break;
   }
   cpa_wait<0>();
+  if (kXT && A.mode == 0) {   // x in w-coordinates: x = D x_hat, from tensor memory
+    double xt[2 * NH];
+    tmem_ld_doubles<2 * NH>(taX, xt);
+    tmem_wait_ld();
+    TF_TILES({
+      const int row = 8 * mt + g;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = 8 * j + 2 * q + e;
+        if (row < nr && c < R) A.x[off + a0 + row + nl * c] = xt[2 * jj + e] * sD[c];
+      }
+    })
+  }
   tmem_fence_before_sync();
   __syncthreads();
   if (warp == 0) tmem_dealloc(tmem_base_s, 512);
   if (A.mode == 1) return;
   // x in w-coordinates: x = D x_hat
-  if (Dl) {
+  if (!kXT && Dl) {
     TF_TILES({
       const int row = 8 * mt + g;
 #pragma unroll

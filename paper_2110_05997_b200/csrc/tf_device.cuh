@@ -175,6 +175,18 @@ __device__ __forceinline__ void tmem_ld_doubles(uint32_t taddr, double* v) {
   if constexpr ((r8 & 1) != 0) tmem_ld_d1(taddr + 2 * (N - 1), v + N - 1);
 }
 
+// N consecutive doubles from v into 2N columns at taddr (chunks of 4, then single doubles)
+template <int N>
+__device__ __forceinline__ void tmem_st_doubles(uint32_t taddr, const double* v) {
+#pragma unroll
+  for (int i = 0; i + 4 <= N; i += 4) {
+    const double c[4] = {v[i], v[i + 1], v[i + 2], v[i + 3]};
+    tmem_st4(taddr + 2 * i, c);
+  }
+#pragma unroll
+  for (int i = (N / 4) * 4; i < N; ++i) tmem_st1(taddr + 2 * i, v[i]);
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
