@@ -56,6 +56,7 @@ struct RowsArgs {
   int mode;               // 0 CG, 1 single matvec
   int bstart[4];          // first block of each mode; bstart[3] = number of blocks
   int mtb;                // row capacity per block = 8 mtb
+  int xtmem;              // 1: x lives in tensor memory (the columns fit), else in global memory
   unsigned long long* tstamp;
 };
 
@@ -70,9 +71,9 @@ __host__ __device__ constexpr size_t rows_smem_doubles(int NT, int mtb) {
 }
 // tensor-memory columns per lane quadrant: the Gram's B fragments W[4s+q][8j+g] (2 mtb k-steps x NT doubles) and the
 // apply's A fragments W[8 mt + g][4s+q] (MG m-tiles x R8/4 k-steps), 2 columns per double
-__host__ __device__ constexpr int rows_tmem_cols(int NT, int mtb, int MG) {
-  return 2 * (2 * mtb * NT + MG * 2 * NT) + (MG == 1 ? 8 * ((NT + 1) / 2) : 0);   // + x (MG = 1)
-}
+__host__ __device__ constexpr int rows_tmem_cols(int NT, int mtb, int MG) { return 2 * (2 * mtb * NT + MG * 2 * NT); }
+// x in tensor memory as well: 2 MG NH doubles per thread, one region per column half
+__host__ __device__ constexpr int rows_tmem_x_cols(int NT, int MG) { return 8 * MG * ((NT + 1) / 2); }
 
 __device__ __forceinline__ void rstamp(const RowsArgs& A, int slot) {
   if (A.tstamp && blockIdx.x == 0 && threadIdx.x == 0 && slot < 48) {
@@ -297,10 +298,10 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
   tmem_fence_after_sync();
   const uint32_t ta = tmem_base_s + ((uint32_t)(32 * wsub) << 16);
   const uint32_t taA = ta + 2 * KG * NT;
-  // MG = 1: this thread's entries of x (2 NH doubles) live in tensor memory too, after the A fragments, one
-  // region per column half (the two warps of a quadrant own different entries)
-  constexpr bool kXT = MG == 1;
-  const uint32_t taX = taA + 2 * MG * (R8 / 4) + whalf * 4 * NH;
+  // when the columns fit, this thread's entries of x (2 MG NH doubles) live in tensor memory too, after the A
+  // fragments, one region per column half (the two warps of a quadrant own different entries)
+  const bool kXT = A.xtmem != 0;
+  const uint32_t taX = taA + 2 * MG * (R8 / 4) + whalf * 4 * MG * NH;
   if (warp < 4) {
 #pragma unroll 1
     for (int s = 0; s < KG; ++s) {
@@ -360,11 +361,11 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
       }
     })
     // x = 0 (after the loads of rhs: no load waits behind a store)
-    if constexpr (kXT) {
-      double z0[2 * NH];
+    if (kXT) {
+      double z0[2 * MG * NH];
 #pragma unroll
-      for (int i = 0; i < 2 * NH; ++i) z0[i] = 0.0;
-      tmem_st_doubles<2 * NH>(taX, z0);
+      for (int i = 0; i < 2 * MG * NH; ++i) z0[i] = 0.0;
+      tmem_st_doubles<2 * MG * NH>(taX, z0);
       tmem_wait_st();
     } else {
       TF_TILES({
@@ -598,9 +599,9 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
     }
     // ---- U: r -= alpha z, x += alpha p at this thread's positions; ||r||^2 (x: all loads first, then stores)
     double s2 = 0.0;
-    if constexpr (kXT) {   // x in tensor memory: load, update, store back
-      double xt[2 * NH];
-      tmem_ld_doubles<2 * NH>(taX, xt);
+    if (kXT) {   // x in tensor memory: load, update, store back
+      double xt[2 * MG * NH];
+      tmem_ld_doubles<2 * MG * NH>(taX, xt);
       tmem_wait_ld();
       TF_TILES({
         const int row = 8 * mt + g;
@@ -608,14 +609,14 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
         for (int e = 0; e < 2; ++e) {
           const int c = 8 * j + 2 * q + e;
           if (row < nr && c < R) {
-            xt[2 * jj + e] = fma(alpha, sP[c * LDR + row], xt[2 * jj + e]);
+            xt[2 * (mi * NH + jj) + e] = fma(alpha, sP[c * LDR + row], xt[2 * (mi * NH + jj) + e]);
             const double rn = fma(-alpha, acc[mi][jj][e], rreg[mi][jj][e]);
             rreg[mi][jj][e] = rn;
             s2 = fma(rn, rn, s2);
           }
         }
       })
-      tmem_st_doubles<2 * NH>(taX, xt);
+      tmem_st_doubles<2 * MG * NH>(taX, xt);
       tmem_wait_st();
     } else {
       double xv[MG][NH][2];
@@ -657,15 +658,15 @@ __global__ void __launch_bounds__(kRThreads, 1) k_cg_rows(RowsArgs A) {
   }
   cpa_wait<0>();
   if (kXT && A.mode == 0) {   // x in w-coordinates: x = D x_hat, from tensor memory
-    double xt[2 * NH];
-    tmem_ld_doubles<2 * NH>(taX, xt);
+    double xt[2 * MG * NH];
+    tmem_ld_doubles<2 * MG * NH>(taX, xt);
     tmem_wait_ld();
     TF_TILES({
       const int row = 8 * mt + g;
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const int c = 8 * j + 2 * q + e;
-        if (row < nr && c < R) A.x[off + a0 + row + nl * c] = xt[2 * jj + e] * sD[c];
+        if (row < nr && c < R) A.x[off + a0 + row + nl * c] = xt[2 * (mi * NH + jj) + e] * sD[c];
       }
     })
   }
@@ -782,6 +783,10 @@ cudaError_t launch_cg_rows(const Modes& m, const double* pi, const double* dscal
   a.mode = mode;
   a.tstamp = cg_debug_tstamp();
   a.mtb = rows_plan(m, grid, a.bstart);
+  {
+    const int NTh = (int)((m.R + 7) / 8), MGh = a.mtb > 4 ? 2 : 1;
+    a.xtmem = rows_tmem_cols(NTh, a.mtb, MGh) + rows_tmem_x_cols(NTh, MGh) <= 512 ? 1 : 0;
+  }
   a.G = G;
   const int NT = (int)((m.R + 7) / 8);
   switch (NT) {
