@@ -29,6 +29,9 @@ constexpr int kP3Unroll = TF_P3_UNROLL;   // Pi-form phase-3 k-loop unroll (deve
 #ifndef TF_TMEM_A
 #define TF_TMEM_A 1   // 1: phase-3 A fragments in tensor memory; 2: phase-2 B fragments instead; 0: neither
 #endif
+#ifndef TF_P2_SOUTER
+#define TF_P2_SOUTER 1   // Pi-form phase 2 with the k-steps outer (NT independent accumulators per warp)
+#endif
 #ifndef TF_TMEM_PIPE
 #define TF_TMEM_PIPE 1   // phase-3 tensor-memory loads one k-step ahead (c4 -1.7%, c5 -0.2%)
 #endif
@@ -144,6 +147,9 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
   // tcgen05.ld instead of 13 shared-memory loads per k-step
   constexpr bool kTmemA = !kPre && TF_TMEM_A == 1;
   constexpr bool kTmemB = (RECON && NT > 4) || (!kPre && TF_TMEM_A == 2);   // residual form: B of phase 2 in TMEM
+  // Pi form with R > 32 (measured: c5 -0.8%, c4 -1.4%; for R <= 32 the prescaled path with its hand-off inside
+  // phase 2 stays, s-outer there was 0.4% slower at c3)
+  constexpr bool kP2SOuter = TF_P2_SOUTER && !RECON && !kPre && !kTmemB;
   constexpr int NT4 = 4 * ((NT + 3) / 4);
   // sAc pitch: with the fragments in TMEM the only per-slice reads of sAc are dF/dC's rows 8w + 2q + e, which a
   // pitch = 2 (mod 8) doubles makes conflict-free (2 * pitch = 4 mod 16); otherwise the fragment pitch LDF
@@ -461,7 +467,43 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
 
     // ---- phase 2: P^T_t = B_t^T E^T for i-cols 8*warp.. (t outer, E fragments in registers);
     //      accA^T += diag(c) P^T; dF/dC partial = sum_i A o P; the sAc hand-off sits between the halves
-    {
+    if constexpr (kP2SOuter) {
+      // Pi form (no sAc hand-off inside phase 2): k-steps outer and the NT r-tiles inner, so every warp keeps NT
+      // independent DMMA accumulators in flight (like phase 3) instead of two chains per r-tile
+      double Pt[NT][2];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) Pt[t][0] = Pt[t][1] = 0.0;
+#pragma unroll
+      for (int s = 0; s < kBJ / 4; ++s) {
+        const double e = sT[(4 * s + q) * kLDE + 8 * warp + g];
+        if (s & 1) fsum1 = fma(e, e, fsum1);   // sum t^2 of this slice tile (rows 8w.., all 64 columns)
+        else fsum0 = fma(e, e, fsum0);
+        const double* pbs = sB + (4 * s + q) * LDF + g;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) dmma(Pt[t], pbs[8 * t], e);
+      }
+      double gcv[NV];
+#pragma unroll
+      for (int j = NT; j < NV; ++j) gcv[j] = 0.0;
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const double cr = sc[8 * t + g];
+        const double P0 = Pt[t][0], P1 = Pt[t][1];   // P[i = 8w+2q+e][r = 8t+g]
+        accA[t][0] = fma(cr, P0, accA[t][0]);
+        accA[t][1] = fma(cr, P1, accA[t][1]);
+        const double* pa = sAc + (8 * warp + 2 * q) * LDA + 8 * t + g;
+        gcv[t] = fma(pa[0], P0, pa[LDA] * P1);
+      }
+      TL(kk, 7);
+      butterfly4<NV>(gcv, q);
+      const int base = ((q >> 1) & 1) * (NV / 2) + (q & 1) * (NV / 4);
+      double* gdst = sGC + (kk & 1) * NW * S::GCS + warp * S::GCS + q * S::GCP;
+#pragma unroll
+      for (int j = 0; j < NV / 4; ++j) {
+        const int t = base + j;
+        if (t < NT) gdst[8 * t + g] = gcv[j];
+      }
+    } else {
       double ea[kBJ / 4];
 #pragma unroll
       for (int s = 0; s < kBJ / 4; ++s) ea[s] = sT[(4 * s + q) * kLDE + 8 * warp + g];
