@@ -29,6 +29,9 @@ constexpr int kP3Unroll = TF_P3_UNROLL;   // Pi-form phase-3 k-loop unroll (deve
 #ifndef TF_TMEM_A
 #define TF_TMEM_A 1   // 1: phase-3 A fragments in tensor memory; 2: phase-2 B fragments instead; 0: neither
 #endif
+#ifndef TF_C_ASYNC
+#define TF_C_ASYNC 1     // the c_k ring is filled by cp.async two slices ahead (no load latency on the slice path)
+#endif
 #ifndef TF_P2_SOUTER
 #define TF_P2_SOUTER 1   // Pi-form phase 2 with the k-steps outer (NT independent accumulators per warp)
 #endif
@@ -188,6 +191,12 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
   auto load_c = [&](int64_t kloc, int slot) {
     if (tid < RP) sC[slot * RP + tid] = (tid < p.R) ? p.C[(p.kbeg + kloc) + p.Ktot * tid] : 0.0;
   };
+  // in-loop refill of the ring: asynchronous; waited for (wait_group 0) just before the next slice barrier, a
+  // whole slice after the issue. Rows R..RP-1 of every slot stay zero from the prologue fill.
+  auto load_c_async = [&](int64_t kloc, int slot) {
+    if (tid < p.R) cp_async8_ca(&sC[slot * RP + tid], &p.C[(p.kbeg + kloc) + p.Ktot * tid]);
+    cp_async_commit();
+  };
   auto load_tile_plain = [&](int64_t kloc, double* dst) {
     for (int idx = tid; idx < kBI * kBJ; idx += kThreads) {
       const int j = idx / kBI, i = idx % kBI;
@@ -320,7 +329,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
     }
   };
   if (nk > 0) {
-    for (int u = 0; u < 2 && u < nk; ++u) load_c(kA + u, u);
+    for (int u = 0; u < 4; ++u) load_c(kA + min(u, nk - 1), u);   // all four slots: sets the zero padding rows
     __syncthreads();
     if constexpr (kPre) rebuild_sAc(sC);
   }
@@ -382,6 +391,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
         }
     }
     TL(kk, 2);
+    if (TF_C_ASYNC) cp_async_wait0();   // c_{k+1} (issued in slice k-1) has landed
     __syncthreads();  // S2_k: E_k complete; every warp is past phases 2/3 of slice k-1
     TL(kk, 3);
 
@@ -401,7 +411,10 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
       for (int w = 0; w < NW; ++w) v += gsrc[w * S::GCS];
       p.gCp[((int64_t)(it * p.nTj + jt) * p.K + (k - 1)) * RP + tid] = v;
     }
-    if (kk + 2 < nk) load_c(k + 2, (kk + 2) & 3);
+    if (kk + 2 < nk) {
+      if (TF_C_ASYNC) load_c_async(k + 2, (kk + 2) & 3);
+      else load_c(k + 2, (kk + 2) & 3);
+    }
 
     // ---- phase 3: accB^T += (-A diag c)^T E for j-cols 8*warp.., all R (prescaled sAc: no DMUL)
     if constexpr (kPre) {

@@ -48,7 +48,6 @@ __device__ __forceinline__ void cp_async8z(double* dst, const double* src, bool 
                "r"(valid ? 8 : 0)
                : "memory");
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
