@@ -135,8 +135,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 // RECON = false is the Pi-form pass (the three MTTKRPs of T itself): phase 1 is skipped,
 // phases 2-3 run on T_k, and the per-CTA scalar is sum t^2 (for the Gram expansion of f).
+// two co-resident CTAs of the 64-wide tile where R is small enough (<= 128 registers; measured: c3's Pi pass 0.49
+// vs 0.56 ms with one CTA per SM, the second CTA hides the per-slice barrier and reduction latency)
+template <int NT, bool RECON>
+constexpr int eval_min_blocks(int BT) {
+  return (BT == 32 || NT <= 2 || (!RECON && NT <= 3)) ? 2 : 1;
+}
 template <int NT, bool kTMA, int BT, bool RECON>
-__global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
+__global__ void __launch_bounds__(EvalTile<BT>::THREADS, eval_min_blocks<NT, RECON>(BT))
     k_eval_fused(const __grid_constant__ CUtensorMap tmapT, const double* __restrict__ T, EvalArgs p) {
   if (p.run_if && *p.run_if == 0) return;   // guarded fallback not needed (uniform across the grid)
   using S = EvalSmem<NT, BT>;
@@ -179,14 +185,69 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
   const int bid = blockIdx.x;
-  const int it = bid % p.nTi;
-  const int jt = (bid / p.nTi) % p.nTj;
-  const int kc = bid / (p.nTi * p.nTj);
-  const int64_t i0 = (int64_t)it * kBI, j0 = (int64_t)jt * kBJ;
-  const int64_t kA = (int64_t)kc * p.kChunk;
-  const int64_t kB = min(p.K, kA + p.kChunk);
-  const int nk = (int)max((int64_t)0, kB - kA);
   const int ks1 = (int)((p.R + 3) / 4);    // phase-1 k-steps actually needed (R padded to 4, not 8)
+
+  // ---- once per CTA: barriers, tensor memory
+  TLC(0);
+  if (tid == 0) {
+    if (kTMA) prefetch_tmap(&tmapT);
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(p3done, NW);
+    mbar_init(aready, NW);
+    fence_barrier_init();
+  }
+  uint32_t ta = 0;
+  if constexpr (kTmemA || kTmemB) {
+    if (warp == 0) tmem_alloc(&tmem_base_s, 512);
+  }
+  tmem_fence_before_sync();
+  __syncthreads();
+  tmem_fence_after_sync();
+  if constexpr (kTmemA || kTmemB) ta = tmem_base_s + ((uint32_t)(32 * (warp & 3)) << 16);
+  double fsum0 = 0.0, fsum1 = 0.0;
+
+  // ---- the CTA's segments. Stream-K (p.streamK): the (tile, slice) units in tile-major order are cut into
+  // equal runs of p.unitsPerCta, one per CTA of a persistent grid (no partial last wave); a run covers the tail
+  // of one tile, whole tiles and the head of another, each a segment with its own partial slot (sidx < nseg
+  // <= p.kSplit). Otherwise one segment per CTA: tile bid % tiles, k-chunk bid / tiles.
+  const int64_t tiles = (int64_t)p.nTi * p.nTj;
+  int64_t u = p.streamK ? (int64_t)bid * p.unitsPerCta : 0;
+  const int64_t uend = p.streamK ? min(tiles * p.K, u + p.unitsPerCta) : 1;
+  for (bool firstSeg = true; u < uend; firstSeg = false) {
+  int64_t tile, kA, kB;
+  int sidx, nseg;
+  if (p.streamK) {
+    tile = u / p.K;
+    kA = u - tile * p.K;
+    kB = min(p.K, kA + (uend - u));
+    const int64_t c0 = (tile * p.K) / p.unitsPerCta, c1 = (tile * p.K + p.K - 1) / p.unitsPerCta;
+    sidx = (int)(bid - c0);
+    nseg = (int)(c1 - c0 + 1);
+    u += kB - kA;
+  } else {
+    tile = bid % tiles;
+    const int kc = (int)(bid / tiles);
+    kA = (int64_t)kc * p.kChunk;
+    kB = min(p.K, kA + p.kChunk);
+    sidx = kc;
+    nseg = p.kSplit;
+    u = 1;
+  }
+  const int it = (int)(tile % p.nTi), jt = (int)(tile / p.nTi);
+  const int64_t i0 = (int64_t)it * kBI, j0 = (int64_t)jt * kBJ;
+  const int nk = (int)max((int64_t)0, kB - kA);
+  if (!firstSeg) {   // every barrier of the previous segment has completed all its phases: start afresh
+    if (tid == 0) {
+      for (int b = 0; b < 4; ++b) mbar_inval(&bar[b]);
+      mbar_init(&full[0], 1);
+      mbar_init(&full[1], 1);
+      mbar_init(p3done, NW);
+      mbar_init(aready, NW);
+      fence_barrier_init();
+    }
+    __syncthreads();
+  }
 
   auto load_c = [&](int64_t kloc, int slot) {
     if (tid < RP) sC[slot * RP + tid] = (tid < p.R) ? p.C[(p.kbeg + kloc) + p.Ktot * tid] : 0.0;
@@ -205,18 +266,9 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
     }
   };
 
-  // ---- prologue
-  TLC(0);
-  if (tid == 0) {
-    if (kTMA) prefetch_tmap(&tmapT);
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
-    mbar_init(p3done, NW);
-    mbar_init(aready, NW);
-    fence_barrier_init();
-  }
-  __syncthreads();
+  // ---- segment prologue
   if (kTMA && tid == 0) {
+    fence_proxy_async_smem();   // generic-proxy use of the tile buffers by the previous segment
     for (int u = 0; u < 2 && u < nk; ++u) {
       mbar_arrive_expect_tx(&full[u], kTileBytes);
       tma_load_3d(sTE + u * (kLDE * kBJ), &tmapT, (int)i0, (int)j0, (int)(kA + u), &full[u]);
@@ -273,13 +325,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
 #pragma unroll
       for (int e = 0; e < 2; ++e) Areg[t][e] = sAc[(8 * warp + 2 * q + e) * LDA + 8 * t + g];
   }
-  uint32_t ta = 0;
   if constexpr (kTmemB) {   // phase-2 B fragments B[4s + q][8t + g], per lane: t-major, 16 k-steps per t
-    if (warp == 0) tmem_alloc(&tmem_base_s, 512);
-    tmem_fence_before_sync();
-    __syncthreads();
-    tmem_fence_after_sync();
-    ta = tmem_base_s + ((uint32_t)(32 * (warp & 3)) << 16);
     if (warp < 4) {
 #pragma unroll 1
       for (int t = 0; t < NT; ++t) {
@@ -298,11 +344,6 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
     tmem_fence_after_sync();
   }
   if constexpr (kTmemA) {
-    if (warp == 0) tmem_alloc(&tmem_base_s, 512);
-    tmem_fence_before_sync();
-    __syncthreads();
-    tmem_fence_after_sync();
-    ta = tmem_base_s + ((uint32_t)(32 * (warp & 3)) << 16);
     if (warp < 4) {   // one warp per lane quadrant writes the fragments A[4s + q][8t + g] of every (s, t)
 #pragma unroll 1
       for (int s2 = 0; s2 < kBI / 4; ++s2) {
@@ -338,7 +379,6 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
   double accA[NT][2], accB[NT][2];
 #pragma unroll
   for (int t = 0; t < NT; ++t) accA[t][0] = accA[t][1] = accB[t][0] = accB[t][1] = 0.0;
-  double fsum0 = 0.0, fsum1 = 0.0;
 
   const int wi = warp & 1, wj = warp >> 1;   // phase-1 warp tile: rows (BT/2)*wi.., cols 16*wj..
 
@@ -591,12 +631,9 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
       __syncthreads();
     }
   }
+  tmem_fence_before_sync();
   __syncthreads();
-  TLC(2);
-  if constexpr (kTmemA || kTmemB) {
-    tmem_fence_after_sync();
-    if (warp == 0) tmem_dealloc(tmem_base_s, 512);
-  }
+  tmem_fence_after_sync();
   if (nk > 0 && tid < RP) {
     const double* gsrc = sGC + ((nk - 1) & 1) * NW * S::GCS + tid + ((tid >> 3) / (NV / 4)) * S::GCP;
     double v = 0.0;
@@ -611,15 +648,24 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, BT == 32 ? 2 : 1)
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int64_t i = i0 + 8 * warp + 2 * q + e;
-      p.gAp[((int64_t)(jt * p.kSplit + kc) * p.Ipad + i) * RP + 8 * t + g] = accA[t][e];
+      p.gAp[((int64_t)(jt * p.kSplit + sidx) * p.Ipad + i) * RP + 8 * t + g] = accA[t][e];
+      if (sidx == nseg - 1)   // the tile's last segment zeroes the slots no segment of this tile uses
+        for (int s2 = nseg; s2 < p.kSplit; ++s2) p.gAp[((int64_t)(jt * p.kSplit + s2) * p.Ipad + i) * RP + 8 * t + g] = 0.0;
     }
 #pragma unroll
   for (int t = 0; t < NT; ++t)
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int64_t j = j0 + 8 * warp + 2 * q + e;
-      p.gBp[((int64_t)(it * p.kSplit + kc) * p.Jpad + j) * RP + 8 * t + g] = accB[t][e];
+      p.gBp[((int64_t)(it * p.kSplit + sidx) * p.Jpad + j) * RP + 8 * t + g] = accB[t][e];
+      if (sidx == nseg - 1)
+        for (int s2 = nseg; s2 < p.kSplit; ++s2) p.gBp[((int64_t)(it * p.kSplit + s2) * p.Jpad + j) * RP + 8 * t + g] = 0.0;
     }
+  }   // segments
+  TLC(2);
+  if constexpr (kTmemA || kTmemB) {
+    if (warp == 0) tmem_dealloc(tmem_base_s, 512);
+  }
   double fsum = warp_sum(fsum0 + fsum1);
   if (lane == 0) sRed[warp] = fsum;
   __syncthreads();

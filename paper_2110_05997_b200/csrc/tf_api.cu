@@ -157,6 +157,13 @@ tf_status grams_impl(tf_ctx* c, const tf_dims& d, const double* w, double* grams
   return TF_OK;
 }
 
+// Stream-K decomposition of the fused kernel's (tile, slice) space: TF_EVAL_STREAMK=0 selects the k-chunk grid
+// (development comparison); read per call.
+static bool eval_streamk() {
+  const char* e = getenv("TF_EVAL_STREAMK");
+  return !(e && atoi(e) == 0);
+}
+
 // Tile size of the fused kernel: TF_EVAL_TILE=32|64 overrides (development); default 64.
 int eval_tile() {
   static int bt = 0;
@@ -195,9 +202,29 @@ tf_status eval_impl(tf_ctx* c, const tf_dims& d, const double* T, const double* 
   p.Ipad = (int64_t)p.nTi * BT;
   p.Jpad = (int64_t)p.nTj * BT;
   const int64_t tiles = (int64_t)p.nTi * p.nTj;
-  p.kSplit = choose_ksplit(tiles, d.K, c->nsm * ctas_per_sm);
-  p.kChunk = (d.K + p.kSplit - 1) / p.kSplit;
-  p.nCta = (int)(tiles * p.kSplit);
+  if (eval_streamk() && d.K > 0) {
+    // stream-K: a persistent grid of every co-resident CTA, each with an equal run of (tile, slice) units
+    const char* ecps = getenv("TF_EVAL_PERSIST_CPS");   // development override of the CTAs per SM
+    const int cps = (ecps && atoi(ecps) > 0) ? atoi(ecps) : (BT == 32 ? 2 : eval_ctas_per_sm(NT, !pi_form));
+    const int64_t units = tiles * d.K;
+    int64_t grid = std::min<int64_t>(units, (int64_t)c->nsm * cps);
+    p.unitsPerCta = (units + grid - 1) / grid;
+    grid = (units + p.unitsPerCta - 1) / p.unitsPerCta;
+    int smax = 1;
+    for (int64_t t = 0; t < tiles; ++t) {
+      const int64_t c0 = (t * d.K) / p.unitsPerCta, c1 = (t * d.K + d.K - 1) / p.unitsPerCta;
+      smax = std::max<int>(smax, (int)(c1 - c0 + 1));
+    }
+    p.streamK = 1;
+    p.kSplit = smax;
+    p.kChunk = d.K;
+    p.nCta = (int)grid;
+  } else {
+    p.streamK = 0;
+    p.kSplit = choose_ksplit(tiles, d.K, c->nsm * ctas_per_sm);
+    p.kChunk = (d.K + p.kSplit - 1) / p.kSplit;
+    p.nCta = (int)(tiles * p.kSplit);
+  }
   tf_status s;
   if ((s = ensure(c, c->gAp, (size_t)p.nTj * p.kSplit * p.Ipad * RP * 8))) return s;
   if ((s = ensure(c, c->gBp, (size_t)p.nTi * p.kSplit * p.Jpad * RP * 8))) return s;

@@ -14,6 +14,8 @@ struct EvalArgs {
   int64_t I, J, K, R, ldT, Ktot, kbeg;
   int nTi, nTj, kSplit, nCta;
   int64_t kChunk, Ipad, Jpad;
+  int64_t unitsPerCta;   // stream-K: (tile, slice) units per CTA of the persistent grid
+  int streamK;           // 1: stream-K segments (kSplit = partial slots per tile); 0: one k-chunk per CTA
   double* gAp;  // [nTj*kSplit][Ipad][RP]
   double* gBp;  // [nTi*kSplit][Jpad][RP]
   double* gCp;  // [nTi*nTj][K][RP]

@@ -85,6 +85,28 @@ def test_shapes(ctx, dims):
     check_eval(ctx, T, w, I, J, K, R)
 
 
+@pytest.mark.parametrize("form", ["residual", "pi"])
+@pytest.mark.parametrize("split", ["chunks", "streamk-cps1", "streamk-cps2", "streamk-cps3"])
+@pytest.mark.parametrize("dims", [(130, 70, 40, 20), (200, 150, 61, 13), (65, 63, 3, 9), (90, 40, 7, 33)])
+def test_eval_work_decompositions(ctx, dims, split, form, monkeypatch):
+    """The fused kernel's two decompositions of the (tile, slice) space agree with the oracle: one k-chunk per CTA,
+    and stream-K (equal runs of units per CTA of a persistent grid; the runs cut tiles mid-K, so a tile's partials
+    come from several segments, and a CTA crosses tile boundaries). The CTAs-per-SM override moves the cut points."""
+    if split == "chunks":
+        monkeypatch.setenv("TF_EVAL_STREAMK", "0")
+    else:
+        monkeypatch.setenv("TF_EVAL_PERSIST_CPS", split[-1])
+    I, J, K, R = dims
+    rng = np.random.default_rng(I * J + K + R)
+    T = rng.standard_normal(I * J * K)
+    w = rng.standard_normal(R * (I + J + K))
+    ctx.set_eval_form(form)
+    try:
+        check_eval(ctx, T, w, I, J, K, R)
+    finally:
+        ctx.set_eval_form("auto")
+
+
 @pytest.mark.parametrize("form", ["auto", "pi"])
 def test_padded_leading_dimension(ctx, form):
     """ldT > I (both an even ldT -> TMA path and an odd ldT -> cooperative-load path), both forms."""
