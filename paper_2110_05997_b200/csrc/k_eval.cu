@@ -143,7 +143,8 @@ constexpr int eval_min_blocks(int BT) {
 }
 template <int NT, bool kTMA, int BT, bool RECON>
 __global__ void __launch_bounds__(EvalTile<BT>::THREADS, eval_min_blocks<NT, RECON>(BT))
-    k_eval_fused(const __grid_constant__ CUtensorMap tmapT, const double* __restrict__ T, EvalArgs p) {
+    k_eval_fused(const __grid_constant__ CUtensorMap tmapT, const __grid_constant__ CUtensorMap tmapT4,
+                 const double* __restrict__ T, EvalArgs p) {
   if (p.run_if && *p.run_if == 0) return;   // guarded fallback not needed (uniform across the grid)
   using S = EvalSmem<NT, BT>;
   using Gm = EvalTile<BT>;
@@ -190,7 +191,10 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, eval_min_blocks<NT, REC
   // ---- once per CTA: barriers, tensor memory
   TLC(0);
   if (tid == 0) {
-    if (kTMA) prefetch_tmap(&tmapT);
+    if (kTMA) {
+      prefetch_tmap(&tmapT);
+      if (p.tma4) prefetch_tmap(&tmapT4);
+    }
     mbar_init(&full[0], 1);
     mbar_init(&full[1], 1);
     mbar_init(p3done, NW);
@@ -258,6 +262,15 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, eval_min_blocks<NT, REC
     if (tid < p.R) cp_async8_ca(&sC[slot * RP + tid], &p.C[(p.kbeg + kloc) + p.Ktot * tid]);
     cp_async_commit();
   };
+  // TMA box of BT + 4 rows (the smem row pitch; bank-conflict-free fragments) by BT columns. Interior i-tiles
+  // go through the 4-D view (i mod BT, i / BT, j, k) whose first extent is BT, so the 4 padding rows are out of
+  // bounds there (zero fill, never fetched: otherwise each 512-byte row read drags in the next tile's first
+  // sector, which the stream-K grid no longer reads at the same time — 19.0 instead of 13.9 GB at c5); the last,
+  // partial i-tile uses the 3-D map (its padding rows are past I anyway).
+  auto load_tile_tma = [&](double* dst, int64_t kloc, uint64_t* fb) {
+    if (p.tma4 && i0 + kBI <= p.I) tma_load_4d(dst, &tmapT4, 0, it, (int)j0, (int)kloc, fb);
+    else tma_load_3d(dst, &tmapT, (int)i0, (int)j0, (int)kloc, fb);
+  };
   auto load_tile_plain = [&](int64_t kloc, double* dst) {
     for (int idx = tid; idx < kBI * kBJ; idx += kThreads) {
       const int j = idx / kBI, i = idx % kBI;
@@ -271,7 +284,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, eval_min_blocks<NT, REC
     fence_proxy_async_smem();   // generic-proxy use of the tile buffers by the previous segment
     for (int u = 0; u < 2 && u < nk; ++u) {
       mbar_arrive_expect_tx(&full[u], kTileBytes);
-      tma_load_3d(sTE + u * (kLDE * kBJ), &tmapT, (int)i0, (int)j0, (int)(kA + u), &full[u]);
+      load_tile_tma(sTE + u * (kLDE * kBJ), kA + u, &full[u]);
     }
   }
   if (!kTMA && nk > 0) load_tile_plain(kA, sTE);
@@ -440,7 +453,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, eval_min_blocks<NT, REC
         if (kk >= 1 && tid == 0) {   // slices 0 and 1 were issued in the prologue
           fence_proxy_async_smem();
           mbar_arrive_expect_tx(&full[b ^ 1], kTileBytes);
-          tma_load_3d(sTE + (b ^ 1) * (kLDE * kBJ), &tmapT, (int)i0, (int)j0, (int)(k + 1), &full[b ^ 1]);
+          load_tile_tma(sTE + (b ^ 1) * (kLDE * kBJ), k + 1, &full[b ^ 1]);
         }
       }
     }
@@ -844,12 +857,12 @@ static cudaError_t launch_eval_ntr(const CUtensorMap* map, const double* T, cons
     auto kern = k_eval_fused<NT, true, BT, RECON>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<p.nCta, threads, smem, st>>>(*map, T, p);
+    kern<<<p.nCta, threads, smem, st>>>(map[0], map[1], T, p);
   } else {
     auto kern = k_eval_fused<NT, false, BT, RECON>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<p.nCta, threads, smem, st>>>(*map, T, p);
+    kern<<<p.nCta, threads, smem, st>>>(map[0], map[1], T, p);
   }
   return cudaGetLastError();
 }

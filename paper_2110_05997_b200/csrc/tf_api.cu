@@ -164,6 +164,15 @@ static bool eval_streamk() {
   return !(e && atoi(e) == 0);
 }
 
+// L2 promotion of the T tiles' TMA reads (TF_EVAL_L2PROMO = 0 | 64 | 128 | 256, development comparison).
+static CUtensorMapL2promotion eval_l2_promotion() {
+  const char* e = getenv("TF_EVAL_L2PROMO");
+  const int v = e ? atoi(e) : 0;
+  return v == 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                  : v == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                             : v == 64 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+}
+
 // Tile size of the fused kernel: TF_EVAL_TILE=32|64 overrides (development); default 64.
 int eval_tile() {
   static int bt = 0;
@@ -235,8 +244,8 @@ tf_status eval_impl(tf_ctx* c, const tf_dims& d, const double* T, const double* 
   p.gCp = (double*)c->gCp.p;
   p.fp = (double*)c->fp.p;
 
-  CUtensorMap map;
-  memset(&map, 0, sizeof(map));
+  CUtensorMap map[2];   // [0] 3-D (I, J, K) view; [1] 4-D (i mod BT, i / BT, J, K) view of the whole i-tiles
+  memset(map, 0, sizeof(map));
   bool tma = (d.ldT % 2 == 0) && ((reinterpret_cast<uintptr_t>(T) & 15) == 0);
   if (tma) {
     EncodeTiledFn enc = get_encode_fn();
@@ -247,10 +256,21 @@ tf_status eval_impl(tf_ctx* c, const tf_dims& d, const double* T, const double* 
       cuuint64_t gstride[2] = {(cuuint64_t)d.ldT * 8, (cuuint64_t)d.ldT * d.J * 8};
       cuuint32_t box[3] = {(cuuint32_t)(BT + 4), (cuuint32_t)BT, 1};
       cuuint32_t estr[3] = {1, 1, 1};
-      CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(T), gdim, gstride, box, estr,
-                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      CUresult r = enc(&map[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(T), gdim, gstride, box,
+                       estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, eval_l2_promotion(),
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (r != CUDA_SUCCESS) tma = false;
+      const char* e4 = getenv("TF_EVAL_TMA4");   // development switch: 0 = 3-D map only
+      if (tma && d.I >= BT && !(e4 && atoi(e4) == 0)) {
+        cuuint64_t gdim4[4] = {(cuuint64_t)BT, (cuuint64_t)(d.I / BT), (cuuint64_t)d.J, (cuuint64_t)d.K};
+        cuuint64_t gstride4[3] = {(cuuint64_t)BT * 8, (cuuint64_t)d.ldT * 8, (cuuint64_t)d.ldT * d.J * 8};
+        cuuint32_t box4[4] = {(cuuint32_t)(BT + 4), 1, (cuuint32_t)BT, 1};
+        cuuint32_t estr4[4] = {1, 1, 1, 1};
+        r = enc(&map[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(T), gdim4, gstride4, box4, estr4,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, eval_l2_promotion(),
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        p.tma4 = r == CUDA_SUCCESS ? 1 : 0;
+      }
     }
   }
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -272,7 +292,7 @@ tf_status eval_impl(tf_ctx* c, const tf_dims& d, const double* T, const double* 
   c->last_eval_pi = pi_form;
   c->last_eval_tma = tma ? 1 : 0;
   if (!pi_form) {
-    TF_CUDA(c, launch_eval(&map, T, p, NT, tma, BT, c->stream));
+    TF_CUDA(c, launch_eval(map, T, p, NT, tma, BT, c->stream));
     if (c->timing) TF_CUDA(c, cudaEventRecord(e1, c->stream));
     TF_CUDA(c, launch_eval_finalize(p, RP, f, grad, c->nsm, c->stream));
     c->eval_launches += 1;
@@ -288,7 +308,7 @@ tf_status eval_impl(tf_ctx* c, const tf_dims& d, const double* T, const double* 
   double* grams = (double*)c->evGrams.p;
   double* part = (double*)c->evPart.p;
   int* flag = reinterpret_cast<int*>(part + 3 * nblk);
-  TF_CUDA(c, launch_eval(&map, T, p, NT, tma, BT, c->stream, false));
+  TF_CUDA(c, launch_eval(map, T, p, NT, tma, BT, c->stream, false));
   // Equal-size modes sit I*R apart in w (and their Grams / Pi blocks R*R apart), so their small GEMMs run as
   // one batched launch: the three Grams (whole tensor, I = J = K) or A^T A and B^T B (I = J).
   const bool cube = d.I == d.J && d.J == d.K && d.K == d.K_total;
@@ -337,7 +357,7 @@ tf_status eval_impl(tf_ctx* c, const tf_dims& d, const double* T, const double* 
   TF_CUDA(c, launch_eval_pi_guard(p, grams, part, nblk, f, flag, c->stream, !c->eval_f_only));
   EvalArgs pr = p;
   pr.run_if = flag;
-  TF_CUDA(c, launch_eval(&map, T, pr, NT, tma, BT, c->stream, true));
+  TF_CUDA(c, launch_eval(map, T, pr, NT, tma, BT, c->stream, true));
   if (c->timing) TF_CUDA(c, cudaEventRecord(e1, c->stream));
   TF_CUDA(c, launch_eval_finalize(pr, RP, f, grad, c->nsm, c->stream));
   c->eval_launches += 1;

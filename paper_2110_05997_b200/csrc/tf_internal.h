@@ -16,6 +16,7 @@ struct EvalArgs {
   int64_t kChunk, Ipad, Jpad;
   int64_t unitsPerCta;   // stream-K: (tile, slice) units per CTA of the persistent grid
   int streamK;           // 1: stream-K segments (kSplit = partial slots per tile); 0: one k-chunk per CTA
+  int tma4;              // 1: interior i-tiles load through the 4-D map (no over-read of the 4 padding rows)
   double* gAp;  // [nTj*kSplit][Ipad][RP]
   double* gBp;  // [nTi*kSplit][Jpad][RP]
   double* gCp;  // [nTi*nTj][K][RP]
@@ -34,6 +35,7 @@ cudaError_t launch_eval_pi_guard(const EvalArgs& p, const double* grams, const d
                                  int* flag, cudaStream_t st, bool check_grad = true);
 int eval_pi_blocks(int nsm);
 
+// map[0]: the 3-D TMA view of T, map[1]: the 4-D view of its whole i-tiles (used when p.tma4)
 cudaError_t launch_eval(const CUtensorMap* map, const double* T, const EvalArgs& p, int NT, bool tma, int BT,
                         cudaStream_t st, bool recon = true);
 cudaError_t launch_eval_finalize(const EvalArgs& p, int RP, double* f, double* grad, int nsm, cudaStream_t st);
