@@ -35,6 +35,9 @@ constexpr int kP3Unroll = TF_P3_UNROLL;   // Pi-form phase-3 k-loop unroll (deve
 #ifndef TF_P2_SOUTER
 #define TF_P2_SOUTER 1   // Pi-form phase 2 with the k-steps outer (NT independent accumulators per warp)
 #endif
+#ifndef TF_PI_PRE_MAXNT
+#define TF_PI_PRE_MAXNT 0   // Pi pass: prescaled -A diag(c_k) rebuilt per slice up to this NT, else unscaled A in TMEM
+#endif
 #ifndef TF_TMEM_PIPE
 #define TF_TMEM_PIPE 1   // phase-3 tensor-memory loads one k-step ahead (c4 -1.7%, c5 -0.2%)
 #endif
@@ -68,8 +71,9 @@ struct EvalSmem {
   static constexpr int GCS = RP + 3 * GCP;                     // row stride of the dF/dC partials
   static constexpr size_t off_gc = off_c + 4 * (size_t)RP * 8;            // 2 x [NW][GCS] (per-warp dF/dC partials)
   static constexpr size_t off_red = off_gc + 2 * G::NW * (size_t)GCS * 8; // [NW]
-  static constexpr size_t off_bar = off_red + G::NW * 8;                  // 4 mbarriers: full[2], p3done, aready
-  static constexpr size_t bytes = off_bar + 4 * 8;
+  // 12 mbarriers: full[2], p3done, aready; the decoupled Pi pass adds empty[2], gcf[2], gce[2], mid[2]
+  static constexpr size_t off_bar = off_red + G::NW * 8;
+  static constexpr size_t bytes = off_bar + 12 * 8;
   static_assert(bytes <= 232448, "exceeds the 227 KB per-CTA shared memory of sm_100a");
 };
 
@@ -97,6 +101,13 @@ __device__ __forceinline__ void butterfly4(double (&v)[N], int q) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
+// one arrival on the mbarrier once every cp.async this thread issued so far has landed (not counted in advance:
+// the barrier's expected count includes it)
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+// block barrier 1 among the 128 threads of warp group 1 (warps 4-7)
+__device__ __forceinline__ void group1_sync() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
 
 // Schedule of one CTA over its slices (one block-wide barrier per slice; the sAc hand-off uses two
 // 8-warp mbarriers whose waits sit after independent work, so they normally cost nothing):
@@ -149,9 +160,10 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, eval_min_blocks<NT, REC
   using S = EvalSmem<NT, BT>;
   using Gm = EvalTile<BT>;
   // phase 3 with the prescaled tile -A diag(c_k) (rebuilt per slice, needed by phase 1 of the residual form)
-  // or, in the Pi pass with R > 32, with unscaled A and the per-slice scaling on the product (measured: c4/c5
-  // 6%/2.5% faster; for R <= 32 the rebuild is cheaper than the extra accumulators, c3 9%)
-  constexpr bool kPre = RECON || NT <= 4;
+  // or, in the Pi pass, with unscaled A (in tensor memory) and the per-slice scaling on the product (measured: c4/c5
+  // 6%/2.5% faster; at small R, with the stream-K grid and A in tensor memory, too: 500^3 R = 16/24/32 -5%/-2%/-8%,
+  // R = 8 equal; round 1's prescaled path was 9% faster at c3 when A came from shared memory)
+  constexpr bool kPre = RECON || NT <= TF_PI_PRE_MAXNT;
   // Pi pass with the unscaled A: phase 3's A fragments are the same for every slice and every warp, so they
   // are parked once in tensor memory (16 k-steps x NT4 doubles per lane = 512 columns) and read with
   // tcgen05.ld instead of 13 shared-memory loads per k-step
@@ -161,6 +173,10 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, eval_min_blocks<NT, REC
   // phase 2 stays, s-outer there was 0.4% slower at c3)
   constexpr bool kP2SOuter = TF_P2_SOUTER && !RECON && !kPre && !kTmemB;
   constexpr int NT4 = 4 * ((NT + 3) / 4);
+  // tensor-memory columns: 16 k-steps x NT4 (phase-3 A) or NT x 16 (phase-2 B) doubles per lane, 2 columns each,
+  // rounded up to a power of two (small R leaves room for a co-resident CTA's allocation)
+  constexpr int kTmemNeed = kTmemB ? 32 * NT : 32 * NT4;
+  constexpr int kTmemCols = kTmemNeed <= 32 ? 32 : kTmemNeed <= 64 ? 64 : kTmemNeed <= 128 ? 128 : kTmemNeed <= 256 ? 256 : 512;
   // sAc pitch: with the fragments in TMEM the only per-slice reads of sAc are dF/dC's rows 8w + 2q + e, which a
   // pitch = 2 (mod 8) doubles makes conflict-free (2 * pitch = 4 mod 16); otherwise the fragment pitch LDF
   constexpr int LDA = kTmemA ? 8 * NT + 2 : S::LDF;
@@ -183,9 +199,40 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, eval_min_blocks<NT, REC
   uint64_t* full = bar;          // [2] TMA completion per T/E buffer
   uint64_t* p3done = bar + 2;    // all 8 warps finished reading sAc_k (phase 3)
   uint64_t* aready = bar + 3;    // all 8 warps wrote their rows of sAc_{k+1}
+  // Decoupled Pi pass (kDec): no block barrier per slice. Warp group 0 (warps 0-3) runs ahead of group 1 (warps
+  // 4-7, one of each per sub-partition), so that one warp's slice epilogue (scaling, butterfly, dF/dC rows) and
+  // barrier waits overlap the other's DMMA stream instead of idling the pipe on every sub-partition at once.
+  //   full[b]  T_k (TMA) and c_k (cp.async, 32 lanes of warp 4) landed in buffer / slot b = k % 2 (33 arrivals)
+  //   empty[b] all 8 warps are done with buffer b; warp 4 then issues slice k + 2 into it
+  //   gcf[x]   group 0 wrote its dF/dC rows of slice k into sGC[x = k % 2]; group 1 reduces them with its own
+  //   gce[x]   group 1 finished reducing sGC[x]; group 0 may overwrite it (slice k + 2)
+  uint64_t* empty = bar + 4;
+  uint64_t* gcf = bar + 6;
+  uint64_t* gce = bar + 8;
+  //   mid[x]   group 1 finished phase 3 of slice k (x = k % 2): group 0 starts slice k + 1 only then, so that it
+  //            leads by at most about half a slice (the TMA of slice k + 2, issued when slice k is done everywhere,
+  //            keeps half a slice of lead; unthrottled, group 0 ran up to the TMA and waited on it every slice)
+  uint64_t* mid = bar + 10;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
   const int bid = blockIdx.x;
+  constexpr bool kDecOK = kTMA && !RECON && !kPre && kTmemA && kP2SOuter && TF_TMEM_PIPE && BT == 64;
+  const bool dec = kDecOK && p.decouple;
+  auto init_bars = [&]() {
+    mbar_init(&full[0], dec ? 33 : 1);
+    mbar_init(&full[1], dec ? 33 : 1);
+    mbar_init(p3done, NW);
+    mbar_init(aready, NW);
+    if (dec) {
+      for (int x = 0; x < 2; ++x) {
+        mbar_init(&empty[x], NW);
+        mbar_init(&gcf[x], 4);
+        mbar_init(&gce[x], 4);
+        mbar_init(&mid[x], 4);
+      }
+    }
+    fence_barrier_init();
+  };
   const int ks1 = (int)((p.R + 3) / 4);    // phase-1 k-steps actually needed (R padded to 4, not 8)
 
   // ---- once per CTA: barriers, tensor memory
@@ -195,15 +242,14 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, eval_min_blocks<NT, REC
       prefetch_tmap(&tmapT);
       if (p.tma4) prefetch_tmap(&tmapT4);
     }
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
-    mbar_init(p3done, NW);
-    mbar_init(aready, NW);
-    fence_barrier_init();
+    init_bars();
   }
+  // the decoupled pass fills only rows < R of the c slots (cp.async): the padding rows stay zero from here
+  if (dec)
+    for (int x = tid; x < 4 * RP; x += kThreads) sC[x] = 0.0;
   uint32_t ta = 0;
   if constexpr (kTmemA || kTmemB) {
-    if (warp == 0) tmem_alloc(&tmem_base_s, 512);
+    if (warp == 0) tmem_alloc(&tmem_base_s, kTmemCols);
   }
   tmem_fence_before_sync();
   __syncthreads();
@@ -243,12 +289,8 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, eval_min_blocks<NT, REC
   const int nk = (int)max((int64_t)0, kB - kA);
   if (!firstSeg) {   // every barrier of the previous segment has completed all its phases: start afresh
     if (tid == 0) {
-      for (int b = 0; b < 4; ++b) mbar_inval(&bar[b]);
-      mbar_init(&full[0], 1);
-      mbar_init(&full[1], 1);
-      mbar_init(p3done, NW);
-      mbar_init(aready, NW);
-      fence_barrier_init();
+      for (int b = 0; b < (dec ? 12 : 4); ++b) mbar_inval(&bar[b]);
+      init_bars();
     }
     __syncthreads();
   }
@@ -279,8 +321,21 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, eval_min_blocks<NT, REC
     }
   };
 
+  // decoupled pass: warp 4 issues slice kloc into buffer / c slot buf (TMA of T_k by lane 0, c_k by cp.async)
+  auto issue_dec = [&](int64_t kloc, int buf) {
+    if (lane == 0) {
+      fence_proxy_async_smem();   // generic-proxy reads of the buffer (previous slice) before the async write
+      mbar_arrive_expect_tx(&full[buf], kTileBytes);
+      load_tile_tma(sTE + buf * (kLDE * kBJ), kloc, &full[buf]);
+    }
+    for (int r = lane; r < p.R; r += 32) cp_async8_ca(&sC[buf * RP + r], &p.C[(p.kbeg + kloc) + p.Ktot * r]);
+    cp_async_mbar_arrive_noinc(&full[buf]);
+  };
   // ---- segment prologue
-  if (kTMA && tid == 0) {
+  if (dec) {
+    if (warp == 4)
+      for (int u = 0; u < 2 && u < nk; ++u) issue_dec(kA + u, u);
+  } else if (kTMA && tid == 0) {
     fence_proxy_async_smem();   // generic-proxy use of the tile buffers by the previous segment
     for (int u = 0; u < 2 && u < nk; ++u) {
       mbar_arrive_expect_tx(&full[u], kTileBytes);
@@ -382,7 +437,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, eval_min_blocks<NT, REC
       sAc[(8 * warp + 2 * q + 1) * LDA + 8 * t + g] = Areg[t][1] * cr;
     }
   };
-  if (nk > 0) {
+  if (nk > 0 && !dec) {
     for (int u = 0; u < 4; ++u) load_c(kA + min(u, nk - 1), u);   // all four slots: sets the zero padding rows
     __syncthreads();
     if constexpr (kPre) rebuild_sAc(sC);
@@ -396,7 +451,116 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, eval_min_blocks<NT, REC
   const int wi = warp & 1, wj = warp >> 1;   // phase-1 warp tile: rows (BT/2)*wi.., cols 16*wj..
 
   TLC(1);
-  for (int kk = 0; kk < nk; ++kk) {
+  if constexpr (kDecOK) {
+    if (dec) {
+      const int grp = warp >> 2;
+      if (grp == 1 && p.skewNs > 0) {   // group 0's head start (re-established at every segment start)
+        unsigned long long t0, t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        do {
+          __nanosleep(256);
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        } while (t - t0 < (unsigned long long)p.skewNs);
+      }
+      for (int kk = 0; kk < nk; ++kk) {
+        const int b = kk & 1;
+        const uint32_t use = (uint32_t)(kk >> 1);   // how many times buffer / slot b was used before
+        const int64_t k = kA + kk;
+        const double* sT = sTE + b * (kLDE * kBJ);
+        const double* sc = sC + b * RP;
+        if (grp == 0 && kk > 0 && p.decouple == 1) mbar_wait(&mid[b ^ 1], ((kk - 1) >> 1) & 1);
+        mbar_wait(&full[b], use & 1);
+        // ---- phase 3: Q = A^T T_k (A fragments from tensor memory), accB^T -= diag(c_k) Q
+        {
+          double Qt[NT][2];
+#pragma unroll
+          for (int t = 0; t < NT; ++t) Qt[t][0] = Qt[t][1] = 0.0;
+          const double* pe = sT + (8 * warp + g) * kLDE + q;
+          double af[2][NT];
+          tmem_ld_doubles<NT>(ta, af[0]);
+          tmem_wait_ld();
+#pragma unroll
+          for (int s = 0; s < kBI / 4; ++s) {
+            if (s + 1 < kBI / 4) tmem_ld_doubles<NT>(ta + 2 * (s + 1) * NT4, af[(s + 1) & 1]);
+            const double bb = pe[4 * s];
+#pragma unroll
+            for (int t = 0; t < NT; ++t) dmma(Qt[t], af[s & 1][t], bb);
+            if (s + 1 < kBI / 4) tmem_wait_ld();
+          }
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            const double cr = -sc[8 * t + g];
+            accB[t][0] = fma(cr, Qt[t][0], accB[t][0]);
+            accB[t][1] = fma(cr, Qt[t][1], accB[t][1]);
+          }
+        }
+        if (grp == 1) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&mid[b]);
+        }
+        // ---- phase 2: P = T_k B (k-steps outer, NT accumulators), accA += P diag(c_k), dF/dC rows
+        double Pt[NT][2];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) Pt[t][0] = Pt[t][1] = 0.0;
+#pragma unroll
+        for (int s = 0; s < kBJ / 4; ++s) {
+          const double e = sT[(4 * s + q) * kLDE + 8 * warp + g];
+          if (s & 1) fsum1 = fma(e, e, fsum1);
+          else fsum0 = fma(e, e, fsum0);
+          const double* pbs = sB + (4 * s + q) * LDF + g;
+#pragma unroll
+          for (int t = 0; t < NT; ++t) dmma(Pt[t], pbs[8 * t], e);
+        }
+        double gcv[NV];
+#pragma unroll
+        for (int j = NT; j < NV; ++j) gcv[j] = 0.0;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const double cr = sc[8 * t + g];
+          const double P0 = Pt[t][0], P1 = Pt[t][1];
+          accA[t][0] = fma(cr, P0, accA[t][0]);
+          accA[t][1] = fma(cr, P1, accA[t][1]);
+          const double* pa = sAc + (8 * warp + 2 * q) * LDA + 8 * t + g;
+          gcv[t] = fma(pa[0], P0, pa[LDA] * P1);
+        }
+        butterfly4<NV>(gcv, q);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[b]);   // this warp's last reads of buffer b and c slot b are done
+        if (grp == 0 && kk >= 2) mbar_wait(&gce[b], (use - 1) & 1);   // group 1 reduced slice k - 2 from sGC[b]
+        {
+          const int base = ((q >> 1) & 1) * (NV / 2) + (q & 1) * (NV / 4);
+          double* gdst = sGC + b * NW * S::GCS + warp * S::GCS + q * S::GCP;
+#pragma unroll
+          for (int j = 0; j < NV / 4; ++j) {
+            const int t = base + j;
+            if (t < NT) gdst[8 * t + g] = gcv[j];
+          }
+        }
+        if (grp == 0) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&gcf[b]);
+        } else {
+          group1_sync();                   // group 1's rows of slice k are in sGC[b]
+          mbar_wait(&gcf[b], use & 1);     // and group 0's
+          const int t1 = tid - 128;
+          if (t1 < RP) {
+            const double* gsrc = sGC + b * NW * S::GCS + t1 + ((t1 >> 3) / (NV / 4)) * S::GCP;
+            double v = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) v += gsrc[w * S::GCS];
+            p.gCp[((int64_t)(it * p.nTj + jt) * p.K + k) * RP + t1] = v;
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&gce[b]);
+          if (warp == 4 && kk + 2 < nk) {
+            mbar_wait(&empty[b], use & 1);   // every warp is done with slice k
+            issue_dec(k + 2, b);
+          }
+        }
+      }
+    }
+  }
+  for (int kk = 0; kk < (dec ? 0 : nk); ++kk) {
     const int b = kk & 1;
     const int64_t k = kA + kk;
     double* sT = sTE + b * (kLDE * kBJ);
@@ -647,7 +811,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, eval_min_blocks<NT, REC
   tmem_fence_before_sync();
   __syncthreads();
   tmem_fence_after_sync();
-  if (nk > 0 && tid < RP) {
+  if (nk > 0 && tid < RP && !dec) {
     const double* gsrc = sGC + ((nk - 1) & 1) * NW * S::GCS + tid + ((tid >> 3) / (NV / 4)) * S::GCP;
     double v = 0.0;
 #pragma unroll
@@ -677,7 +841,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, eval_min_blocks<NT, REC
   }   // segments
   TLC(2);
   if constexpr (kTmemA || kTmemB) {
-    if (warp == 0) tmem_dealloc(tmem_base_s, 512);
+    if (warp == 0) tmem_dealloc(tmem_base_s, kTmemCols);
   }
   double fsum = warp_sum(fsum0 + fsum1);
   if (lane == 0) sRed[warp] = fsum;

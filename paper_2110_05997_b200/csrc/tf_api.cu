@@ -164,6 +164,20 @@ static bool eval_streamk() {
   return !(e && atoi(e) == 0);
 }
 
+// Decoupled warp groups in the Pi-form pass: 0 = the per-slice block barrier, 1 = decoupled with group 0
+// throttled to about half a slice ahead, 2 = decoupled, unthrottled; TF_EVAL_DECOUPLE overrides (development).
+// Default from the 500^3 sweep over R = 8..40 and c4/c5 (tools/gpu_r02dec4.sh): only NT = 3 gains (R = 24: 0.485 ->
+// 0.473 ms, 2 CTAs per SM); every other NT loses 3-11%, c5 6%. The head start of group 0 in ns: TF_EVAL_SKEW_NS,
+// default about half a slice (260 ns per r-tile; no measurable effect).
+static int eval_decouple(int NT) {
+  const char* e = getenv("TF_EVAL_DECOUPLE");
+  return e ? atoi(e) : (NT == 3 ? 2 : 0);
+}
+static int eval_skew_ns(int NT) {
+  const char* e = getenv("TF_EVAL_SKEW_NS");
+  return e ? atoi(e) : 260 * NT;
+}
+
 // L2 promotion of the T tiles' TMA reads (TF_EVAL_L2PROMO = 0 | 64 | 128 | 256, development comparison).
 static CUtensorMapL2promotion eval_l2_promotion() {
   const char* e = getenv("TF_EVAL_L2PROMO");
@@ -210,11 +224,16 @@ tf_status eval_impl(tf_ctx* c, const tf_dims& d, const double* T, const double* 
   p.nTj = (int)((d.J + BT - 1) / BT);
   p.Ipad = (int64_t)p.nTi * BT;
   p.Jpad = (int64_t)p.nTj * BT;
+  p.decouple = eval_decouple(NT);
+  p.skewNs = eval_skew_ns(NT);
   const int64_t tiles = (int64_t)p.nTi * p.nTj;
   if (eval_streamk() && d.K > 0) {
     // stream-K: a persistent grid of every co-resident CTA, each with an equal run of (tile, slice) units
     const char* ecps = getenv("TF_EVAL_PERSIST_CPS");   // development override of the CTAs per SM
-    const int cps = (ecps && atoi(ecps) > 0) ? atoi(ecps) : (BT == 32 ? 2 : eval_ctas_per_sm(NT, !pi_form));
+    // the Pi pass runs two CTAs per SM where its launch bounds guarantee them (R <= 24), one otherwise (measured:
+    // 500^3 R = 8/16/24 at two CTAs 0.242/0.351/0.485 ms vs one 0.294/0.385/0.526 ms; R = 32 one CTA 0.621 vs 0.636)
+    const int cps = (ecps && atoi(ecps) > 0) ? atoi(ecps)
+                                             : (BT == 32 ? 2 : pi_form ? (NT <= 3 ? 2 : 1) : eval_ctas_per_sm(NT, true));
     const int64_t units = tiles * d.K;
     int64_t grid = std::min<int64_t>(units, (int64_t)c->nsm * cps);
     p.unitsPerCta = (units + grid - 1) / grid;

@@ -17,6 +17,9 @@ struct EvalArgs {
   int64_t unitsPerCta;   // stream-K: (tile, slice) units per CTA of the persistent grid
   int streamK;           // 1: stream-K segments (kSplit = partial slots per tile); 0: one k-chunk per CTA
   int tma4;              // 1: interior i-tiles load through the 4-D map (no over-read of the 4 padding rows)
+  int decouple;          // 1: Pi-form pass with the two warp groups decoupled (mbarrier hand-offs, no per-slice
+                         //    block barrier; used by the instantiations that support it, ignored elsewhere)
+  int skewNs;            // decoupled pass: head start of warp group 0 over group 1 at each segment start
   double* gAp;  // [nTj*kSplit][Ipad][RP]
   double* gBp;  // [nTi*kSplit][Jpad][RP]
   double* gCp;  // [nTi*nTj][K][RP]
