@@ -15,10 +15,14 @@ config, the one the north star's scaling target is quoted on, and it fits one GP
 N>1 is launched by torchrun (one rank per GPU, NCCL); T is sharded along K (strong scaling of one
 problem: total work fixed). Timing: W untimed warm-up steps, then K steps bracketed by a barrier and
 cuda synchronize, CUDA events on the evaluation stream, max over ranks. T (13.8 GB) exceeds the
-126 MB L2, so no flush is needed between steps. `--impl reference` times the CPU oracle (the
+126 MB L2, so no flush is needed between steps; for configs whose T would fit in L2 (c1, c2) every timed
+step is preceded by a 256 MB L2-flushing write and timed by its own CUDA-event pair (the flush outside it). `--impl reference` times the CPU oracle (the
 "reference arm" of this tier) on a bounded sample of the same workload.
 """
 from __future__ import annotations
+
+L2_BYTES = 126 * 1024 * 1024        # B200 L2
+L2_FLUSH_BYTES = 256 * 1024 * 1024  # written between timed steps when T could stay in L2
 
 import argparse
 import json
@@ -361,14 +365,25 @@ def run_ours(args):
     ctx.kernel_stats(reset=True)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    flush_l2 = cfg.t_bytes < 2 * L2_BYTES   # T (and the factors) could stay in L2 from one step to the next
+    scratch = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev) if flush_l2 else None
     with ClockSampler(local) as clk:
         barrier()
-        e0.record(stream)
-        for _ in range(args.steps):
-            step()
-        e1.record(stream)
+        if flush_l2:
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.steps)]
+            for i in range(args.steps):
+                scratch.fill_(i)           # evicts T, the factors and the workspaces from L2
+                evs[i][0].record(stream)
+                step()
+                evs[i][1].record(stream)
+        else:
+            e0.record(stream)
+            for _ in range(args.steps):
+                step()
+            e1.record(stream)
         barrier()
-    ms_local = e0.elapsed_time(e1)
+    ms_local = sum(a.elapsed_time(b) for a, b in evs) if flush_l2 else e0.elapsed_time(e1)
     eval_ms, eval_n, launches = ctx.kernel_stats(reset=True)
     ctx.set_timing(False)
     ms_total = max_over_ranks(ms_local, dev, world)
@@ -583,7 +598,9 @@ def run_ours(args):
                        "parallelism": (f"K-sharded x{world} + 1 {backend.upper()} all-reduce of [grad|f]"
                                        + ("" if backend == "nccl" else " (development switch: ranks share a GPU; "
                                           "not a scaling measurement)")) if world > 1 else "1 GPU",
-                       "l2": f"inputs larger than L2 (T = {cfg.t_bytes / 1e9:.2f} GB > 126 MB), no flush",
+                       "l2": (f"T = {cfg.t_bytes / 1e6:.1f} MB could stay in the 126 MB L2: a 256 MB write flushes "
+                              "L2 before every timed step, outside that step's CUDA-event pair" if flush_l2 else
+                              f"inputs larger than L2 (T = {cfg.t_bytes / 1e9:.2f} GB > 126 MB), no flush"),
                        "step": "tf_cpd_eval (F, grad, Grams) + tf_cg_solve(cg_iters)" if world == 1 else
                                "tf_cpd_eval (local, + Grams of the full factors) + all_reduce([grad|f]) + tf_cg_solve(cg_iters)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,

@@ -107,6 +107,26 @@ def test_eval_work_decompositions(ctx, dims, split, form, monkeypatch):
         ctx.set_eval_form("auto")
 
 
+@pytest.mark.parametrize("decouple", ["0", "1", "2"])
+@pytest.mark.parametrize("dims", [(130, 70, 40, 20), (200, 150, 61, 13), (90, 40, 7, 33), (52, 52, 19, 100),
+                                  (256, 200, 75, 24)])
+def test_eval_decoupled_warp_groups(ctx, dims, decouple, monkeypatch):
+    """The Pi pass with the per-slice block barrier (0) and with decoupled warp groups (mbarrier hand-offs of T_k
+    and c_k, the dF/dC rows and the buffers; 1 throttled, 2 unthrottled) agrees with the oracle, on stream-K runs
+    that cross tiles (segments of 1..17 slices, so every issue / wait path of the two-buffer ring runs)."""
+    monkeypatch.setenv("TF_EVAL_DECOUPLE", decouple)
+    I, J, K, R = dims
+    rng = np.random.default_rng(7 * I + J + K + R)
+    T = rng.standard_normal(I * J * K)
+    w = rng.standard_normal(R * (I + J + K))
+    ctx.set_eval_form("pi")
+    try:
+        check_eval(ctx, T, w, I, J, K, R)
+        assert ctx.eval_fell_back() == 0
+    finally:
+        ctx.set_eval_form("auto")
+
+
 @pytest.mark.parametrize("form", ["auto", "pi"])
 def test_padded_leading_dimension(ctx, form):
     """ldT > I (both an even ldT -> TMA path and an odd ldT -> cooperative-load path), both forms."""
@@ -667,8 +687,8 @@ def test_sharded_dgn_matches_single_device(ctx):
                                   (45, 80, 30, 104), (30, 40, 25, 128), (130, 70, 20, 57),
                                   (41, 41, 41, 13), (52, 52, 19, 100)])
 def test_pi_form_shapes(ctx, dims):
-    """The guarded Pi-form pass forced at every fragment-count regime (R = 1 .. 128: the prescaled phase 3 for
-    R <= 32, the tensor-memory fragments above, R = 128 filling all 512 TMEM columns), ragged tiles, at a
+    """The guarded Pi-form pass forced at every fragment-count regime (R = 1 .. 128: tensor-memory A fragments in
+    32 .. 512 columns, two CTAs per SM for R <= 24, R = 128 filling all 512 TMEM columns), ragged tiles, at a
     random point (no fallback): F and grad against the oracle."""
     I, J, K, R = dims
     P = synth.make_problem("c2", "cpu", dims=dims)
