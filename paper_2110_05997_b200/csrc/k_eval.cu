@@ -38,6 +38,21 @@ constexpr int kP3Unroll = TF_P3_UNROLL;   // Pi-form phase-3 k-loop unroll (deve
 #ifndef TF_PI_PRE_MAXNT
 #define TF_PI_PRE_MAXNT 0   // Pi pass: prescaled -A diag(c_k) rebuilt per slice up to this NT, else unscaled A in TMEM
 #endif
+#ifndef TF_P2_UNROLL
+#define TF_P2_UNROLL 8   // Pi-form phase-2 k-step loop unroll from TF_P2_UNROLL_MINNT r-tiles on (else full)
+#endif
+#ifndef TF_P2_UNROLL_MINNT
+// measured (tools/gpu_r02unr.sh): unroll 8 instead of 16 is 1.1% faster at NT = 13 (c5), 0.25% at NT = 15, 0.9%
+// slower at NT = 9; c4's NT = 7 1.1% slower (a smaller body helps once the fully unrolled slice exceeds ~15 KB)
+#define TF_P2_UNROLL_MINNT 13
+#endif
+#ifndef TF_P3_UNROLL_T
+#define TF_P3_UNROLL_T 16   // Pi-form phase-3 (tensor-memory) k-step loop unroll (development knob; even)
+#endif
+template <int NT>
+__host__ __device__ constexpr int p2_unroll() { return NT >= TF_P2_UNROLL_MINNT ? TF_P2_UNROLL : 16; }
+template <int NT>
+__host__ __device__ constexpr int p3_unroll() { return TF_P3_UNROLL_T; }
 #ifndef TF_TMEM_PIPE
 #define TF_TMEM_PIPE 1   // phase-3 tensor-memory loads one k-step ahead (c4 -1.7%, c5 -0.2%)
 #endif
@@ -173,6 +188,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, eval_min_blocks<NT, REC
   // phase 2 stays, s-outer there was 0.4% slower at c3)
   constexpr bool kP2SOuter = TF_P2_SOUTER && !RECON && !kPre && !kTmemB;
   constexpr int NT4 = 4 * ((NT + 3) / 4);
+  constexpr int kP2U = p2_unroll<NT>(), kP3U = p3_unroll<NT>();
   // tensor-memory columns: 16 k-steps x NT4 (phase-3 A) or NT x 16 (phase-2 B) doubles per lane, 2 columns each,
   // rounded up to a power of two (small R leaves room for a co-resident CTA's allocation)
   constexpr int kTmemNeed = kTmemB ? 32 * NT : 32 * NT4;
@@ -659,7 +675,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, eval_min_blocks<NT, REC
         double af[2][NT];
         tmem_ld_doubles<NT>(ta, af[0]);
         tmem_wait_ld();
-#pragma unroll
+#pragma unroll kP3U
         for (int s = 0; s < kBI / 4; ++s) {
           if (s + 1 < kBI / 4) tmem_ld_doubles<NT>(ta + 2 * (s + 1) * NT4, af[(s + 1) & 1]);
           const double bb = pe[4 * s];
@@ -703,7 +719,7 @@ __global__ void __launch_bounds__(EvalTile<BT>::THREADS, eval_min_blocks<NT, REC
       double Pt[NT][2];
 #pragma unroll
       for (int t = 0; t < NT; ++t) Pt[t][0] = Pt[t][1] = 0.0;
-#pragma unroll
+#pragma unroll kP2U
       for (int s = 0; s < kBJ / 4; ++s) {
         const double e = sT[(4 * s + q) * kLDE + 8 * warp + g];
         if (s & 1) fsum1 = fma(e, e, fsum1);   // sum t^2 of this slice tile (rows 8w.., all 64 columns)
